@@ -1,0 +1,164 @@
+/*
+ * pu_unwrap.h — C ABI of the B200-native L1 phase unwrapper (libpu_unwrap.so).
+ *
+ * Drop-in boundary for the hot path `phaseirls.unwrap` (reference
+ * pkg/src/phaseirls/irls.py:132-224).  The reference is pure Python; its
+ * only compiled seam is the numba kernel module rebound by
+ * `kernels.select_backend` (kernels.py:170-187).  Each entry point below
+ * replaces one reference function on that path (cited per function); the
+ * Python host (paper_2401_09961_b200/) mirrors irls.py / pcg.py above it.
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers owned by the caller.
+ *  - A "plane" is an N x M grid stored row-major with row pitch
+ *    pu_pitch(h) elements (dtype of the handle: float or double); pitch
+ *    padding must be zero-initialised by the caller.  A "system vector"
+ *    (reference SystemVector, operators.py:39-101) is 3 consecutive planes
+ *    [u | vv | vh]; vv's last row and vh's last column are zero pads.
+ *    Arc-shaped inputs (gv, gh, cv, ch, wv, wh, dv, dh) are planes with the
+ *    same pads.
+ *  - Scalar results are written as fp64 to caller-provided device memory.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  No entry
+ *    point synchronises unless documented.
+ *  - Return value: PU_OK or an error code; pu_last_error() describes it.
+ *    No C++ exception crosses the ABI.
+ */
+#ifndef PU_UNWRAP_H
+#define PU_UNWRAP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PU_ABI_VERSION 1
+
+enum pu_dtype { PU_F32 = 0, PU_F64 = 1 };
+
+enum pu_status {
+  PU_OK = 0,
+  PU_ERR_ARG = 1,          /* invalid argument (reference raises ValueError) */
+  PU_ERR_CUDA = 2,         /* CUDA runtime error */
+  PU_ERR_UNSUPPORTED = 3,  /* grid size outside the shared-memory FFT limits */
+  PU_ERR_NOMEM = 4
+};
+
+/* Device-side PCG control block (caller allocates pu_pcg_ctrl_bytes()).
+ * Mirrors pcg_solve's scalars and outcome (pcg.py:24-38, 47-116). */
+typedef struct pu_pcg_ctrl {
+  double rho, alpha, beta, thr, bnorm, pap, rn, mean_ru, rho_s;
+  int32_t done;        /* loop finished */
+  int32_t converged;   /* PcgOutcome.converged */
+  int32_t breakdown;   /* -1, or NumericalBreakdown.iteration */
+  int32_t bkind;       /* 0 initial residual, 1 p'Ap, 2 ||r||, 3 r.z */
+  int32_t iterations;  /* PcgOutcome.iterations = len(residual_norms) - 1 */
+  int32_t max_iters;
+  int32_t pad_[2];
+} pu_pcg_ctrl;
+
+typedef struct pu_handle pu_handle;
+
+int pu_abi_version(void);
+const char* pu_last_error(void);
+int pu_pcg_ctrl_bytes(void);
+/* Number of kernels this library has launched in the process so far. */
+int64_t pu_launch_count(void);
+
+/* Plan an N x M grid (FFT tables, launch shapes, reduction scratch).
+ * tau/delta: ModelParams (objective.py:30-41). */
+int pu_create(pu_handle** out, int n, int m, int dtype, double tau, double delta);
+int pu_destroy(pu_handle* h);
+int64_t pu_pitch(const pu_handle* h);
+int64_t pu_plane_elems(const pu_handle* h);
+/* Describe the launch plan (for logs): writes a NUL-terminated string. */
+int pu_describe(const pu_handle* h, char* buf, int cap);
+
+/* Layout helpers: compact fp64 (rows x cols, pitch lds) <-> plane. */
+int pu_pack(pu_handle* h, const double* src, int64_t lds, int rows, int cols, void* dst, void* stream);
+int pu_unpack(pu_handle* h, const void* src, int rows, int cols, double* dst, void* stream);
+int pu_fill(pu_handle* h, void* dst, int nplanes, double value, void* stream);
+int pu_copy(pu_handle* h, const void* src, void* dst, int nplanes, void* stream);
+
+/* phase.py:140-149 wrapped_gradients (+ wrap_to_principal phase.py:118-137,
+ * kernels.diff_rows/diff_cols kernels.py:87-103).  x: fp64 N x M, pitch ldx.
+ * Bit-identical to the reference in fp64. lo must be 0 or -pi. */
+int pu_wrapped_gradients(pu_handle* h, const double* x, int64_t ldx, void* gv, void* gh, double lo,
+                         void* stream);
+
+/* irls.py:167 initial state x = (0, -gv, -gh). */
+int pu_init_state(pu_handle* h, const void* gv, const void* gh, void* x, void* stream);
+
+/* operators.py:156-162 build_rhs. b: system vector. */
+int pu_build_rhs(pu_handle* h, const void* gv, const void* gh, void* b, void* stream);
+
+/* operators.py:138-153 apply_system (= kernels.apply_system_blocks,
+ * kernels.py:125-145). y = A(d) x. */
+int pu_apply_system(pu_handle* h, const void* x, const void* dv, const void* dh, void* y, void* stream);
+
+/* operators.py:70-75 SystemVector.dot over nplanes planes (1 or 3). */
+int pu_dot(pu_handle* h, const void* a, const void* b, int nplanes, double* out, void* stream);
+
+/* preconditioner.py:86-100 sylvester_solve on one plane (u block): z = the
+ * Neumann-Poisson pseudo-inverse of tau * r via DCT-II/III.  spec: one plane
+ * of scratch.  r and z may alias. */
+int pu_sylvester_solve(pu_handle* h, const void* r, void* z, void* spec, void* stream);
+
+/* preconditioner.py:103-115 apply_preconditioner (block diagonal D^+). */
+int pu_apply_preconditioner(pu_handle* h, const void* r, const void* dv, const void* dh, void* z, void* spec,
+                            void* stream);
+
+/* objective.py:92-100 update_weights + irls.py:191 (d = c^2 / w) and the
+ * H_delta pair of irls.py:176-177: out[0] = H(x, w_prev) (if wpv != NULL),
+ * out[1] = H(x, w). */
+int pu_weights_hpair(pu_handle* h, const void* x, const void* cv, const void* ch, const void* gv,
+                     const void* gh, const void* wpv, const void* wph, void* wv, void* wh, void* dv, void* dh,
+                     double* out, void* stream);
+
+/* objective.py:77-89 eval_h_delta. out[0] = H_delta(x, w). */
+int pu_eval_h_delta(pu_handle* h, const void* x, const void* wv, const void* wh, const void* gv,
+                    const void* gh, const void* cv, const void* ch, double* out, void* stream);
+
+/* objective.py:63-66 eval_f. out[0] = F, out[1] = weighted L1 part. */
+int pu_eval_f(pu_handle* h, const void* x, const void* gv, const void* gh, const void* cv, const void* ch,
+              double* out, void* stream);
+
+/* objective.py:118-125 candidate_step with stepsize 1/lipschitz. */
+int pu_candidate_step(pu_handle* h, const void* x, const void* wv, const void* wh, const void* gv,
+                      const void* gh, const void* cv, const void* ch, double lipschitz, void* out, void* stream);
+
+/* irls.py:202-205: out[0] = H(xa, w), out[1] = H(xb, w),
+ * out[2] = mean(u) of the accepted state, out[3] = 1.0 if xa is accepted. */
+int pu_hpair_states(pu_handle* h, const void* xa, const void* xb, const void* wv, const void* wh,
+                    const void* gv, const void* gh, const void* cv, const void* ch, double* out, void* stream);
+
+/* irls.py:206-215: dst = (sel[1] ? xa : xb) with u -= sel[0];
+ * out[0] = H(dst, w).  dst must not alias xa or xb. */
+int pu_accept_center(pu_handle* h, const void* xa, const void* xb, const double* sel, void* dst,
+                     const void* wv, const void* wh, const void* gv, const void* gh, const void* cv,
+                     const void* ch, double* out, void* stream);
+
+/* pcg.py:47-116 pcg_solve with apply_system and apply_preconditioner fused
+ * in (4 kernels per iteration).  x = x0 on entry; x0 is not modified.
+ * r, z, p0, p1: system-vector scratch; spec: one plane.  ctrl: device
+ * pu_pcg_ctrl; res_norms: device fp64 [max_iters + 1].  Enqueues without
+ * synchronising when max_iters <= 64; longer budgets poll ctrl->done
+ * every 64 iterations. */
+int pu_pcg_solve(pu_handle* h, const void* b, const void* x0, void* x, const void* dv, const void* dh,
+                 void* r, void* z, void* p0, void* p1, void* spec, int max_iters, double rel_tol,
+                 void* ctrl, double* res_norms, void* stream);
+
+/* Per-launch CUDA-event timing on the launching stream (off by default).
+ * pu_timing_read synchronises on the recorded events and returns the number
+ * of records (kind, iteration, milliseconds) written, up to cap; kinds:
+ * 0 pcg_start, 1 K1 (p, Ap, p'Ap), 2 K2 (x, r, z_s, row DCT-II), 3 K3
+ * (column DCT pair), 4 K4 (row DCT-III), 5 reprojection update, 6 weights,
+ * 7 candidate, 8 H pair, 9 accept.  Iteration -1 = PCG setup / outer kernel. */
+int pu_timing_enable(pu_handle* h, int on);
+int pu_timing_read(pu_handle* h, int* kinds, int* its, float* ms, int cap);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PU_UNWRAP_H */

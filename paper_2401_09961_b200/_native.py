@@ -1,0 +1,105 @@
+"""ctypes binding of libpu_unwrap.so (include/pu_unwrap.h).
+
+There is no fallback: if the shared library is missing, or no CUDA device is
+visible, every entry point raises.  `ensure()` is the single gate.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libpu_unwrap.so")
+
+PU_F32, PU_F64 = 0, 1
+PU_OK, PU_ERR_ARG, PU_ERR_CUDA, PU_ERR_UNSUPPORTED, PU_ERR_NOMEM = 0, 1, 2, 3, 4
+
+_vp, _i, _d, _i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int64
+
+# name -> (restype, argtypes); mirrors include/pu_unwrap.h
+SIGNATURES = {
+    "pu_abi_version": (_i, []),
+    "pu_last_error": (ctypes.c_char_p, []),
+    "pu_pcg_ctrl_bytes": (_i, []),
+    "pu_launch_count": (_i64, []),
+    "pu_create": (_i, [ctypes.POINTER(_vp), _i, _i, _i, _d, _d]),
+    "pu_destroy": (_i, [_vp]),
+    "pu_pitch": (_i64, [_vp]),
+    "pu_plane_elems": (_i64, [_vp]),
+    "pu_describe": (_i, [_vp, ctypes.c_char_p, _i]),
+    "pu_pack": (_i, [_vp, _vp, _i64, _i, _i, _vp, _vp]),
+    "pu_unpack": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
+    "pu_fill": (_i, [_vp, _vp, _i, _d, _vp]),
+    "pu_copy": (_i, [_vp, _vp, _vp, _i, _vp]),
+    "pu_init_state": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "pu_wrapped_gradients": (_i, [_vp, _vp, _i64, _vp, _vp, _d, _vp]),
+    "pu_build_rhs": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "pu_apply_system": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "pu_dot": (_i, [_vp, _vp, _vp, _i, _vp, _vp]),
+    "pu_sylvester_solve": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "pu_apply_preconditioner": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pu_weights_hpair": (_i, [_vp] + [_vp] * 11 + [_vp, _vp]),
+    "pu_eval_h_delta": (_i, [_vp] + [_vp] * 7 + [_vp, _vp]),
+    "pu_eval_f": (_i, [_vp] + [_vp] * 5 + [_vp, _vp]),
+    "pu_candidate_step": (_i, [_vp] + [_vp] * 7 + [_d, _vp, _vp]),
+    "pu_hpair_states": (_i, [_vp] + [_vp] * 8 + [_vp, _vp]),
+    "pu_accept_center": (_i, [_vp] + [_vp] * 10 + [_vp, _vp]),
+    "pu_pcg_solve": (_i, [_vp] + [_vp] * 10 + [_i, _d, _vp, _vp, _vp]),
+    "pu_timing_enable": (_i, [_vp, _i]),
+    "pu_timing_read": (_i, [_vp, _vp, _vp, _vp, _i]),
+}
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    """A CUDA-side failure reported through the C ABI."""
+
+
+def load():
+    """Load the shared library (no GPU needed); raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} not found: build it with `python -m paper_2401_09961_b200.build_ext` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.pu_abi_version() != 1:
+        raise ImportError("libpu_unwrap.so ABI version mismatch; rebuild it")
+    _lib = lib
+    return lib
+
+
+def ensure():
+    """Library loaded AND a CUDA device present — the product path's gate."""
+    lib = load()
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2401_09961_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+    return lib
+
+
+def check(rc):
+    if rc == PU_OK:
+        return
+    msg = _lib.pu_last_error().decode() if _lib is not None else "unknown"
+    if rc == PU_ERR_ARG:
+        raise ValueError(msg)
+    if rc == PU_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise NativeError(f"libpu_unwrap error {rc}: {msg}")
+
+
+def call(name, *args):
+    check(getattr(_lib, name)(*args))
+
+
+def exported_symbols():
+    return sorted(SIGNATURES)

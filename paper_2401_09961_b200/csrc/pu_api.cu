@@ -1,0 +1,704 @@
+// Host side of libpu_unwrap.so: FFT/DCT plans, launch shapes, the PCG
+// enqueue loop and the extern "C" entry points declared in include/pu_unwrap.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pu_dct_launch.cuh"
+
+namespace pu {
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define PU_CUDA(call)                                                                       \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) return fail(PU_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// process-wide count of kernels launched through this library (bench.py reports it)
+static std::atomic<long long> g_launches{0};
+
+#define PU_LAUNCH_CHECK()                                                                   \
+  do {                                                                                      \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                                     \
+    cudaError_t e_ = cudaGetLastError();                                                    \
+    if (e_ != cudaSuccess) return fail(PU_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define PU_DCT(call)                                       \
+  do {                                                     \
+    g_launches.fetch_add(1, std::memory_order_relaxed);    \
+    PU_CUDA(call);                                         \
+  } while (0)
+
+enum Site { S_DOT = 0, S_WH, S_EVH, S_HPAIR, S_ACC, S_EVF, S_START, S_K1, S_K2, S_K3, S_UPD, S_NSITES };
+
+typedef long double ld_t;
+static const ld_t kPi = 3.141592653589793238462643383279502884L;
+
+// ---------------------------------------------------------------------------
+// Plans
+// ---------------------------------------------------------------------------
+static void host_fft_pow2(std::vector<std::complex<ld_t>>& a) {
+  const size_t n = a.size();
+  for (size_t i = 1, j = 0; i < n; ++i) {
+    size_t bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(a[i], a[j]);
+  }
+  for (size_t len = 2; len <= n; len <<= 1) {
+    for (size_t i = 0; i < n; i += len)
+      for (size_t k = 0; k < len / 2; ++k) {
+        const ld_t ang = -2.0L * kPi * (ld_t)k / (ld_t)len;
+        const std::complex<ld_t> w(cosl(ang), sinl(ang));
+        const std::complex<ld_t> u = a[i + k], v = a[i + k + len / 2] * w;
+        a[i + k] = u + v;
+        a[i + k + len / 2] = u - v;
+      }
+  }
+}
+
+static bool factor_smooth(int n, int emax, std::vector<int>& rad) {
+  rad.clear();
+  int r = n;
+  int p2 = 0;
+  while (r % 2 == 0) { r /= 2; ++p2; }
+  const int big = emax >= 16 ? 4 : 3;  // log2 of the largest power-of-two radix
+  while (p2 >= big) { rad.push_back(1 << big); p2 -= big; }
+  if (p2 > 0) rad.push_back(1 << p2);
+  for (int p : {3, 5, 7}) while (r % p == 0) { rad.push_back(p); r /= p; }
+  return r == 1;
+}
+
+template <typename T>
+struct HostPlan {
+  FftPlan<T> dev{};
+  std::vector<void*> allocs;
+  int seq_capacity = 0;  // min over stages of R * floor(EMAX/R)
+  int emax = 0;
+
+  int build(int n) {
+    emax = sizeof(T) == 4 ? 16 : 8;
+    std::memset(&dev, 0, sizeof(dev));
+    dev.n = n;
+    std::vector<int> rad;
+    int L = n;
+    bool blue = !factor_smooth(n, emax, rad);
+    if (blue) {
+      L = 1;
+      while (L < 2 * n - 1) L <<= 1;
+      factor_smooth(L, emax, rad);
+    }
+    if ((int)rad.size() > PU_FFT_MAX_STAGES) return fail(PU_ERR_UNSUPPORTED, "too many FFT stages");
+    dev.L = L;
+    dev.bluestein = blue ? 1 : 0;
+    dev.nst = (int)rad.size();
+    seq_capacity = emax;
+    std::sort(rad.begin(), rad.end());  // the radix with Q > 1 runs first, twiddle-free
+    for (size_t s = 0; s < rad.size(); ++s) {
+      dev.rad[s] = rad[s];
+      seq_capacity = std::min(seq_capacity, rad[s] * (emax / rad[s]));
+    }
+    dev.cap = seq_capacity;
+    dev.ldseq = ldseq_for(L);  // spad(L-1) + 1 (+ pad), kept even for 16-byte alignment
+    using C = cplx<T>;
+    std::vector<C> tw(L), dctw(n), chirp(n), filt(L);
+    std::vector<T> scale(n);
+    std::vector<double> lam(n);
+    for (int k = 0; k < L; ++k) {
+      const ld_t a = -2.0L * kPi * (ld_t)k / (ld_t)L;
+      tw[k].x = (T)cosl(a); tw[k].y = (T)sinl(a);
+    }
+    for (int k = 0; k < n; ++k) {
+      const ld_t a = kPi * (ld_t)k / (2.0L * (ld_t)n);
+      dctw[k].x = (T)cosl(a); dctw[k].y = (T)sinl(a);
+      scale[k] = (T)sqrtl((k == 0 ? 1.0L : 2.0L) / (ld_t)n);
+      const ld_t sh = sinl(a);
+      lam[k] = (double)(4.0L * sh * sh);  // 2 - 2 cos(pi k / n), cancellation-free
+    }
+    lam[0] = 0.0;
+    if (blue) {
+      std::vector<std::complex<ld_t>> h(L, std::complex<ld_t>(0, 0));
+      for (int k = 0; k < n; ++k) {
+        const long long q = ((long long)k * k) % (2LL * n);
+        const ld_t a = -kPi * (ld_t)q / (ld_t)n;
+        chirp[k].x = (T)cosl(a); chirp[k].y = (T)sinl(a);
+        const std::complex<ld_t> b(cosl(-a), sinl(-a));  // conj(chirp)
+        h[k] = b;
+        if (k > 0) h[L - k] = b;
+      }
+      host_fft_pow2(h);
+      for (int k = 0; k < L; ++k) {
+        filt[k].x = (T)(h[k].real() / (ld_t)L);
+        filt[k].y = (T)(h[k].imag() / (ld_t)L);
+      }
+    }
+    int rc;
+    if ((rc = upload(tw, &dev.tw)) || (rc = upload(dctw, &dev.dctw)) || (rc = upload(scale, &dev.scale)) ||
+        (rc = upload(lam, &dev.lam)))
+      return rc;
+    if (blue && ((rc = upload(chirp, &dev.chirp)) || (rc = upload(filt, &dev.filt)))) return rc;
+    return PU_OK;
+  }
+
+  template <typename V, typename P>
+  int upload(const std::vector<V>& v, const P** dst) {
+    void* p = nullptr;
+    PU_CUDA(cudaMalloc(&p, std::max<size_t>(1, v.size()) * sizeof(V)));
+    allocs.push_back(p);
+    PU_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(V), cudaMemcpyHostToDevice));
+    *dst = reinterpret_cast<const P*>(p);
+    return PU_OK;
+  }
+
+  void release() {
+    for (void* p : allocs) cudaFree(p);
+    allocs.clear();
+  }
+
+  // threads for `nseq` sequences: at least one whole sequence per stage,
+  // at most the instantiation's launch bound (larger groups run sequentially)
+  int max_threads() const {
+    const bool stat = (dev.L & (dev.L - 1)) == 0 && dev.L >= 512 && dev.L <= (emax == 16 ? 16384 : 8192);
+    return fft_max_threads(stat ? dev.L : 0, emax);
+  }
+  int threads_for(int nseq) const {
+    const long long need = ((long long)nseq * dev.L + seq_capacity - 1) / seq_capacity;
+    long long t = ((need + 31) / 32) * 32;
+    t = std::min<long long>(t, max_threads());
+    const long long one = ((dev.L + seq_capacity - 1) / seq_capacity + 31) / 32 * 32;
+    return (int)std::max<long long>(std::max<long long>(t, one), 64);
+  }
+  size_t smem_for(int nseq) const { return (size_t)nseq * dev.ldseq * sizeof(cplx<T>); }
+};
+
+template <typename T>
+struct DctOps {
+  cudaError_t (*set_attrs)(size_t, size_t);
+  decltype(&DctLaunch<T, 0>::rows_plain) rows_plain;
+  decltype(&DctLaunch<T, 0>::rows_init) rows_init;
+  decltype(&DctLaunch<T, 0>::rows_update) rows_update;
+  decltype(&DctLaunch<T, 0>::rows_submean) rows_submean;
+  decltype(&DctLaunch<T, 0>::rows_inv) rows_inv;
+  decltype(&DctLaunch<T, 0>::cols) cols;
+  int ls;
+};
+
+template <typename T, int LS>
+static DctOps<T> make_ops() {
+  using D = DctLaunch<T, LS>;
+  return DctOps<T>{&D::set_attrs, &D::rows_plain, &D::rows_init, &D::rows_update, &D::rows_submean,
+                   &D::rows_inv, &D::cols, LS};
+}
+
+template <typename T>
+static DctOps<T> ops_for(int L) {
+  switch (L) {
+    case 512: return make_ops<T, 512>();
+    case 1024: return make_ops<T, 1024>();
+    case 2048: return make_ops<T, 2048>();
+    case 4096: return make_ops<T, 4096>();
+    case 8192: return make_ops<T, 8192>();
+    default: break;
+  }
+  if constexpr (sizeof(T) == 4) {
+    if (L == 16384) return make_ops<T, 16384>();
+  }
+  return make_ops<T, 0>();
+}
+
+// Optional per-launch CUDA-event timing (bench.py's roofline numbers are
+// taken from these, on the launching stream).
+struct Timer {
+  bool on = false;
+  struct Rec { int kind, it; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    cudaEvent_t e = nullptr;
+    if (!pool.empty()) { e = pool.back(); pool.pop_back(); }
+    else cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t begin(cudaStream_t st) {
+    if (!on) return nullptr;
+    cudaEvent_t a = get();
+    cudaEventRecord(a, st);
+    return a;
+  }
+  void end(cudaStream_t st, cudaEvent_t a, int kind, int it) {
+    if (!on || !a) return;
+    cudaEvent_t b = get();
+    cudaEventRecord(b, st);
+    recs.push_back(Rec{kind, it, a, b});
+  }
+  int read(int* kinds, int* its, float* ms, int cap) {
+    int n = 0;
+    for (auto& r : recs) {
+      float t = 0.f;
+      cudaEventSynchronize(r.b);
+      cudaEventElapsedTime(&t, r.a, r.b);
+      if (n < cap) { kinds[n] = r.kind; its[n] = r.it; ms[n] = t; }
+      ++n;
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    recs.clear();
+    return std::min(n, cap);
+  }
+  ~Timer() {
+    for (auto& r : recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+enum TimeKind { TK_START = 0, TK_K1, TK_K2, TK_K3, TK_K4, TK_UPD, TK_WEIGHTS, TK_CAND, TK_HPAIR, TK_ACCEPT, TK_OTHER };
+
+static const size_t kSmemLimit = 227 * 1024 - 4096;  // leave room for static reduction scratch
+
+// ---------------------------------------------------------------------------
+// Handle
+// ---------------------------------------------------------------------------
+struct HandleBase {
+  virtual ~HandleBase() {}
+};
+
+template <typename T>
+struct Impl : HandleBase {
+  Grid g{};
+  HostPlan<T> prow, pcol;  // row transforms (length m), column transforms (length n)
+  int rows_per_cta = 2, row_threads = 64;
+  int cols_per_cta = 2, col_threads = 64;
+  size_t row_smem = 0, col_smem = 0;
+  int ew_grid = 1, ew_threads = 32;
+  RedScratch rs{};
+  int* pinned_done = nullptr;
+  DctOps<T> rops{}, cops{};  // transform kernels for the row / column internal lengths
+  Timer tm;
+
+  ~Impl() override {
+    prow.release();
+    pcol.release();
+    if (rs.partials) cudaFree(rs.partials);
+    if (rs.ticket) cudaFree(rs.ticket);
+    if (pinned_done) cudaFreeHost(pinned_done);
+  }
+
+  int init(int n, int m, double tau, double delta) {
+    g.n = n; g.m = m;
+    g.ld = ((long long)m + 7) / 8 * 8;
+    g.plane = (long long)n * g.ld;
+    g.tau = tau; g.inv_tau = 1.0 / tau; g.delta = delta;
+    int rc;
+    if ((rc = prow.build(m)) || (rc = pcol.build(n))) return rc;
+    // row kernels: aim for ~8K (f32) / 4K (f64) complex per CTA but keep >= ~2 CTAs per SM
+    const int target = sizeof(T) == 4 ? 8192 : 4096;
+    const int seqs_total = (n + 1) / 2;
+    int c = std::max(1, target / prow.dev.L);
+    c = std::min(c, std::max(1, seqs_total / (2 * 148)));
+    while (c > 1 && (prow.threads_for(c) > prow.max_threads() || prow.smem_for(c) > kSmemLimit)) --c;
+    if (prow.threads_for(c) > prow.max_threads() || prow.smem_for(c) > kSmemLimit)
+      return fail(PU_ERR_UNSUPPORTED, "row length " + std::to_string(m) + " exceeds the shared-memory FFT limit");
+    rows_per_cta = 2 * c;
+    row_threads = prow.threads_for(c);
+    row_smem = prow.smem_for(c);
+    // column kernels: panel of W = 2c columns; prefer 32-byte row segments
+    int cc = sizeof(T) == 4 ? 4 : 2;
+    cc = std::min(cc, std::max(1, (m + 1) / 2));
+    while (cc > 1 && (pcol.threads_for(cc) > pcol.max_threads() || pcol.smem_for(cc) > kSmemLimit)) --cc;
+    if (pcol.threads_for(cc) > pcol.max_threads() || pcol.smem_for(cc) > kSmemLimit)
+      return fail(PU_ERR_UNSUPPORTED, "column length " + std::to_string(n) + " exceeds the shared-memory FFT limit");
+    cols_per_cta = 2 * cc;
+    col_threads = pcol.threads_for(cc);
+    col_smem = pcol.smem_for(cc);
+    // element-wise kernels: block-strided rows, thread-strided columns
+    ew_threads = std::min(256, std::max(32, (m + 31) / 32 * 32));
+    ew_grid = std::min(n, 148 * 8);
+    rs.stride = std::max(std::max(ew_grid, (n + rows_per_cta - 1) / rows_per_cta),
+                         (m + cols_per_cta - 1) / cols_per_cta) + 1;
+    PU_CUDA(cudaMalloc(&rs.partials, sizeof(double) * PU_MAX_SUMS * rs.stride));
+    PU_CUDA(cudaMalloc(&rs.ticket, sizeof(unsigned int) * 32));
+    PU_CUDA(cudaMemset(rs.ticket, 0, sizeof(unsigned int) * 32));
+    PU_CUDA(cudaMallocHost(&pinned_done, sizeof(int)));
+    return set_smem_attrs();
+  }
+
+  static constexpr int EM = sizeof(T) == 4 ? 16 : 8;
+
+  int set_smem_attrs() {
+    rops = ops_for<T>(prow.dev.L);
+    cops = ops_for<T>(pcol.dev.L);
+    // the attribute is per kernel (process-wide): always raise it to the cap so
+    // that handles of different sizes sharing an instantiation never shrink it
+    PU_CUDA(rops.set_attrs(kSmemLimit, kSmemLimit));
+    PU_CUDA(cops.set_attrs(kSmemLimit, kSmemLimit));
+    return PU_OK;
+  }
+
+  XLaunch rl(cudaStream_t st) const { return XLaunch{row_grid(), row_threads, row_smem, st}; }
+  XLaunch cl(cudaStream_t st) const { return XLaunch{col_grid(), col_threads, col_smem, st}; }
+
+  int row_grid() const { return (g.n + rows_per_cta - 1) / rows_per_cta; }
+  int col_grid() const { return (g.m + cols_per_cta - 1) / cols_per_cta; }
+
+  // ---- preconditioner passes ----
+  int sylvester(const T* r, T* z, T* spec, cudaStream_t st) {
+    PU_DCT(rops.rows_plain(rl(st), g, prow.dev, rows_per_cta, r, spec, rs, S_K2));
+    PU_DCT(cops.cols(MODE_API, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, nullptr, rs, S_K3, 0));
+    PU_DCT(rops.rows_inv(rl(st), g, prow.dev, rows_per_cta, spec, z, nullptr));
+    return PU_OK;
+  }
+
+  int pcg(const T* b, const T* x0, T* x, const T* dv, const T* dh, T* r, T* z, T* p0, T* p1, T* spec,
+          int max_iters, double rel_tol, PcgCtrl* ctrl, double* norms, cudaStream_t st) {
+    cudaEvent_t e = tm.begin(st);
+    k_pcg_start<T><<<ew_grid, ew_threads, 0, st>>>(g, b, x0, x, r, dv, dh, ctrl, norms, rel_tol, max_iters, rs,
+                                                   S_START);
+    PU_LAUNCH_CHECK();
+    tm.end(st, e, TK_START, -1);
+    {
+      RowsPcg<T, false, false, MODE_INIT> pol{nullptr, x, r, z, dv, dh, ctrl, norms, -1};
+      e = tm.begin(st);
+      PU_DCT(rops.rows_init(rl(st), g, prow.dev, rows_per_cta, spec, pol, rs, S_K2));
+      tm.end(st, e, TK_K2, -1);
+      e = tm.begin(st);
+      PU_DCT(cops.cols(MODE_INIT, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, ctrl, rs, S_K3, -1));
+      tm.end(st, e, TK_K3, -1);
+      e = tm.begin(st);
+      PU_DCT(rops.rows_inv(rl(st), g, prow.dev, rows_per_cta, spec, z, ctrl));
+      tm.end(st, e, TK_K4, -1);
+    }
+    T* pbuf[2] = {p0, p1};
+    const int chunk = 64;
+    for (int it = 0; it < max_iters; ++it) {
+      if (it > 0 && it % chunk == 0) {
+        PU_CUDA(cudaMemcpyAsync(pinned_done, &ctrl->done, sizeof(int), cudaMemcpyDeviceToHost, st));
+        PU_CUDA(cudaStreamSynchronize(st));
+        if (*pinned_done) break;
+      }
+      T* pn = pbuf[it & 1];
+      const T* po = pbuf[(it + 1) & 1];
+      e = tm.begin(st);
+      k_pcg_p<T><<<ew_grid, ew_threads, 0, st>>>(g, z, po, pn, dv, dh, ctrl, rs, S_K1, it);
+      PU_LAUNCH_CHECK();
+      tm.end(st, e, TK_K1, it);
+      if ((it + 1) % 50 == 0) {
+        e = tm.begin(st);
+        k_pcg_update_sum<T><<<ew_grid, ew_threads, 0, st>>>(g, pn, dv, dh, x, r, ctrl, rs, S_UPD);
+        PU_LAUNCH_CHECK();
+        tm.end(st, e, TK_UPD, it);
+        RowsPcg<T, false, true, MODE_ITER> pol{pn, x, r, z, dv, dh, ctrl, norms, it};
+        e = tm.begin(st);
+        PU_DCT(rops.rows_submean(rl(st), g, prow.dev, rows_per_cta, spec, pol, rs, S_K2));
+        tm.end(st, e, TK_K2, it);
+      } else {
+        RowsPcg<T, true, false, MODE_ITER> pol{pn, x, r, z, dv, dh, ctrl, norms, it};
+        e = tm.begin(st);
+        PU_DCT(rops.rows_update(rl(st), g, prow.dev, rows_per_cta, spec, pol, rs, S_K2));
+        tm.end(st, e, TK_K2, it);
+      }
+      e = tm.begin(st);
+      PU_DCT(cops.cols(MODE_ITER, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, ctrl, rs, S_K3, it));
+      tm.end(st, e, TK_K3, it);
+      e = tm.begin(st);
+      PU_DCT(rops.rows_inv(rl(st), g, prow.dev, rows_per_cta, spec, z, ctrl));
+      tm.end(st, e, TK_K4, it);
+    }
+    return PU_OK;
+  }
+};
+
+}  // namespace pu
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+using namespace pu;
+
+struct pu_handle {
+  int dtype;
+  Impl<float>* f = nullptr;
+  Impl<double>* d = nullptr;
+};
+
+#define PU_DISPATCH(h, ...)                            \
+  do {                                                 \
+    if (!(h)) return fail(PU_ERR_ARG, "null handle");  \
+    if ((h)->dtype == PU_F32) {                        \
+      using T = float;                                 \
+      auto& I = *(h)->f;                               \
+      __VA_ARGS__                                      \
+    } else {                                           \
+      using T = double;                                \
+      auto& I = *(h)->d;                               \
+      __VA_ARGS__                                      \
+    }                                                  \
+  } while (0)
+
+#define ST(s) reinterpret_cast<cudaStream_t>(s)
+#define CP(p) reinterpret_cast<const T*>(p)
+#define MP(p) reinterpret_cast<T*>(p)
+
+extern "C" {
+
+int pu_abi_version(void) { return PU_ABI_VERSION; }
+int64_t pu_launch_count(void) { return g_launches.load(); }
+const char* pu_last_error(void) { return g_last_error.c_str(); }
+int pu_pcg_ctrl_bytes(void) { return (int)sizeof(pu_pcg_ctrl); }
+
+int pu_create(pu_handle** out, int n, int m, int dtype, double tau, double delta) {
+  if (!out) return fail(PU_ERR_ARG, "null output");
+  *out = nullptr;
+  if (n < 1 || m < 1) return fail(PU_ERR_ARG, "grid dimensions must be >= 1");
+  if (!(tau > 0) || !std::isfinite(tau)) return fail(PU_ERR_ARG, "tau must be positive and finite");
+  if (!(delta > 0) || !std::isfinite(delta)) return fail(PU_ERR_ARG, "delta must be positive and finite");
+  if (dtype != PU_F32 && dtype != PU_F64) return fail(PU_ERR_ARG, "dtype must be PU_F32 or PU_F64");
+  pu_handle* h = new pu_handle();
+  h->dtype = dtype;
+  int rc;
+  if (dtype == PU_F32) {
+    h->f = new Impl<float>();
+    rc = h->f->init(n, m, tau, delta);
+  } else {
+    h->d = new Impl<double>();
+    rc = h->d->init(n, m, tau, delta);
+  }
+  if (rc != PU_OK) {
+    std::string keep = g_last_error;
+    delete h->f;
+    delete h->d;
+    delete h;
+    g_last_error = keep;
+    return rc;
+  }
+  *out = h;
+  return PU_OK;
+}
+
+int pu_destroy(pu_handle* h) {
+  if (!h) return PU_OK;
+  delete h->f;
+  delete h->d;
+  delete h;
+  return PU_OK;
+}
+
+int64_t pu_pitch(const pu_handle* h) { return h ? (h->dtype == PU_F32 ? h->f->g.ld : h->d->g.ld) : -1; }
+int64_t pu_plane_elems(const pu_handle* h) { return h ? (h->dtype == PU_F32 ? h->f->g.plane : h->d->g.plane) : -1; }
+
+int pu_describe(const pu_handle* h, char* buf, int cap) {
+  if (!h || !buf || cap < 1) return fail(PU_ERR_ARG, "bad arguments");
+  auto fmt = [&](auto& I) {
+    std::snprintf(buf, cap,
+                  "{\"n\":%d,\"m\":%d,\"ld\":%lld,\"dtype\":\"%s\",\"row_fft\":{\"n\":%d,\"L\":%d,\"bluestein\":%d,"
+                  "\"stages\":%d},\"col_fft\":{\"n\":%d,\"L\":%d,\"bluestein\":%d,\"stages\":%d},"
+                  "\"rows_per_cta\":%d,\"row_threads\":%d,\"row_smem\":%zu,\"cols_per_cta\":%d,"
+                  "\"col_threads\":%d,\"col_smem\":%zu,\"ew_grid\":%d,\"ew_threads\":%d}",
+                  I.g.n, I.g.m, I.g.ld, h->dtype == PU_F32 ? "f32" : "f64", I.prow.dev.n, I.prow.dev.L,
+                  I.prow.dev.bluestein, I.prow.dev.nst, I.pcol.dev.n, I.pcol.dev.L, I.pcol.dev.bluestein,
+                  I.pcol.dev.nst, I.rows_per_cta, I.row_threads, I.row_smem, I.cols_per_cta, I.col_threads,
+                  I.col_smem, I.ew_grid, I.ew_threads);
+  };
+  if (h->dtype == PU_F32) fmt(*h->f); else fmt(*h->d);
+  return PU_OK;
+}
+
+int pu_pack(pu_handle* h, const double* src, int64_t lds, int rows, int cols, void* dst, void* stream) {
+  PU_DISPATCH(h, {
+    k_pack<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, src, lds, rows, cols, MP(dst));
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
+int pu_unpack(pu_handle* h, const void* src, int rows, int cols, double* dst, void* stream) {
+  PU_DISPATCH(h, {
+    if (rows > 0 && cols > 0) {
+      k_unpack<T><<<std::min(rows, 148 * 8), I.ew_threads, 0, ST(stream)>>>(I.g, CP(src), rows, cols, dst);
+      PU_LAUNCH_CHECK();
+    }
+  });
+  return PU_OK;
+}
+
+int pu_fill(pu_handle* h, void* dst, int nplanes, double value, void* stream) {
+  PU_DISPATCH(h, {
+    k_fill<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, MP(dst), nplanes, (T)value);
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
+int pu_copy(pu_handle* h, const void* src, void* dst, int nplanes, void* stream) {
+  PU_DISPATCH(h, {
+    k_copy<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(src), MP(dst), nplanes);
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
+int pu_wrapped_gradients(pu_handle* h, const double* x, int64_t ldx, void* gv, void* gh, double lo, void* stream) {
+  if (!(lo == 0.0 || lo == -3.141592653589793)) return fail(PU_ERR_ARG, "lo must be 0 or -pi");
+  PU_DISPATCH(h, {
+    k_grad<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, x, ldx, MP(gv), MP(gh), lo);
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
+int pu_init_state(pu_handle* h, const void* gv, const void* gh, void* x, void* stream) {
+  PU_DISPATCH(h, {
+    k_init_state<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(gv), CP(gh), MP(x));
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
+int pu_build_rhs(pu_handle* h, const void* gv, const void* gh, void* b, void* stream) {
+  PU_DISPATCH(h, {
+    k_rhs<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(gv), CP(gh), MP(b));
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
+int pu_apply_system(pu_handle* h, const void* x, const void* dv, const void* dh, void* y, void* stream) {
+  PU_DISPATCH(h, {
+    k_apply_system<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(x), CP(dv), CP(dh), MP(y));
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
+int pu_dot(pu_handle* h, const void* a, const void* b, int nplanes, double* out, void* stream) {
+  if (nplanes < 1 || nplanes > 3) return fail(PU_ERR_ARG, "nplanes must be 1..3");
+  PU_DISPATCH(h, {
+    k_dot<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(a), CP(b), nplanes, I.rs, S_DOT, out);
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
+int pu_sylvester_solve(pu_handle* h, const void* r, void* z, void* spec, void* stream) {
+  PU_DISPATCH(h, { return I.sylvester(CP(r), MP(z), MP(spec), ST(stream)); });
+}
+
+int pu_apply_preconditioner(pu_handle* h, const void* r, const void* dv, const void* dh, void* z, void* spec,
+                            void* stream) {
+  PU_DISPATCH(h, {
+    k_precond_slack<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(r), CP(dv), CP(dh), MP(z));
+    PU_LAUNCH_CHECK();
+    return I.sylvester(CP(r), MP(z), MP(spec), ST(stream));
+  });
+}
+
+int pu_weights_hpair(pu_handle* h, const void* x, const void* cv, const void* ch, const void* gv, const void* gh,
+                     const void* wpv, const void* wph, void* wv, void* wh, void* dv, void* dh, double* out,
+                     void* stream) {
+  PU_DISPATCH(h, {
+    cudaEvent_t te_ = I.tm.begin(ST(stream));
+    k_weights_hpair<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(x), CP(cv), CP(ch), CP(gv), CP(gh),
+                                                                  CP(wpv), CP(wph), MP(wv), MP(wh), MP(dv), MP(dh),
+                                                                  I.rs, S_WH, out);
+    PU_LAUNCH_CHECK();
+    I.tm.end(ST(stream), te_, TK_WEIGHTS, -1);
+  });
+  return PU_OK;
+}
+
+int pu_eval_h_delta(pu_handle* h, const void* x, const void* wv, const void* wh, const void* gv, const void* gh,
+                    const void* cv, const void* ch, double* out, void* stream) {
+  PU_DISPATCH(h, {
+    k_eval_h<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(x), CP(wv), CP(wh), CP(gv), CP(gh), CP(cv),
+                                                           CP(ch), I.rs, S_EVH, out);
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
+int pu_eval_f(pu_handle* h, const void* x, const void* gv, const void* gh, const void* cv, const void* ch,
+              double* out, void* stream) {
+  PU_DISPATCH(h, {
+    k_eval_f<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(x), CP(gv), CP(gh), CP(cv), CP(ch), I.rs,
+                                                           S_EVF, out);
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
+int pu_candidate_step(pu_handle* h, const void* x, const void* wv, const void* wh, const void* gv, const void* gh,
+                      const void* cv, const void* ch, double lipschitz, void* out, void* stream) {
+  if (!(lipschitz > 0)) return fail(PU_ERR_ARG, "lipschitz constant must be positive");
+  PU_DISPATCH(h, {
+    cudaEvent_t te_ = I.tm.begin(ST(stream));
+    k_candidate<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(x), CP(wv), CP(wh), CP(gv), CP(gh), CP(cv),
+                                                              CP(ch), (T)(-1.0 / lipschitz), MP(out));
+    PU_LAUNCH_CHECK();
+    I.tm.end(ST(stream), te_, TK_CAND, -1);
+  });
+  return PU_OK;
+}
+
+int pu_hpair_states(pu_handle* h, const void* xa, const void* xb, const void* wv, const void* wh, const void* gv,
+                    const void* gh, const void* cv, const void* ch, double* out, void* stream) {
+  PU_DISPATCH(h, {
+    cudaEvent_t te_ = I.tm.begin(ST(stream));
+    k_hpair_states<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(xa), CP(xb), CP(wv), CP(wh), CP(gv),
+                                                                 CP(gh), CP(cv), CP(ch), I.rs, S_HPAIR, out);
+    PU_LAUNCH_CHECK();
+    I.tm.end(ST(stream), te_, TK_HPAIR, -1);
+  });
+  return PU_OK;
+}
+
+int pu_accept_center(pu_handle* h, const void* xa, const void* xb, const double* sel, void* dst, const void* wv,
+                     const void* wh, const void* gv, const void* gh, const void* cv, const void* ch, double* out,
+                     void* stream) {
+  if (dst == xa || dst == xb) return fail(PU_ERR_ARG, "dst must not alias xa or xb");
+  PU_DISPATCH(h, {
+    cudaEvent_t te_ = I.tm.begin(ST(stream));
+    k_accept<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(xa), CP(xb), sel, MP(dst), CP(wv), CP(wh),
+                                                           CP(gv), CP(gh), CP(cv), CP(ch), I.rs, S_ACC, out);
+    PU_LAUNCH_CHECK();
+    I.tm.end(ST(stream), te_, TK_ACCEPT, -1);
+  });
+  return PU_OK;
+}
+
+int pu_timing_enable(pu_handle* h, int on) {
+  PU_DISPATCH(h, { I.tm.on = on != 0; });
+  return PU_OK;
+}
+
+int pu_timing_read(pu_handle* h, int* kinds, int* its, float* ms, int cap) {
+  if (!kinds || !its || !ms || cap < 0) return -1;
+  PU_DISPATCH(h, { return I.tm.read(kinds, its, ms, cap); });
+}
+
+int pu_pcg_solve(pu_handle* h, const void* b, const void* x0, void* x, const void* dv, const void* dh, void* r,
+                 void* z, void* p0, void* p1, void* spec, int max_iters, double rel_tol, void* ctrl, double* res_norms,
+                 void* stream) {
+  if (max_iters < 0) return fail(PU_ERR_ARG, "max_iters must be >= 0");
+  if (rel_tol < 0) return fail(PU_ERR_ARG, "rel_tol must be >= 0");
+  if (x == x0) return fail(PU_ERR_ARG, "x must not alias x0");
+  PU_DISPATCH(h, {
+    return I.pcg(CP(b), CP(x0), MP(x), CP(dv), CP(dh), MP(r), MP(z), MP(p0), MP(p1), MP(spec), max_iters, rel_tol,
+                 reinterpret_cast<PcgCtrl*>(ctrl), res_norms, ST(stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+// Common device-side definitions for the B200 phase unwrapper.
+//
+// Memory layout: every grid-shaped array is an N x M
+// row-major plane with row pitch `ld` (elements, multiple of 8).  A system
+// vector (reference SystemVector, operators.py:39-101) is three consecutive
+// planes [u | vv | vh]; vv keeps a zero last row, vh a zero last column, and
+// pitch padding is zero, so BLAS-1 reductions may run over whole planes.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pu_unwrap.h"
+
+namespace pu {
+
+struct Grid {
+  int n;            // rows (N)
+  int m;            // cols (M)
+  long long ld;     // row pitch in elements
+  long long plane;  // n * ld
+  double tau;
+  double inv_tau;
+  double delta;
+};
+
+template <typename T> struct Vec2;
+template <> struct Vec2<float> { using type = float2; };
+template <> struct Vec2<double> { using type = double2; };
+template <typename T> using cplx = typename Vec2<T>::type;
+
+template <typename T> __device__ __forceinline__ cplx<T> mk(T x, T y) { cplx<T> c; c.x = x; c.y = y; return c; }
+template <typename T> __device__ __forceinline__ cplx<T> cadd(cplx<T> a, cplx<T> b) { return mk<T>(a.x + b.x, a.y + b.y); }
+template <typename T> __device__ __forceinline__ cplx<T> csub(cplx<T> a, cplx<T> b) { return mk<T>(a.x - b.x, a.y - b.y); }
+template <typename T> __device__ __forceinline__ cplx<T> cmul(cplx<T> a, cplx<T> b) {
+  return mk<T>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+template <typename T> __device__ __forceinline__ cplx<T> cconj(cplx<T> a) { return mk<T>(a.x, -a.y); }
+
+// ---------------------------------------------------------------------------
+// PCG device control block (one per solve, lives in device memory).
+// Mirrors the scalar state of pcg_solve (pcg.py:47-116): every kernel of the
+// iteration first reads `done` and returns early once the loop has ended, so
+// the host can enqueue a whole budget without synchronising.
+// ---------------------------------------------------------------------------
+using PcgCtrl = pu_pcg_ctrl;  // layout shared with the C ABI (include/pu_unwrap.h)
+
+// Deterministic two-level reduction: each block writes its partial sums to
+// `partials[s * stride + blockIdx.x]`; the last block to arrive (atomic
+// ticket) reduces them in a fixed order and runs the finaliser.  The result
+// therefore does not depend on block scheduling.
+struct RedScratch {
+  double* partials;       // [PU_MAX_SUMS][stride]
+  unsigned int* ticket;   // one counter per reduction site
+  int stride;             // >= max gridDim.x of any reducing kernel
+};
+
+#define PU_MAX_SUMS 12
+#define PU_RED_THREADS_MAX 1024
+
+template <int NS>
+__device__ __forceinline__ void block_sum(double (&v)[NS], double* sh /* [NS][32] */) {
+  // warp shuffle, then one warp over the per-warp results
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[s] += __shfl_xor_sync(0xffffffffu, v[s], o);
+  }
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) sh[s * 32 + warp] = v[s];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      double t = lane < nw ? sh[s * 32 + lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      v[s] = t;  // valid in warp 0
+    }
+  }
+  __syncthreads();
+}
+
+// Returns true in exactly one block (the last to finish); in that block all
+// threads see `tot[s]` = the grid-wide sums.
+template <int NS>
+__device__ __forceinline__ bool grid_reduce(double (&v)[NS], RedScratch rs, int site, double (&tot)[NS]) {
+  __shared__ double sh[NS * 32];
+  __shared__ bool last;
+  block_sum<NS>(v, sh);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) rs.partials[(size_t)s * rs.stride + blockIdx.x] = v[s];
+    __threadfence();
+    unsigned int t = atomicAdd(rs.ticket + site, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  double acc[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    acc[s] = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+      acc[s] += ((volatile double*)rs.partials)[(size_t)s * rs.stride + b];
+  }
+  block_sum<NS>(acc, sh);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) sh[s * 32] = acc[s];
+    rs.ticket[site] = 0u;  // re-arm for the next launch
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < NS; ++s) tot[s] = sh[s * 32];
+  __syncthreads();
+  return true;
+}
+
+__device__ __forceinline__ bool finite_d(double x) { return isfinite(x); }
+
+}  // namespace pu

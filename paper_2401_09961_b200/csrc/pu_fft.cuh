@@ -1,0 +1,453 @@
+// Shared-memory FFT engine and DCT-II/III building blocks (sm_100a).
+//
+// The reference applies its Poisson preconditioner with dense eigenbases
+// (preconditioner.py:64-100).  Those bases are the orthonormal DCT-II basis
+// (SURVEY.md §0 fact 2), so here every 1-D transform is a DCT computed by
+// Makhoul's n-point method on a complex FFT that packs two real sequences:
+//     v[p(m)] = a[m] + i b[m],  p(m) = m/2 (m even), n-1-(m-1)/2 (m odd)
+//     Z = FFT_n(v);  X_a[k] = s_k Re(e^{-i pi k/2n} (Z_k + conj Z_{n-k})/2), ...
+// The FFT itself is a Stockham autosort transform on one shared-memory
+// buffer: each stage loads its butterflies into registers, barriers, and
+// writes them back (radix 16/8/4/2 and 3/5/7).  Lengths with other prime
+// factors use Bluestein's chirp-z on an internal power-of-two length L.
+#pragma once
+
+#include "pu_common.cuh"
+
+namespace pu {
+
+#define PU_FFT_MAX_STAGES 20
+#define PU_FFT_MAX_THREADS 1024  // absolute per-CTA thread cap of the transform kernels
+
+// Per-instantiation launch bounds: a stage holds one whole sequence, so a CTA
+// needs L / EMAX threads; below that, 256 threads at <= 128 registers (two
+// CTAs per SM).  LS = 0 (runtime plan) allows 512 threads.
+__host__ __device__ constexpr int fft_max_threads(int LS, int EMAX) {
+  return LS == 0 ? 512 : (LS / EMAX > 256 ? LS / EMAX : 256);
+}
+__host__ __device__ constexpr int fft_min_blocks(int LS, int EMAX) {
+  return fft_max_threads(LS, EMAX) <= 256 ? 2 : 1;
+}
+
+// Runtime plan for one transform length (built on the host, pu_dct_plan.cu).
+template <typename T>
+struct FftPlan {
+  int n;                  // transform length
+  int L;                  // internal FFT length (n, or Bluestein power of two)
+  int nst;                // number of Stockham stages
+  int bluestein;          // 1 if Bluestein
+  int rad[PU_FFT_MAX_STAGES];
+  int ldseq;              // shared-memory stride between sequences (padded)
+  int cap;                // complex values per thread a stage can hold (min R*floor(EMAX/R))
+  const cplx<T>* tw;      // [L]  exp(-2 pi i k / L)
+  const cplx<T>* chirp;   // [n]  exp(-i pi k^2 / n)          (Bluestein)
+  const cplx<T>* filt;    // [L]  FFT_L(conj chirp, symmetric)/L (Bluestein)
+  const cplx<T>* dctw;    // [n]  (cos, sin)(pi k / 2n)
+  const T* scale;         // [n]  s_k: sqrt(1/n) for k = 0, sqrt(2/n) otherwise
+  const double* lam;      // [n]  2 - 2 cos(pi k / n), lam[0] = 0
+};
+
+// Bank-conflict padding: one complex slot every 16.
+__device__ __forceinline__ int spad(int i) { return i + (i >> 4); }
+
+// Makhoul permutation p(m).
+__device__ __forceinline__ int mperm(int m, int n) { return (m & 1) ? (n - 1 - (m >> 1)) : (m >> 1); }
+
+// ---------------------------------------------------------------------------
+// In-register DFTs (forward, e^{-2 pi i jk/R}).
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ cplx<T> mul_negi(cplx<T> a) { return mk<T>(a.y, -a.x); }  // a * (-i)
+
+template <typename T, int R>
+struct Dft;
+
+template <typename T>
+struct Dft<T, 2> {
+  __device__ __forceinline__ static void run(cplx<T>* a) {
+    cplx<T> t = a[1];
+    a[1] = csub<T>(a[0], t);
+    a[0] = cadd<T>(a[0], t);
+  }
+};
+
+template <typename T>
+struct Dft<T, 4> {
+  __device__ __forceinline__ static void run(cplx<T>* a) {
+    cplx<T> s0 = cadd<T>(a[0], a[2]), d0 = csub<T>(a[0], a[2]);
+    cplx<T> s1 = cadd<T>(a[1], a[3]), d1 = mul_negi<T>(csub<T>(a[1], a[3]));
+    a[0] = cadd<T>(s0, s1);
+    a[2] = csub<T>(s0, s1);
+    a[1] = cadd<T>(d0, d1);
+    a[3] = csub<T>(d0, d1);
+  }
+};
+
+// cos/sin(2 pi k / 16), k = 0..15
+__device__ __forceinline__ double c16(int k) {
+  const double t[16] = {1.0, 0.92387953251128674, 0.70710678118654757, 0.38268343236508984,
+                        0.0, -0.38268343236508984, -0.70710678118654757, -0.92387953251128674,
+                        -1.0, -0.92387953251128674, -0.70710678118654757, -0.38268343236508984,
+                        0.0, 0.38268343236508984, 0.70710678118654757, 0.92387953251128674};
+  return t[k & 15];
+}
+__device__ __forceinline__ double s16(int k) { return c16(k + 12); }  // sin(x) = cos(x - pi/2)
+
+// twiddle W_16^k = exp(-2 pi i k/16) applied to a
+template <typename T, int K>
+__device__ __forceinline__ cplx<T> w16(cplx<T> a) {
+  constexpr int k = K & 15;
+  if constexpr (k == 0) return a;
+  else if constexpr (k == 4) return mul_negi<T>(a);
+  else if constexpr (k == 8) return mk<T>(-a.x, -a.y);
+  else if constexpr (k == 12) return mk<T>(-a.y, a.x);
+  else {
+    const T c = (T)c16(k), s = (T)(-s16(k));
+    return mk<T>(a.x * c - a.y * s, a.x * s + a.y * c);
+  }
+}
+
+template <typename T>
+struct Dft<T, 8> {
+  __device__ __forceinline__ static void run(cplx<T>* a) {
+    // radix-2 DIT over two radix-4 halves
+    cplx<T> e[4] = {a[0], a[2], a[4], a[6]}, o[4] = {a[1], a[3], a[5], a[7]};
+    Dft<T, 4>::run(e);
+    Dft<T, 4>::run(o);
+    cplx<T> t1 = w16<T, 2>(o[1]), t2 = w16<T, 4>(o[2]), t3 = w16<T, 6>(o[3]);
+    a[0] = cadd<T>(e[0], o[0]); a[4] = csub<T>(e[0], o[0]);
+    a[1] = cadd<T>(e[1], t1);   a[5] = csub<T>(e[1], t1);
+    a[2] = cadd<T>(e[2], t2);   a[6] = csub<T>(e[2], t2);
+    a[3] = cadd<T>(e[3], t3);   a[7] = csub<T>(e[3], t3);
+  }
+};
+
+template <typename T>
+struct Dft<T, 16> {
+  __device__ __forceinline__ static void run(cplx<T>* a) {
+    // 4 x 4: columns (stride 4), twiddle, rows
+    cplx<T> c0[4] = {a[0], a[4], a[8], a[12]};
+    cplx<T> c1[4] = {a[1], a[5], a[9], a[13]};
+    cplx<T> c2[4] = {a[2], a[6], a[10], a[14]};
+    cplx<T> c3[4] = {a[3], a[7], a[11], a[15]};
+    Dft<T, 4>::run(c0); Dft<T, 4>::run(c1); Dft<T, 4>::run(c2); Dft<T, 4>::run(c3);
+    // twiddle c_q[k] *= W16^(q k)
+    c1[1] = w16<T, 1>(c1[1]); c1[2] = w16<T, 2>(c1[2]); c1[3] = w16<T, 3>(c1[3]);
+    c2[1] = w16<T, 2>(c2[1]); c2[2] = w16<T, 4>(c2[2]); c2[3] = w16<T, 6>(c2[3]);
+    c3[1] = w16<T, 3>(c3[1]); c3[2] = w16<T, 6>(c3[2]); c3[3] = w16<T, 9>(c3[3]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      cplx<T> r[4] = {c0[k], c1[k], c2[k], c3[k]};
+      Dft<T, 4>::run(r);
+      a[k] = r[0]; a[k + 4] = r[1]; a[k + 8] = r[2]; a[k + 12] = r[3];
+    }
+  }
+};
+
+// Odd primes: direct O(R^2) DFT with exact constant tables.
+template <typename T, int R>
+struct DftOdd {
+  __device__ __forceinline__ static double cs(int k) {
+    // cos(2 pi k / R) for R in {3,5,7}
+    if (R == 3) { const double t[3] = {1.0, -0.5, -0.5}; return t[k % 3]; }
+    if (R == 5) { const double t[5] = {1.0, 0.30901699437494745, -0.80901699437494734, -0.80901699437494734, 0.30901699437494745}; return t[k % 5]; }
+    const double t[7] = {1.0, 0.62348980185873359, -0.22252093395631434, -0.90096886790241915,
+                         -0.90096886790241915, -0.22252093395631434, 0.62348980185873359};
+    return t[k % 7];
+  }
+  __device__ __forceinline__ static double sn(int k) {
+    // sin(2 pi k / R)
+    if (R == 3) { const double t[3] = {0.0, 0.86602540378443860, -0.86602540378443860}; return t[k % 3]; }
+    if (R == 5) { const double t[5] = {0.0, 0.95105651629515353, 0.58778525229247314, -0.58778525229247314, -0.95105651629515353}; return t[k % 5]; }
+    const double t[7] = {0.0, 0.78183148246802981, 0.97492791218182362, 0.43388373911755812,
+                         -0.43388373911755812, -0.97492791218182362, -0.78183148246802981};
+    return t[k % 7];
+  }
+  __device__ __forceinline__ static void run(cplx<T>* a) {
+    cplx<T> out[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      T re = a[0].x, im = a[0].y;
+#pragma unroll
+      for (int j = 1; j < R; ++j) {
+        const T c = (T)cs(j * k), s = (T)(-sn(j * k));
+        re += a[j].x * c - a[j].y * s;
+        im += a[j].x * s + a[j].y * c;
+      }
+      out[k] = mk<T>(re, im);
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) a[k] = out[k];
+  }
+};
+template <typename T> struct Dft<T, 3> { __device__ __forceinline__ static void run(cplx<T>* a) { DftOdd<T, 3>::run(a); } };
+template <typename T> struct Dft<T, 5> { __device__ __forceinline__ static void run(cplx<T>* a) { DftOdd<T, 5>::run(a); } };
+template <typename T> struct Dft<T, 7> { __device__ __forceinline__ static void run(cplx<T>* a) { DftOdd<T, 7>::run(a); } };
+
+// ---------------------------------------------------------------------------
+// One Stockham stage over sequences [seq0, seq0 + nseq) of length L held in
+// shared memory.  Butterfly j (0 <= j < L/R) of a sequence reads X[j + r L/R],
+// applies the twiddles W_{Ns R}^{r (j mod Ns)}, runs a radix-R DFT and writes
+// Y[(j / Ns) Ns R + (j mod Ns) + r Ns].  Each thread holds at most EMAX complex
+// values (Q = EMAX/R butterflies), so the caller sizes the sequence group so
+// that blockDim.x * Q >= nseq * L / R.  FIRST stages (Ns = 1) need no twiddles;
+// plans put the radix with Q > 1 first so the others run with Q = 1.
+// ---------------------------------------------------------------------------
+template <typename T, int R, int EMAX, bool FIRST>
+__device__ __forceinline__ void fft_stage(cplx<T>* buf, int L, int seq0, int nseq, int ldseq, int Ns,
+                                          const cplx<T>* __restrict__ tw) {
+  constexpr int Q = EMAX / R;
+  static_assert(Q >= 1, "radix exceeds per-thread capacity");
+  const int nb = L / R;
+  const int total = nseq * nb;
+  cplx<T> v[Q][R];
+  int obase[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int b = threadIdx.x + q * blockDim.x;
+    obase[q] = -1;
+    if (b < total) {
+      const int s = b / nb;
+      const int j = b - s * nb;
+      const cplx<T>* sb = buf + (seq0 + s) * ldseq;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[q][r] = sb[spad(j + r * nb)];
+      if constexpr (FIRST) {
+        obase[q] = (seq0 + s) * ldseq + j * R;
+      } else {
+        const int k = j % Ns;
+        const int tws = (L / (Ns * R)) * k;
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[q][r] = cmul<T>(v[q][r], __ldg(tw + r * tws));
+        obase[q] = (seq0 + s) * ldseq + (j - k) * R + k;
+      }
+      Dft<T, R>::run(v[q]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    if (obase[q] >= 0) {
+      // obase already includes the sequence offset; spad acts on the in-sequence index
+      const int s0 = (obase[q] / ldseq) * ldseq;
+      const int i0 = obase[q] - s0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) buf[s0 + spad(i0 + r * (FIRST ? 1 : Ns))] = v[q][r];
+    }
+  }
+  __syncthreads();
+}
+
+template <typename T, int EMAX, bool FIRST>
+__device__ __forceinline__ void fft_stage_rt(int R, cplx<T>* buf, int L, int seq0, int nseq, int ldseq, int Ns,
+                                             const cplx<T>* tw) {
+  switch (R) {
+    case 16: if constexpr (EMAX >= 16) fft_stage<T, 16, EMAX, FIRST>(buf, L, seq0, nseq, ldseq, Ns, tw); break;
+    case 8: fft_stage<T, 8, EMAX, FIRST>(buf, L, seq0, nseq, ldseq, Ns, tw); break;
+    case 4: fft_stage<T, 4, EMAX, FIRST>(buf, L, seq0, nseq, ldseq, Ns, tw); break;
+    case 2: fft_stage<T, 2, EMAX, FIRST>(buf, L, seq0, nseq, ldseq, Ns, tw); break;
+    case 3: fft_stage<T, 3, EMAX, FIRST>(buf, L, seq0, nseq, ldseq, Ns, tw); break;
+    case 5: fft_stage<T, 5, EMAX, FIRST>(buf, L, seq0, nseq, ldseq, Ns, tw); break;
+    case 7: fft_stage<T, 7, EMAX, FIRST>(buf, L, seq0, nseq, ldseq, Ns, tw); break;
+    default: break;
+  }
+}
+
+// Full forward FFT of length plan.L on nseq sequences (in place, natural
+// order), processed in groups of sequences sized to the thread block.
+template <typename T, int EMAX>
+__device__ __forceinline__ void fft_pow(cplx<T>* buf, int nseq, const FftPlan<T>& pl) {
+  const int grp = max(1, (int)(blockDim.x * pl.cap) / pl.L);
+  for (int sg = 0; sg < nseq; sg += grp) {
+    const int cnt = min(grp, nseq - sg);
+    int Ns = 1;
+    for (int st = 0; st < pl.nst; ++st) {
+      const int R = pl.rad[st];
+      if (st == 0) fft_stage_rt<T, EMAX, true>(R, buf, pl.L, sg, cnt, pl.ldseq, 1, pl.tw);
+      else fft_stage_rt<T, EMAX, false>(R, buf, pl.L, sg, cnt, pl.ldseq, Ns, pl.tw);
+      Ns *= R;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Compile-time plans for power-of-two internal lengths (the production sizes):
+// stage 0 takes the remainder radix (twiddle-free, Q = EMAX/R butterflies per
+// thread), every later stage the largest radix (16 for fp32, 8 for fp64) with
+// Q = 1.  All strides are constants, so addressing folds into immediates.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int ldseq_for(int L) { return (L + (L >> 4) + 2) + ((L + (L >> 4) + 2) & 1); }
+
+template <int L, int EMAX>
+__host__ __device__ constexpr int first_radix() {
+  const int big = EMAX >= 16 ? 16 : 8;
+  int rem = L;
+  while (rem > 1 && rem % big == 0) rem /= big;
+  return rem == 1 ? big : rem;
+}
+
+template <typename T, int R, int EMAX, int L, int NS>
+__device__ __forceinline__ void fft_stage_s(cplx<T>* buf, int seq0, int nseq, const cplx<T>* __restrict__ tw) {
+  constexpr int Q = EMAX / R;
+  constexpr int NB = L / R;
+  constexpr int LD = ldseq_for(L);
+  static_assert(Q >= 1 && NB * R == L, "bad static stage");
+  const int total = nseq * NB;
+  cplx<T> v[Q][R];
+  int ob[Q], sbase[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int b = threadIdx.x + q * blockDim.x;
+    ob[q] = -1;
+    if (b < total) {
+      const int s = b / NB;
+      const int j = b - s * NB;
+      const int base = (seq0 + s) * LD;
+      sbase[q] = base;
+      if constexpr (NB % 16 == 0) {
+        // spad(j + r NB) = spad(j) + r (NB + NB/16): one base register, immediate offsets
+        const cplx<T>* src = buf + base + spad(j);
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[q][r] = src[r * (NB + NB / 16)];
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[q][r] = buf[base + spad(j + r * NB)];
+      }
+      if constexpr (NS > 1) {
+        const int k = j % NS;
+        constexpr int TWS = L / (NS * R);
+        const cplx<T>* twk = tw + k * TWS;
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[q][r] = cmul<T>(v[q][r], __ldg(twk + (r - 1) * k * TWS));
+        ob[q] = (j - k) * R + k;
+      } else {
+        ob[q] = j * R;
+      }
+      Dft<T, R>::run(v[q]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    if (ob[q] >= 0) {
+      const int base = sbase[q];
+      const int i0 = ob[q];
+      if constexpr (NS % 16 == 0) {
+        cplx<T>* dst = buf + base + spad(i0);
+#pragma unroll
+        for (int r = 0; r < R; ++r) dst[r * (NS + NS / 16)] = v[q][r];
+      } else if constexpr (NS == 1 && R == 16) {
+        cplx<T>* dst = buf + base + spad(i0);  // i0 = 16 j: spad(16 j + r) = 17 j + r
+#pragma unroll
+        for (int r = 0; r < R; ++r) dst[r] = v[q][r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[base + spad(i0 + r * NS)] = v[q][r];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <typename T, int EMAX, int L, int NS>
+__device__ __forceinline__ void fft_stages_s(cplx<T>* buf, int seq0, int nseq, const cplx<T>* tw) {
+  if constexpr (NS < L) {
+    constexpr int R = (NS == 1) ? first_radix<L, EMAX>() : (EMAX >= 16 ? 16 : 8);
+    fft_stage_s<T, R, EMAX, L, NS>(buf, seq0, nseq, tw);
+    fft_stages_s<T, EMAX, L, NS * R>(buf, seq0, nseq, tw);
+  }
+}
+
+// Forward FFT of internal length L on all sequences; LS > 0 selects the
+// compile-time plan (requires pl.L == LS), LS == 0 the runtime plan.
+template <typename T, int EMAX, int LS>
+__device__ __forceinline__ void fft_internal(cplx<T>* buf, int nseq, const FftPlan<T>& pl) {
+  if constexpr (LS > 0) {
+    const int grp = max(1, (int)(blockDim.x * EMAX) / LS);
+    for (int sg = 0; sg < nseq; sg += grp) fft_stages_s<T, EMAX, LS, 1>(buf, sg, min(grp, nseq - sg), pl.tw);
+  } else {
+    fft_pow<T, EMAX>(buf, nseq, pl);
+  }
+}
+
+// Forward DFT of length plan.n (entries [0, n) of each sequence), in place.
+// Callers must __syncthreads() before (data staged) — this returns synced.
+template <typename T, int EMAX, int LS>
+__device__ __forceinline__ void fft_n(cplx<T>* buf, int nseq, const FftPlan<T>& pl) {
+  if (!pl.bluestein) {
+    fft_internal<T, EMAX, LS>(buf, nseq, pl);
+    return;
+  }
+  const int n = pl.n, L = pl.L;
+  // a_m = x_m * chirp_m, zero-padded to L
+  for (int e = threadIdx.x; e < nseq * L; e += blockDim.x) {
+    const int s = e / L, m = e - s * L;
+    cplx<T>* sb = buf + s * pl.ldseq;
+    if (m < n) sb[spad(m)] = cmul<T>(sb[spad(m)], __ldg(pl.chirp + m));
+    else sb[spad(m)] = mk<T>((T)0, (T)0);
+  }
+  __syncthreads();
+  fft_internal<T, EMAX, LS>(buf, nseq, pl);
+  for (int e = threadIdx.x; e < nseq * L; e += blockDim.x) {
+    const int s = e / L, k = e - s * L;
+    cplx<T>* sb = buf + s * pl.ldseq;
+    sb[spad(k)] = cconj<T>(cmul<T>(sb[spad(k)], __ldg(pl.filt + k)));
+  }
+  __syncthreads();
+  fft_internal<T, EMAX, LS>(buf, nseq, pl);
+  for (int e = threadIdx.x; e < nseq * n; e += blockDim.x) {
+    const int s = e / n, k = e - s * n;
+    cplx<T>* sb = buf + s * pl.ldseq;
+    sb[spad(k)] = cmul<T>(cconj<T>(sb[spad(k)]), __ldg(pl.chirp + k));
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// DCT-II post-processing for the packed pair (a + i b) at bins k and n-k.
+// Given Z = FFT(v), returns the orthonormal DCT-II coefficients.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct PairOut { T a_k, b_k, a_nk, b_nk; };
+
+template <typename T>
+__device__ __forceinline__ PairOut<T> dct2_post(cplx<T> zk, cplx<T> znk, int k, int nk, const FftPlan<T>& pl) {
+  const T h = (T)0.5;
+  const T reA = h * (zk.x + znk.x), imA = h * (zk.y - znk.y);
+  const T reB = h * (zk.y + znk.y), imB = -h * (zk.x - znk.x);
+  const cplx<T> wk = __ldg(pl.dctw + k), wn = __ldg(pl.dctw + nk);
+  const T sk = __ldg(pl.scale + k), sn = __ldg(pl.scale + nk);
+  PairOut<T> o;
+  o.a_k = sk * (wk.x * reA + wk.y * imA);
+  o.b_k = sk * (wk.x * reB + wk.y * imB);
+  o.a_nk = sn * (wn.x * reA - wn.y * imA);
+  o.b_nk = sn * (wn.x * reB - wn.y * imB);
+  return o;
+}
+
+// DCT-III pre-processing: from orthonormal coefficients (a_k, a_nk, b_k, b_nk)
+// build conj(Z'_k), conj(Z'_nk) where Z' = V_a + i V_b and
+// V_k = e^{i pi k/2n} (Y_k - i Y_{n-k}), Y = X / s.  A forward FFT of the
+// conjugated data followed by conj()/n is the inverse FFT.
+template <typename T>
+__device__ __forceinline__ void dct3_pre(T ak, T ank, T bk, T bnk, int k, int nk, const FftPlan<T>& pl,
+                                         cplx<T>& out_k, cplx<T>& out_nk) {
+  const T isk = (T)1 / __ldg(pl.scale + k), isn = (T)1 / __ldg(pl.scale + nk);
+  const T yak = ak * isk, yank = ank * isn, ybk = bk * isk, ybnk = bnk * isn;
+  const cplx<T> wk = __ldg(pl.dctw + k), wn = __ldg(pl.dctw + nk);
+  T vaRe, vaIm, vbRe, vbIm;
+  if (k == 0) {
+    vaRe = yak; vaIm = 0; vbRe = ybk; vbIm = 0;
+  } else {
+    vaRe = wk.x * yak + wk.y * yank; vaIm = wk.y * yak - wk.x * yank;
+    vbRe = wk.x * ybk + wk.y * ybnk; vbIm = wk.y * ybk - wk.x * ybnk;
+  }
+  out_k = mk<T>(vaRe - vbIm, -(vaIm + vbRe));  // conj(Va + i Vb)
+  if (nk != k) {
+    const T uaRe = wn.x * yank + wn.y * yak, uaIm = wn.y * yank - wn.x * yak;
+    const T ubRe = wn.x * ybnk + wn.y * ybk, ubIm = wn.y * ybnk - wn.x * ybk;
+    out_nk = mk<T>(uaRe - ubIm, -(uaIm + ubRe));
+  }
+}
+
+}  // namespace pu

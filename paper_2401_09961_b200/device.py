@@ -1,0 +1,160 @@
+"""Device workspace: one planned N x M grid and its HBM buffers.
+
+Layout: every grid is a plane of shape (N, ld) with the row
+pitch `ld` chosen by the library (multiple of 8 elements); a system vector
+is a (3, N, ld) tensor [u | vv | vh].  Buffers are torch allocations (the
+caching allocator is the memory manager); all arithmetic is done by
+libpu_unwrap.so through the C ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import threading
+
+import numpy as np
+
+from . import _native as nat
+
+_DTYPES = {"fp32": nat.PU_F32, "float32": nat.PU_F32, "fp64": nat.PU_F64, "float64": nat.PU_F64}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+class Workspace:
+    """Handle + buffers for one (N, M, dtype, tau, delta); reused across calls."""
+
+    _cache: dict = {}
+    _lock = threading.Lock()
+
+    # scalar slots (fp64) in the device scalar block
+    S_HOLD, S_HNEW, S_HPROP, S_HCAND, S_MEAN, S_TAKE, S_HACC, S_F, S_L1, S_DOT, S_EVH = range(11)
+    NSCAL = 16
+
+    @classmethod
+    def get(cls, n, m, dtype="fp64", tau=1e-2, delta=1e-6, device=None):
+        torch = _torch()
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        key = (n, m, dtype, float(tau), float(delta), dev.index)
+        with cls._lock:
+            ws = cls._cache.get(key)
+            if ws is None:
+                ws = cls(n, m, dtype, tau, delta, dev)
+                cls._cache[key] = ws
+            return ws
+
+    def __init__(self, n, m, dtype="fp64", tau=1e-2, delta=1e-6, device=None):
+        self.lib = nat.ensure()
+        torch = _torch()
+        if dtype not in _DTYPES:
+            raise ValueError(f"dtype must be 'fp32' or 'fp64', got {dtype!r}")
+        self.n, self.m, self.dtype = int(n), int(m), dtype
+        self.code = _DTYPES[dtype]
+        self.tdtype = torch.float32 if self.code == nat.PU_F32 else torch.float64
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.tau, self.delta = float(tau), float(delta)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            nat.check(self.lib.pu_create(ctypes.byref(h), self.n, self.m, self.code, self.tau, self.delta))
+        self.h = h
+        self.ld = int(self.lib.pu_pitch(h))
+        self._bufs = {}
+        ctrl_bytes = int(self.lib.pu_pcg_ctrl_bytes())
+        # scalar block: NSCAL doubles followed by the PCG control struct
+        self.block = torch.zeros(self.NSCAL * 8 + ctrl_bytes, dtype=torch.uint8, device=self.device)
+        self.scal = self.block[: self.NSCAL * 8].view(torch.float64)
+        self.ctrl = self.block[self.NSCAL * 8:]
+        self.norms = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self._ctrl_dtype = np.dtype([("rho", "<f8"), ("alpha", "<f8"), ("beta", "<f8"), ("thr", "<f8"),
+                                     ("bnorm", "<f8"), ("pap", "<f8"), ("rn", "<f8"), ("mean_ru", "<f8"),
+                                     ("rho_s", "<f8"), ("done", "<i4"), ("converged", "<i4"),
+                                     ("breakdown", "<i4"), ("bkind", "<i4"), ("iterations", "<i4"),
+                                     ("max_iters", "<i4"), ("pad", "<i4", 2)])
+        assert self._ctrl_dtype.itemsize == ctrl_bytes
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) is not None and self.h.value:
+                self.lib.pu_destroy(self.h)
+        except Exception:
+            pass
+
+    # ---- plumbing -------------------------------------------------------
+    def stream(self):
+        return ctypes.c_void_p(_torch().cuda.current_stream(self.device).cuda_stream)
+
+    def describe(self):
+        buf = ctypes.create_string_buffer(1024)
+        nat.check(self.lib.pu_describe(self.h, buf, 1024))
+        return json.loads(buf.value.decode())
+
+    def planes(self, k):
+        """A fresh zeroed (k, N, ld) device tensor."""
+        return _torch().zeros((k, self.n, self.ld), dtype=self.tdtype, device=self.device)
+
+    def buf(self, name, k):
+        t = self._bufs.get(name)
+        if t is None:
+            t = self.planes(k)
+            self._bufs[name] = t
+        return t
+
+    def call(self, name, *args):
+        nat.check(getattr(self.lib, name)(self.h, *args))
+
+    # ---- host <-> device --------------------------------------------------
+    def pack(self, arr, dst):
+        """Compact host/device fp64 array (rows x cols) -> device plane dst."""
+        torch = _torch()
+        src = torch.as_tensor(np.ascontiguousarray(arr, dtype=np.float64)) if isinstance(arr, np.ndarray) else arr
+        src = src.to(device=self.device, dtype=torch.float64).contiguous()
+        rows, cols = (src.shape[0], src.shape[1]) if src.dim() == 2 else (0, 0)
+        lds = cols if cols > 0 else 1
+        self.call("pu_pack", _ptr(src) if src.numel() else ctypes.c_void_p(0), lds, rows, cols, _ptr(dst),
+                  self.stream())
+        return src  # keep alive until the stream has consumed it
+
+    def unpack(self, src, rows, cols):
+        """Device plane -> compact fp64 device tensor (rows x cols)."""
+        torch = _torch()
+        out = torch.empty((max(rows, 0), max(cols, 0)), dtype=torch.float64, device=self.device)
+        if rows > 0 and cols > 0:
+            self.call("pu_unpack", _ptr(src), rows, cols, _ptr(out), self.stream())
+        return out
+
+    def to_system(self, u, vv, vh, dst=None):
+        dst = dst if dst is not None else self.planes(3)
+        keep = [self.pack(u, dst[0]), self.pack(vv, dst[1]), self.pack(vh, dst[2])]
+        return dst, keep
+
+    def from_system(self, x):
+        n, m = self.n, self.m
+        return self.unpack(x[0], n, m), self.unpack(x[1], n - 1, m), self.unpack(x[2], n, m - 1)
+
+    def read_block(self):
+        """Synchronising read of the scalar block: (scalars[NSCAL], ctrl record)."""
+        host = self.block.cpu().numpy()
+        scal = host[: self.NSCAL * 8].view(np.float64).copy()
+        ctrl = host[self.NSCAL * 8:].view(self._ctrl_dtype)[0]
+        return scal, ctrl
+
+    def ensure_norms(self, max_iters):
+        if self.norms.numel() < max_iters + 1:
+            self.norms = _torch().zeros(max_iters + 1, dtype=torch_float64(), device=self.device)
+        return self.norms
+
+    def sp(self, slot):
+        """Device pointer to scalar slot `slot`."""
+        return ctypes.c_void_p(self.scal.data_ptr() + 8 * slot)
+
+
+def torch_float64():
+    return _torch().float64

@@ -1,0 +1,118 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library loads and
+exports every entry point include/pu_unwrap.h declares; host-side logic
+(parameter validation, budget rule) matches the reference."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2401_09961_b200 import _native
+from paper_2401_09961_b200.params import (IrlsParams, ModelParams, cg_budget_update, lipschitz_constant,
+                                          relative_improvement)
+from paper_2401_09961_b200.phase import WeightField
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "pu_unwrap.h")
+
+
+def header_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(pu_\w+)\s*\(", text, re.M)))
+
+
+def test_header_and_binding_agree():
+    assert header_symbols() == _native.exported_symbols()
+
+
+def test_library_exports_every_symbol():
+    if not os.path.exists(_native.LIB_PATH):
+        from paper_2401_09961_b200 import build_ext
+        build_ext.build()
+    lib = _native.load()
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+    assert lib.pu_abi_version() == 1
+    assert lib.pu_pcg_ctrl_bytes() == 9 * 8 + 8 * 4
+
+
+def test_create_fails_cleanly_without_gpu():
+    """No GPU in this container: planning must fail with a CUDA error code, not crash."""
+    import ctypes
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = _native.load()
+    h = ctypes.c_void_p()
+    rc = lib.pu_create(ctypes.byref(h), 8, 8, 0, 1e-2, 1e-6)
+    assert rc == _native.PU_ERR_CUDA
+    assert lib.pu_last_error()
+    # argument validation happens before any CUDA call (reference raises ValueError)
+    assert lib.pu_create(ctypes.byref(h), 0, 8, 0, 1e-2, 1e-6) == _native.PU_ERR_ARG
+    assert lib.pu_create(ctypes.byref(h), 8, 8, 0, -1.0, 1e-6) == _native.PU_ERR_ARG
+
+
+def test_product_path_fails_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2401_09961_b200 import unwrap
+    with pytest.raises(RuntimeError, match="CUDA"):
+        unwrap(np.zeros((4, 4)))
+
+
+class TestBudgetRules:
+    # reference tests/test_irls.py:30-58
+    D = IrlsParams()
+
+    def test_keep(self):
+        d = cg_budget_update(1e-2, 5, 5, self.D)
+        assert (d.action, d.m_cg) == ("keep", 5)
+
+    def test_stop_after_grow(self):
+        assert cg_budget_update(1e-4, 9, 5, self.D).action == "stop"
+
+    def test_grow(self):
+        d = cg_budget_update(1e-4, 5, 5, self.D)
+        assert (d.action, d.m_cg) == ("grow", 9)
+
+    def test_grow_clamps(self):
+        d = cg_budget_update(1e-4, 8, 8, IrlsParams(max_cg_iters_cap=12))
+        assert (d.action, d.m_cg) == ("grow", 12)
+
+    def test_stop_at_cap(self):
+        assert cg_budget_update(1e-4, 8, 8, IrlsParams(max_cg_iters_cap=8, max_iter_cg_start=8)).action == "stop"
+
+    def test_rejects(self):
+        with pytest.raises(ValueError):
+            cg_budget_update(1e-4, 0, 0, self.D)
+
+    def test_relative_improvement(self):
+        assert relative_improvement(2.0, 1.0) == 0.5
+        with pytest.raises(ValueError):
+            relative_improvement(0.0, 1.0)
+
+
+def test_param_validation():
+    for bad in (dict(max_iter_cg_start=0), dict(rel_improvement_tol=0), dict(cg_growth_factor=1.0),
+                dict(max_outer_iters=0), dict(max_cg_iters_cap=2), dict(cg_rel_tol=-1)):
+        with pytest.raises(ValueError):
+            IrlsParams(**bad)
+    with pytest.raises(ValueError):
+        ModelParams(tau=0)
+    with pytest.raises(ValueError):
+        ModelParams(delta=float("inf"))
+
+
+def test_lipschitz():
+    assert lipschitz_constant(WeightField.uniform(3, 3), ModelParams()) == 1_001_200.0
+
+
+def test_weightfield_validation():
+    with pytest.raises(ValueError):
+        WeightField(np.ones((2, 3)), np.ones((3, 3)))
+    with pytest.raises(ValueError):
+        WeightField(-np.ones((2, 3)), np.ones((3, 2)))
+    with pytest.raises(ValueError):
+        WeightField(np.zeros((2, 3)), np.zeros((3, 2)))

@@ -1,0 +1,122 @@
+"""End-to-end parity of the GPU unwrap with the reference (golden fixtures,
+run by the unmodified reference) and with the CPU oracle."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import phaseirls_port as port
+from cases import GOLDEN_UNWRAP_CASES, case_inputs, golden_trace, rel
+
+pytestmark = pytest.mark.gpu
+
+pu = pytest.importorskip("paper_2401_09961_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _weights(cv, ch):
+    return None if cv is None else pu.WeightField(cv, ch)
+
+
+@pytest.mark.parametrize("name", GOLDEN_UNWRAP_CASES)
+def test_fp64_matches_reference(golden_unwrap, golden_meta, name):
+    """north_star fp64 bar: u within 1e-8 relative; identical control flow."""
+    x, cv, ch, tau, delta, prm, lo = case_inputs(golden_unwrap, golden_meta, name)
+    params = pu.IrlsParams(**prm.__dict__)
+    res = pu.unwrap(x, _weights(cv, ch), pu.ModelParams(tau, delta), params, lo, dtype="fp64")
+    want = golden_trace(golden_unwrap, name)
+    recs = res.trace.records
+    assert [r.m_cg for r in recs] == want["m_cg"].tolist()
+    assert [r.cg_iters for r in recs] == want["cg_iters"].tolist()
+    # The safeguard compares H(proposal) with H(cand) (irls.py:203-205).  When PCG
+    # exits at iteration 0 the state is optimal to rel_tol and the two values
+    # differ by ~||grad||^2 / 2L (~1e-18 here), below the summation round-off of
+    # either code, so that comparison is a coin flip (SURVEY §7 hard part 2).
+    # Elsewhere the decision must match.
+    for r, fb, its in zip(recs, want["fallback"].tolist(), want["cg_iters"].tolist()):
+        if its > 0:
+            assert r.fallback_used == fb, f"fallback differs at k={r.k}"
+    np.testing.assert_allclose([r.h_delta for r in recs], want["h_delta"], rtol=1e-8)
+    u_ref = golden_unwrap[f"{name}/u"]
+    assert rel(res.u, u_ref) <= 1e-8 or np.max(np.abs(res.u - u_ref)) <= 1e-12
+    assert res.vv.shape == golden_unwrap[f"{name}/vv"].shape
+    assert abs(res.u.sum()) <= 1e-9 * res.u.size
+
+
+@pytest.mark.parametrize("name", ["noisy64", "noisy96x80", "clean128", "weighted40x36", "random4x4"])
+def test_fp32_objective_within_1e3(golden_unwrap, golden_meta, name):
+    """north_star fp32 bar: final L1 objective F within 1e-3 relative of the reference's.
+
+    Residue-free scenes have F_ref ~ 1e-14 (the relative bar is ill-posed,
+    SURVEY §8(d)); there the fp32 solve must reach F <= 1e-6 absolute."""
+    x, cv, ch, tau, delta, prm, lo = case_inputs(golden_unwrap, golden_meta, name)
+    params = pu.IrlsParams(**prm.__dict__)
+    res = pu.unwrap(x, _weights(cv, ch), pu.ModelParams(tau, delta), params, lo, dtype="fp32")
+    gv, gh = port.grad_wrapped(x, lo)
+    cvv = np.ones_like(gv) if cv is None else cv
+    chh = np.ones_like(gh) if ch is None else ch
+    f_gpu = port.f_l1(port.Triple(res.u, res.vv, res.vh), gv, gh, cvv, chh, tau)
+    ref = port.Triple(golden_unwrap[f"{name}/u"], golden_unwrap[f"{name}/vv"], golden_unwrap[f"{name}/vh"])
+    f_ref = port.f_l1(ref, gv, gh, cvv, chh, tau)
+    assert abs(f_gpu - f_ref) <= max(1e-3 * f_ref, 1e-6)
+
+
+def test_c1_fp64_matches_reference(golden_meta):
+    """Config C1 (512^2): reference trace, F and u (stored as f32) reproduced."""
+    _, x = pu.config_scene("c1")
+    res = pu.unwrap(x, dtype="fp64")
+    ref = golden_meta["configs"]["c1"]
+    assert [r.cg_iters for r in res.trace.records] == ref["trace"]["cg_iters"]
+    assert [r.m_cg for r in res.trace.records] == ref["trace"]["m_cg"]
+    gv, gh = port.grad_wrapped(x)
+    f = port.f_l1(port.Triple(res.u, res.vv, res.vh), gv, gh, np.ones_like(gv), np.ones_like(gh), 1e-2)
+    assert f == pytest.approx(ref["F"], rel=1e-8)
+    assert float(np.linalg.norm(res.u)) == pytest.approx(ref["u_norm"], rel=1e-8)
+    u32 = np.load(os.path.join(os.path.dirname(__file__), "golden", "c1_u_f32.npz"))["u"]
+    assert np.max(np.abs(res.u - u32)) <= 1e-4 * np.abs(u32).max()
+    assert np.mean(port.kmap(res.u, x) != port.kmap(u32.astype(np.float64), x)) == 0.0
+
+
+def test_c1_fp32_objective(golden_meta):
+    _, x = pu.config_scene("c1")
+    res = pu.unwrap(x, dtype="fp32")
+    gv, gh = port.grad_wrapped(x)
+    f = port.f_l1(port.Triple(res.u, res.vv, res.vh), gv, gh, np.ones_like(gv), np.ones_like(gh), 1e-2)
+    assert abs(f - golden_meta["configs"]["c1"]["F"]) / golden_meta["configs"]["c1"]["F"] <= 1e-3
+
+
+def test_torch_input_and_errors():
+    import torch
+    x = pu.wrap_scene(pu.generate_scene(pu.SceneSpec("gaussian-bumps", 24, 20, 4.0, 6.0, 9)))
+    a = pu.unwrap(x)
+    b = pu.unwrap(torch.from_numpy(x).cuda())
+    np.testing.assert_array_equal(a.u, b.u)  # deterministic reductions
+    with pytest.raises(ValueError):
+        pu.unwrap(np.full((3, 3), 9.0))
+    with pytest.raises(ValueError):
+        pu.unwrap(np.zeros((4, 4)), pu.WeightField.uniform(5, 5))
+
+
+def test_shift_equivariance():
+    # reference tests/test_irls.py:130-135
+    t = pu.generate_scene(pu.SceneSpec("gaussian-bumps", 24, 24, 5.0, 6.0, 13))
+    a = pu.unwrap(pu.wrap_scene(t))
+    b = pu.unwrap(pu.wrap_scene(t + 7.7))
+    assert np.max(np.abs(a.u - b.u)) < 1e-8
+
+
+def test_monotone_descent_and_safeguard():
+    # reference acceptance #7 (tests/test_acceptance.py:205-221), fewer scenes
+    for seed in range(4):
+        spec = pu.SceneSpec("gaussian-bumps", 64, 64, 6.0, 10.0, seed)
+        x = pu.add_phase_noise(pu.wrap_scene(pu.generate_scene(spec)), 0.3, seed + 1000)
+        h = pu.unwrap(x).trace.h_values()
+        assert all(b <= a * (1 + 1e-12) for a, b in zip(h, h[1:]))
