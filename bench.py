@@ -1,0 +1,399 @@
+#!/usr/bin/env python3
+"""Benchmark of the unwrap hot path (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--dtype fp32]
+    python bench.py --impl reference ...     # reference CPU path on the host cores
+
+One step = one complete `unwrap` (IRLS to the reference's stopping rule) of
+the config's synthetic wrapped image.  Under torchrun each rank unwraps its
+own image (independent units, no data-path collective: weak scaling); time
+is the max over ranks of CUDA-event time, bracketed by barrier+synchronize.
+Prints ONE JSON line on rank 0 (contract in the task statement / DESIGN.md §6).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "unwrap time & Mpixel/s to convergence at 4096²; PCG iter/s; % HBM roofline"
+UNIT = "Mpixel/s"
+# Final objective F of the reference on C3 (measured in the survey)
+REF_F = {"c1": 81.567, "c2": 765.61, "c3": 8744.586}
+REF_COUNTS = {"c1": (41, 227), "c2": (42, 229), "c3": (39, 218)}  # outer / PCG iterations
+WORKLOAD = {
+    "c1": "512x512 gaussian-bumps(40,32,seed 1) + noise 0.5 (seed 1001)",
+    "c2": "2048x2048 gaussian-bumps(100,128,seed 2) + noise 0.5 (seed 1002)",
+    "c3": "4096x4096 InSAR-like: bumps(150,256,seed 3) + tapered fault 0->4pi (scale 512) + noise 0.5 (seed 1003)",
+}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def algorithmic_bytes(n, m, e):
+    """per-launch compulsory bytes of K1..K4 and of one PCG iteration."""
+    u = n * m
+    s = (n - 1) * m + n * (m - 1)
+    S = u + s
+    return {
+        "K1_p_Ap_pAp": (3 * S + s) * e,
+        "K2_update_rowdct": (5 * S + 2 * s + u) * e,
+        "K3_coldct_spectral": 2 * u * e,
+        "K4_row_idct": 2 * u * e,
+        "iteration": (8 * S + 3 * s + 5 * u) * e,
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[3:7]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+# ---------------------------------------------------------------------------
+# reference CPU path (the oracle port of the reference algorithm)
+# ---------------------------------------------------------------------------
+def cpu_reference_sample(x, n_outer, n_pcg, pcg_reps=2):
+    """Time the reference algorithm (oracle/phaseirls_port.py, dense-eigenbasis
+    preconditioner exactly as preconditioner.py:64-100) on the host cores:
+    the once-per-unwrap setup, `pcg_reps` PCG iterations and one outer
+    iteration's other work, then scale to the full unwrap's iteration counts."""
+    from oracle import phaseirls_port as port
+    n, m = x.shape
+    tau, delta = 1e-2, 1e-6
+    t0 = time.perf_counter()
+    gv, gh = port.grad_wrapped(x)
+    b = port.rhs(gv, gh, tau)
+    solver = port.make_poisson(n, m, "dense")                 # 2 x LAPACK eigh (preconditioner.py:77-83)
+    t_setup = time.perf_counter() - t0
+    cv, ch = np.ones_like(gv), np.ones_like(gh)
+    state = port.Triple(np.zeros((n, m)), -gv.copy(), -gh.copy())
+    t0 = time.perf_counter()
+    w = port.weights(state, cv, ch, delta)                   # irls.py:173-191 outer work
+    h1 = port.h_delta(state, w, gv, gh, cv, ch, tau, delta)
+    h2 = port.h_delta(state, w, gv, gh, cv, ch, tau, delta)
+    dv, dh = cv * cv / w[0], ch * ch / w[1]
+    cand = port.candidate(state, w, gv, gh, cv, ch, tau, port.lipschitz(1.0, tau, delta))
+    h3 = port.h_delta(cand, w, gv, gh, cv, ch, tau, delta)
+    h4 = port.h_delta(state, w, gv, gh, cv, ch, tau, delta)
+    cand.u -= cand.u.mean()
+    h5 = port.h_delta(cand, w, gv, gh, cv, ch, tau, delta)
+    t_outer = time.perf_counter() - t0
+    apply_a = lambda v: port.system_apply(v, dv, dh, tau)       # noqa: E731
+    apply_m = lambda r: port.precond_apply(r, dv, dh, tau, solver)  # noqa: E731
+    t0 = time.perf_counter()
+    port.pcg(apply_a, apply_m, b, state, 0, 0.0)              # start-up: x copy, r = b - A x, ||r||
+    t_start = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    port.pcg(apply_a, apply_m, b, state, pcg_reps, 0.0)       # start-up + z = M r + pcg_reps iterations
+    t_k = time.perf_counter() - t0
+    t_iter = (t_k - t_start) / (pcg_reps + 1)                 # pcg_reps iterations + 1 initial M r
+    total = t_setup + n_outer * (t_outer + t_start + t_iter) + n_pcg * t_iter
+    del h1, h2, h3, h4, h5
+    return {
+        "seconds": total, "t_setup_s": t_setup, "t_outer_s": t_outer, "t_pcg_start_s": t_start,
+        "t_pcg_iter_s": t_iter, "n_outer": n_outer, "n_pcg": n_pcg,
+        "mpix_s": n * m / total / 1e6, "pcg_it_s": n_pcg / total,
+        "sample": (f"reference algorithm (oracle port, dense LAPACK eigenbasis preconditioner) on the full {n}x{m} "
+                   f"input: setup + {pcg_reps} PCG iterations + 1 outer iteration timed "
+                   f"({t_setup + t_outer + t_k + t_start:.1f} s), scaled to {n_outer} outer / {n_pcg} PCG iterations"),
+    }
+
+
+def cpu_info():
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from paper_2401_09961_b200.synth import config_scene
+    _, x = config_scene(args.config)
+    n, m = x.shape
+    n_outer, n_pcg = REF_COUNTS[args.config]
+    model, cores = cpu_info()
+    # each step: the bounded sample (setup + 1 PCG iteration + 1 outer iteration), scaled to the full unwrap
+    for _ in range(args.warmup_ref):
+        cpu_reference_sample(x, n_outer, n_pcg, pcg_reps=1)
+    samples = [cpu_reference_sample(x, n_outer, n_pcg, pcg_reps=1) for _ in range(max(1, args.steps_ref))]
+    secs = statistics.median(s["seconds"] for s in samples)
+    value = n * m / secs / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": len(samples), "warmup": args.warmup_ref, "ms_per_step": secs * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD[args.config], "n": n, "m": m, "cpu": model},
+        "pcg_iters_per_s": n_pcg / secs,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": samples[0]["sample"] + f"; iteration counts from the reference trace "
+                                                         f"(BASELINE.md: {n_outer} outer / {n_pcg} PCG)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "detail": {k: v for k, v in samples[0].items() if k != "sample"},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=("c1", "c2", "c3"), default="c3")
+    ap.add_argument("--dtype", choices=("fp32", "fp64"), default="fp32")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=0,
+                    help="only run N unwraps (for ncu launch lists); prints no JSON")
+    ap.add_argument("--warmup-ref", type=int, default=1)
+    ap.add_argument("--steps-ref", type=int, default=2)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.profile_steps == 0 else args.warmup
+
+    rank, local_rank, world = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2401_09961_b200 as pu
+    from paper_2401_09961_b200 import _native
+    from paper_2401_09961_b200.device import Workspace
+    from paper_2401_09961_b200.irls import unwrap_device
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _native.ensure()
+
+    _, x = pu.config_scene(args.config)
+    n, m = x.shape
+    model, params = pu.ModelParams(), pu.IrlsParams()
+    ws = Workspace.get(n, m, args.dtype, model.tau, model.delta, dev)
+    x_dev = torch.from_numpy(x).to(dev)
+
+    def one_unwrap():
+        run, trace = unwrap_device(x_dev, None, model, params, -np.pi, args.dtype, ws)
+        return run, trace
+
+    if args.profile_steps:
+        for _ in range(args.profile_steps):
+            one_unwrap()
+        torch.cuda.synchronize()
+        return 0
+
+    for _ in range(args.warmup):
+        run, trace = one_unwrap()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- timed region: device-resident input ----
+    ws.timing(True)
+    ws.read_timing()  # drain
+    launches0 = lib.pu_launch_count()
+    kind_ms = {}
+    traces = []
+    with ClockSampler(local_rank) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            run, trace = one_unwrap()
+            traces.append(trace)
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+    launches = lib.pu_launch_count() - launches0
+    ws.timing(False)
+    kinds, its, ms = ws.read_timing()
+    step_ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([step_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = float(t.item())
+    value = world * n * m / (step_ms / 1e3) / 1e6
+
+    # per-kernel statistics (skip launches that returned early after PCG exit)
+    e = 4 if args.dtype == "fp32" else 8
+    alg = algorithmic_bytes(n, m, e)
+    hbm, peak_kind = peaks()
+    per_kind = {}
+    for kd in np.unique(kinds):
+        sel = ms[kinds == kd]
+        ran = sel[sel >= 0.25 * np.median(sel)] if sel.size else sel
+        name = Workspace.TIME_KINDS[kd] if kd < len(Workspace.TIME_KINDS) else str(kd)
+        per_kind[name] = {"launches": int(sel.size), "ran": int(ran.size), "total_ms": float(ran.sum()),
+                          "avg_ms": float(ran.mean()) if ran.size else 0.0}
+    timed_total = sum(v["total_ms"] for v in per_kind.values())
+    dom = max((k for k in per_kind if k in alg), key=lambda k: per_kind[k]["total_ms"])
+    achieved = alg[dom] / (per_kind[dom]["avg_ms"] / 1e3) / 1e9
+    n_pcg = sum(r.cg_iters for r in traces[-1].records)
+    n_outer = len(traces[-1].records)
+    iter_ms = sum(per_kind[k]["total_ms"] for k in ("K1_p_Ap_pAp", "K2_update_rowdct", "K3_coldct_spectral",
+                                                    "K4_row_idct") if k in per_kind) / max(1, args.steps * n_pcg)
+    roofline = {
+        "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "bytes_per_launch": alg[dom],
+        "avg_launch_ms": per_kind[dom]["avg_ms"], "share_of_kernel_time": per_kind[dom]["total_ms"] / timed_total,
+        "traffic": None,
+        "pcg_iteration": {"bytes": alg["iteration"], "ms": iter_ms,
+                          "achieved_gbs": alg["iteration"] / (iter_ms / 1e3) / 1e9 if iter_ms else None,
+                          "frac": (alg["iteration"] / (iter_ms / 1e3) / 1e9) / hbm if iter_ms else None},
+    }
+
+    # objective of the result (device eval_f) against the reference's F
+    f_out = None
+    try:
+        ws.call("pu_eval_f", pu.device._ptr(run.S), pu.device._ptr(run.G[0]), pu.device._ptr(run.G[1]),
+                pu.device._ptr(run.W[0]), pu.device._ptr(run.W[1]), ws.sp(ws.S_F), ws.stream())
+        f_out = float(ws.read_block()[0][ws.S_F])
+    except Exception:
+        pass
+
+    # ---- end to end through the public API: pinned host input -> host result ----
+    x_pin = torch.from_numpy(x).pin_memory()
+    e2e_ms = []
+    for i in range(args.steps + 1):
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = pu.unwrap(x_pin, dtype=args.dtype)
+        t1 = time.perf_counter()
+        if i > 0:
+            e2e_ms.append((t1 - t0) * 1e3)
+    e2e_step = statistics.mean(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_step = float(t.item())
+    h2d = n * m * 8
+    d2h = (res.u.size + res.vv.size + res.vh.size) * 8
+
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        model_name, cores = cpu_info()
+        smp = cpu_reference_sample(x, n_outer, n_pcg)
+        cpu_base = {"value": smp["mpix_s"], "unit": UNIT, "cores": cores, "kind": "port", "sample": smp["sample"],
+                    "cpu": model_name, "pcg_iters_per_s": smp["pcg_it_s"], "seconds_per_unwrap": smp["seconds"]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {WORKLOAD[args.config]}", "n": n, "m": m,
+                       "per_rank": "one independent image per GPU",
+                       "l2": "inputs larger than L2 (~1.6 GB resident working set vs 126 MB L2)",
+                       "plan": ws.describe()},
+            "unwrap_s": step_ms / 1e3,
+            "pcg_iters_per_step": n_pcg, "outer_iters_per_step": n_outer,
+            "pcg_iters_per_s": world * n_pcg / (step_ms / 1e3),
+            "roofline": roofline,
+            "kernels": per_kind,
+            "objective": {"F": f_out, "F_reference": REF_F.get(args.config),
+                          "rel": (abs(f_out - REF_F[args.config]) / REF_F[args.config])
+                          if f_out is not None and args.config in REF_F else None},
+            "cpu_baseline": cpu_base,
+            "e2e": {"value": world * n * m / (e2e_step / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step},
+            "clocks": clocks.summary(),
+            "gpu_launches": int(launches),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -151,6 +151,25 @@ class Workspace:
             self.norms = _torch().zeros(max_iters + 1, dtype=torch_float64(), device=self.device)
         return self.norms
 
+    # ---- instrumentation ---------------------------------------------------
+    TIME_KINDS = ("pcg_start", "K1_p_Ap_pAp", "K2_update_rowdct", "K3_coldct_spectral", "K4_row_idct",
+                  "reproject_update", "weights_hpair", "candidate", "hpair_states", "accept_center")
+
+    def timing(self, on: bool):
+        nat.check(self.lib.pu_timing_enable(self.h, 1 if on else 0))
+
+    def read_timing(self, cap=1 << 16):
+        """(kinds, its, ms) numpy arrays of the per-launch event timings recorded so far."""
+        kinds = (ctypes.c_int * cap)()
+        its = (ctypes.c_int * cap)()
+        ms = (ctypes.c_float * cap)()
+        cnt = int(self.lib.pu_timing_read(self.h, kinds, its, ms, cap))
+        if cnt < 0:
+            raise nat.NativeError("pu_timing_read failed")
+        return (np.frombuffer(kinds, dtype=np.int32, count=cnt).copy(),
+                np.frombuffer(its, dtype=np.int32, count=cnt).copy(),
+                np.frombuffer(ms, dtype=np.float32, count=cnt).astype(np.float64))
+
     def sp(self, slot):
         """Device pointer to scalar slot `slot`."""
         return ctypes.c_void_p(self.scal.data_ptr() + 8 * slot)

@@ -133,31 +133,29 @@ def unwrap(x, c: WeightField | None = None, model: ModelParams | None = None, pa
     from . import _native
     _native.ensure()  # library + CUDA device, or raise: there is no CPU path
     torch = _torch()
+    dev = torch.device(device) if device is not None else (
+        x.device if isinstance(x, torch.Tensor) and x.is_cuda else torch.device("cuda", torch.cuda.current_device()))
     if isinstance(x, torch.Tensor):
         if x.dim() != 2 or x.shape[0] < 1 or x.shape[1] < 1:
             raise ValueError(f"phase grid must be 2-D and non-empty, got shape {tuple(x.shape)}")
-        x_dev = x.to(dtype=torch.float64)
-        if not torch.isfinite(x_dev).all():
+        # host (ideally pinned) tensors are copied first and validated on the device
+        x_dev = x.to(device=dev, dtype=torch.float64, non_blocking=True)
+        lo_hi = torch.stack([x_dev.min(), x_dev.max(), torch.isfinite(x_dev).all().to(torch.float64)]).cpu()
+        if lo_hi[2] != 1.0:
             raise ValueError("phase grid contains non-finite values")
-        if float(x_dev.min()) < 0.0 or float(x_dev.max()) >= 2.0 * np.pi:
+        if float(lo_hi[0]) < 0.0 or float(lo_hi[1]) >= 2.0 * np.pi:
             raise ValueError("wrapped phase values must lie in [0, 2*pi)")
         n, m = x_dev.shape
     else:
         arr = validate_wrapped(x)
         n, m = arr.shape
-        x_dev = None
+        x_dev = torch.from_numpy(arr).to(dev)
     model = model or ModelParams()
     params = params or IrlsParams()
     if c is not None and (c.cv.shape != (n - 1, m) or c.ch.shape != (n, m - 1)):
         raise ValueError(f"weight shapes {c.cv.shape}/{c.ch.shape} do not match grid {(n, m)}")
     if gradient_lo not in (0.0, 0, -np.pi):
         raise ValueError(f"lo must be 0 or -pi, got {gradient_lo!r}")
-    dev = torch.device(device) if device is not None else (
-        x_dev.device if x_dev is not None and x_dev.is_cuda else torch.device("cuda", torch.cuda.current_device()))
-    if x_dev is None:
-        x_dev = torch.from_numpy(arr).to(dev, non_blocking=False)
-    else:
-        x_dev = x_dev.to(dev)
     run, trace = unwrap_device(x_dev, c, model, params, gradient_lo, dtype)
     u, vv, vh = run.result_arrays()
     return UnwrapResult(u=u.cpu().numpy(), vv=vv.cpu().numpy(), vh=vh.cpu().numpy(), trace=trace)
