@@ -139,7 +139,7 @@ int pu_accept_center(pu_handle* h, const void* xa, const void* xb, const double*
                      const void* ch, double* out, void* stream);
 
 /* pcg.py:47-116 pcg_solve with apply_system and apply_preconditioner fused
- * in (4 kernels per iteration).  x = x0 on entry; x0 is not modified.
+ * in (5 kernels per iteration).  x = x0 on entry; x0 is not modified.
  * r, z, p0, p1: system-vector scratch; spec: one plane.  ctrl: device
  * pu_pcg_ctrl; res_norms: device fp64 [max_iters + 1].  Enqueues without
  * synchronising when max_iters <= 64; longer budgets poll ctrl->done
@@ -151,9 +151,10 @@ int pu_pcg_solve(pu_handle* h, const void* b, const void* x0, void* x, const voi
 /* Per-launch CUDA-event timing on the launching stream (off by default).
  * pu_timing_read synchronises on the recorded events and returns the number
  * of records (kind, iteration, milliseconds) written, up to cap; kinds:
- * 0 pcg_start, 1 K1 (p, Ap, p'Ap), 2 K2 (x, r, z_s, row DCT-II), 3 K3
- * (column DCT pair), 4 K4 (row DCT-III), 5 reprojection update, 6 weights,
- * 7 candidate, 8 H pair, 9 accept.  Iteration -1 = PCG setup / outer kernel. */
+ * 0 pcg_start, 1 K1 (p, Ap, p'Ap), 2 K2a (x, r, z_s, norms), 3 K3 (column
+ * DCT pair), 4 K4 (row DCT-III), 5 reprojection update, 6 weights,
+ * 7 candidate, 8 H pair, 9 accept, 10 K2b (row DCT-II of r_u).
+ * Iteration -1 = PCG setup / outer kernel. */
 int pu_timing_enable(pu_handle* h, int on);
 int pu_timing_read(pu_handle* h, int* kinds, int* its, float* ms, int cap);
 

@@ -44,7 +44,7 @@ static std::atomic<long long> g_launches{0};
     PU_CUDA(call);                                         \
   } while (0)
 
-enum Site { S_DOT = 0, S_WH, S_EVH, S_HPAIR, S_ACC, S_EVF, S_START, S_K1, S_K2, S_K3, S_UPD, S_NSITES };
+enum Site { S_DOT = 0, S_WH, S_EVH, S_HPAIR, S_ACC, S_EVF, S_START, S_K1, S_K2, S_K3, S_UPD, S_K2B, S_NSITES };
 
 typedef long double ld_t;
 static const ld_t kPi = 3.141592653589793238462643383279502884L;
@@ -116,21 +116,39 @@ struct HostPlan {
     dev.cap = seq_capacity;
     dev.ldseq = ldseq_for(L);  // spad(L-1) + 1 (+ pad), kept even for 16-byte alignment
     using C = cplx<T>;
-    std::vector<C> tw(L), dctw(n), chirp(n), filt(L);
-    std::vector<T> scale(n);
-    std::vector<double> lam(n);
+    std::vector<C> tw(L), dct2w(n), dct3w(n), chirp(n), filt(L);
+    std::vector<T> lam(n);
     for (int k = 0; k < L; ++k) {
       const ld_t a = -2.0L * kPi * (ld_t)k / (ld_t)L;
       tw[k].x = (T)cosl(a); tw[k].y = (T)sinl(a);
     }
     for (int k = 0; k < n; ++k) {
       const ld_t a = kPi * (ld_t)k / (2.0L * (ld_t)n);
-      dctw[k].x = (T)cosl(a); dctw[k].y = (T)sinl(a);
-      scale[k] = (T)sqrtl((k == 0 ? 1.0L : 2.0L) / (ld_t)n);
+      const ld_t sk = sqrtl((k == 0 ? 1.0L : 2.0L) / (ld_t)n);
+      dct2w[k].x = (T)(sk * cosl(a)); dct2w[k].y = (T)(sk * sinl(a));
+      dct3w[k].x = (T)(cosl(a) / (sk * n)); dct3w[k].y = (T)(sinl(a) / (sk * n));
       const ld_t sh = sinl(a);
-      lam[k] = (double)(4.0L * sh * sh);  // 2 - 2 cos(pi k / n), cancellation-free
+      lam[k] = (T)(4.0L * sh * sh);  // 2 - 2 cos(pi k / n), cancellation-free
     }
-    lam[0] = 0.0;
+    lam[0] = (T)0;
+    // twiddle blocks of the compile-time plan (fft_stages_s): stage s >= 1 with
+    // stride NS and radix R stores W_{NS R}^k for k < NS
+    std::vector<C> stw;
+    if (!blue && (L & (L - 1)) == 0 && L >= 512) {
+      const int big = emax >= 16 ? 16 : 8;
+      int rem = L;
+      while (rem > 1 && rem % big == 0) rem /= big;
+      int ns = rem == 1 ? big : rem;  // first (twiddle-free) radix
+      while (ns < L) {
+        const int R = big;
+        for (int k = 0; k < ns; ++k) {
+          const ld_t a = -2.0L * kPi * (ld_t)k / (ld_t)(ns * R);
+          C c; c.x = (T)cosl(a); c.y = (T)sinl(a);
+          stw.push_back(c);
+        }
+        ns *= R;
+      }
+    }
     if (blue) {
       std::vector<std::complex<ld_t>> h(L, std::complex<ld_t>(0, 0));
       for (int k = 0; k < n; ++k) {
@@ -148,8 +166,8 @@ struct HostPlan {
       }
     }
     int rc;
-    if ((rc = upload(tw, &dev.tw)) || (rc = upload(dctw, &dev.dctw)) || (rc = upload(scale, &dev.scale)) ||
-        (rc = upload(lam, &dev.lam)))
+    if ((rc = upload(tw, &dev.tw)) || (rc = upload(dct2w, &dev.dct2w)) || (rc = upload(dct3w, &dev.dct3w)) ||
+        (rc = upload(lam, &dev.lam)) || (rc = upload(stw, &dev.stw)))
       return rc;
     if (blue && ((rc = upload(chirp, &dev.chirp)) || (rc = upload(filt, &dev.filt)))) return rc;
     return PU_OK;
@@ -173,7 +191,7 @@ struct HostPlan {
   // threads for `nseq` sequences: at least one whole sequence per stage,
   // at most the instantiation's launch bound (larger groups run sequentially)
   int max_threads() const {
-    const bool stat = (dev.L & (dev.L - 1)) == 0 && dev.L >= 512 && dev.L <= (emax == 16 ? 16384 : 8192);
+    const bool stat = !dev.bluestein && (dev.L & (dev.L - 1)) == 0 && dev.L >= 512 && dev.L <= (emax == 16 ? 16384 : 8192);
     return fft_max_threads(stat ? dev.L : 0, emax);
   }
   int threads_for(int nseq) const {
@@ -190,9 +208,6 @@ template <typename T>
 struct DctOps {
   cudaError_t (*set_attrs)(size_t, size_t);
   decltype(&DctLaunch<T, 0>::rows_plain) rows_plain;
-  decltype(&DctLaunch<T, 0>::rows_init) rows_init;
-  decltype(&DctLaunch<T, 0>::rows_update) rows_update;
-  decltype(&DctLaunch<T, 0>::rows_submean) rows_submean;
   decltype(&DctLaunch<T, 0>::rows_inv) rows_inv;
   decltype(&DctLaunch<T, 0>::cols) cols;
   int ls;
@@ -201,12 +216,11 @@ struct DctOps {
 template <typename T, int LS>
 static DctOps<T> make_ops() {
   using D = DctLaunch<T, LS>;
-  return DctOps<T>{&D::set_attrs, &D::rows_plain, &D::rows_init, &D::rows_update, &D::rows_submean,
-                   &D::rows_inv, &D::cols, LS};
+  return DctOps<T>{&D::set_attrs, &D::rows_plain, &D::rows_inv, &D::cols, LS};
 }
 
 template <typename T>
-static DctOps<T> ops_for(int L) {
+static DctOps<T> ops_for(int L) {  // L = internal length of a non-Bluestein plan, else 0
   switch (L) {
     case 512: return make_ops<T, 512>();
     case 1024: return make_ops<T, 1024>();
@@ -266,7 +280,7 @@ struct Timer {
   }
 };
 
-enum TimeKind { TK_START = 0, TK_K1, TK_K2, TK_K3, TK_K4, TK_UPD, TK_WEIGHTS, TK_CAND, TK_HPAIR, TK_ACCEPT, TK_OTHER };
+enum TimeKind { TK_START = 0, TK_K1, TK_K2, TK_K3, TK_K4, TK_UPD, TK_WEIGHTS, TK_CAND, TK_HPAIR, TK_ACCEPT, TK_K2B };
 
 static const size_t kSmemLimit = 227 * 1024 - 4096;  // leave room for static reduction scratch
 
@@ -317,7 +331,10 @@ struct Impl : HandleBase {
     row_threads = prow.threads_for(c);
     row_smem = prow.smem_for(c);
     // column kernels: panel of W = 2c columns; prefer 32-byte row segments
-    int cc = sizeof(T) == 4 ? 4 : 2;
+    // 2 sequences (W = 4 columns) per CTA keeps two CTAs resident per SM; the
+    // spectral plane is L2-resident between K2b and K4, so 16-byte (fp32) row
+    // segments cost L2, not HBM, efficiency
+    int cc = 2;
     cc = std::min(cc, std::max(1, (m + 1) / 2));
     while (cc > 1 && (pcol.threads_for(cc) > pcol.max_threads() || pcol.smem_for(cc) > kSmemLimit)) --cc;
     if (pcol.threads_for(cc) > pcol.max_threads() || pcol.smem_for(cc) > kSmemLimit)
@@ -328,7 +345,7 @@ struct Impl : HandleBase {
     // element-wise kernels: block-strided rows, thread-strided columns
     ew_threads = std::min(256, std::max(32, (m + 31) / 32 * 32));
     ew_grid = std::min(n, 148 * 8);
-    rs.stride = std::max(std::max(ew_grid, (n + rows_per_cta - 1) / rows_per_cta),
+    rs.stride = std::max(std::max(148 * 8, (n + rows_per_cta - 1) / rows_per_cta),
                          (m + cols_per_cta - 1) / cols_per_cta) + 1;
     PU_CUDA(cudaMalloc(&rs.partials, sizeof(double) * PU_MAX_SUMS * rs.stride));
     PU_CUDA(cudaMalloc(&rs.ticket, sizeof(unsigned int) * 32));
@@ -340,8 +357,8 @@ struct Impl : HandleBase {
   static constexpr int EM = sizeof(T) == 4 ? 16 : 8;
 
   int set_smem_attrs() {
-    rops = ops_for<T>(prow.dev.L);
-    cops = ops_for<T>(pcol.dev.L);
+    rops = ops_for<T>(prow.dev.bluestein ? 0 : prow.dev.L);
+    cops = ops_for<T>(pcol.dev.bluestein ? 0 : pcol.dev.L);
     // the attribute is per kernel (process-wide): always raise it to the cap so
     // that handles of different sizes sharing an instantiation never shrink it
     PU_CUDA(rops.set_attrs(kSmemLimit, kSmemLimit));
@@ -357,31 +374,41 @@ struct Impl : HandleBase {
 
   // ---- preconditioner passes ----
   int sylvester(const T* r, T* z, T* spec, cudaStream_t st) {
-    PU_DCT(rops.rows_plain(rl(st), g, prow.dev, rows_per_cta, r, spec, rs, S_K2));
+    PU_DCT(rops.rows_plain(rl(st), g, prow.dev, rows_per_cta, r, spec, nullptr, rs, S_K2));
     PU_DCT(cops.cols(MODE_API, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, nullptr, rs, S_K3, 0));
     PU_DCT(rops.rows_inv(rl(st), g, prow.dev, rows_per_cta, spec, z, nullptr));
     return PU_OK;
   }
 
+  int vec_grid() const {
+    const long long chunks = (long long)g.n * ((g.m + 3) / 4);
+    return (int)std::max<long long>(1, std::min<long long>((chunks + 255) / 256, 148 * 8));
+  }
+
+  // One fused PCG solve (pcg.py:47-116); 5 kernels per iteration:
+  // K1 p/Ap/p'Ap, K2a residual update + slack precond + norms, K2b row DCT-II,
+  // K3 column DCT pair + spectral division + rho, K4 row DCT-III.
   int pcg(const T* b, const T* x0, T* x, const T* dv, const T* dh, T* r, T* z, T* p0, T* p1, T* spec,
           int max_iters, double rel_tol, PcgCtrl* ctrl, double* norms, cudaStream_t st) {
+    const int vg = vec_grid();
     cudaEvent_t e = tm.begin(st);
-    k_pcg_start<T><<<ew_grid, ew_threads, 0, st>>>(g, b, x0, x, r, dv, dh, ctrl, norms, rel_tol, max_iters, rs,
-                                                   S_START);
+    k_pcg_start_v<T><<<vg, 256, 0, st>>>(g, b, x0, x, r, dv, dh, ctrl, norms, rel_tol, max_iters, rs, S_START);
     PU_LAUNCH_CHECK();
     tm.end(st, e, TK_START, -1);
-    {
-      RowsPcg<T, false, false, MODE_INIT> pol{nullptr, x, r, z, dv, dh, ctrl, norms, -1};
-      e = tm.begin(st);
-      PU_DCT(rops.rows_init(rl(st), g, prow.dev, rows_per_cta, spec, pol, rs, S_K2));
-      tm.end(st, e, TK_K2, -1);
-      e = tm.begin(st);
-      PU_DCT(cops.cols(MODE_INIT, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, ctrl, rs, S_K3, -1));
-      tm.end(st, e, TK_K3, -1);
-      e = tm.begin(st);
-      PU_DCT(rops.rows_inv(rl(st), g, prow.dev, rows_per_cta, spec, z, ctrl));
-      tm.end(st, e, TK_K4, -1);
-    }
+    // z = M r, rho = r.z (pcg.py:77-79)
+    e = tm.begin(st);
+    k_pcg_r_v<T, false, false, MODE_INIT><<<vg, 256, 0, st>>>(g, nullptr, dv, dh, x, r, z, ctrl, norms, rs, S_K2, -1);
+    PU_LAUNCH_CHECK();
+    tm.end(st, e, TK_K2, -1);
+    e = tm.begin(st);
+    PU_DCT(rops.rows_plain(rl(st), g, prow.dev, rows_per_cta, r, spec, ctrl, rs, S_K2B));
+    tm.end(st, e, TK_K2B, -1);
+    e = tm.begin(st);
+    PU_DCT(cops.cols(MODE_INIT, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, ctrl, rs, S_K3, -1));
+    tm.end(st, e, TK_K3, -1);
+    e = tm.begin(st);
+    PU_DCT(rops.rows_inv(rl(st), g, prow.dev, rows_per_cta, spec, z, ctrl));
+    tm.end(st, e, TK_K4, -1);
     T* pbuf[2] = {p0, p1};
     const int chunk = 64;
     for (int it = 0; it < max_iters; ++it) {
@@ -393,24 +420,27 @@ struct Impl : HandleBase {
       T* pn = pbuf[it & 1];
       const T* po = pbuf[(it + 1) & 1];
       e = tm.begin(st);
-      k_pcg_p<T><<<ew_grid, ew_threads, 0, st>>>(g, z, po, pn, dv, dh, ctrl, rs, S_K1, it);
+      k_pcg_p_v<T><<<vg, 256, 0, st>>>(g, z, po, pn, dv, dh, ctrl, rs, S_K1, it);
       PU_LAUNCH_CHECK();
       tm.end(st, e, TK_K1, it);
       if ((it + 1) % 50 == 0) {
         e = tm.begin(st);
-        k_pcg_update_sum<T><<<ew_grid, ew_threads, 0, st>>>(g, pn, dv, dh, x, r, ctrl, rs, S_UPD);
+        k_pcg_upd_sum_v<T><<<vg, 256, 0, st>>>(g, pn, dv, dh, x, r, ctrl, rs, S_UPD);
         PU_LAUNCH_CHECK();
         tm.end(st, e, TK_UPD, it);
-        RowsPcg<T, false, true, MODE_ITER> pol{pn, x, r, z, dv, dh, ctrl, norms, it};
         e = tm.begin(st);
-        PU_DCT(rops.rows_submean(rl(st), g, prow.dev, rows_per_cta, spec, pol, rs, S_K2));
+        k_pcg_r_v<T, false, true, MODE_ITER><<<vg, 256, 0, st>>>(g, pn, dv, dh, x, r, z, ctrl, norms, rs, S_K2, it);
+        PU_LAUNCH_CHECK();
         tm.end(st, e, TK_K2, it);
       } else {
-        RowsPcg<T, true, false, MODE_ITER> pol{pn, x, r, z, dv, dh, ctrl, norms, it};
         e = tm.begin(st);
-        PU_DCT(rops.rows_update(rl(st), g, prow.dev, rows_per_cta, spec, pol, rs, S_K2));
+        k_pcg_r_v<T, true, false, MODE_ITER><<<vg, 256, 0, st>>>(g, pn, dv, dh, x, r, z, ctrl, norms, rs, S_K2, it);
+        PU_LAUNCH_CHECK();
         tm.end(st, e, TK_K2, it);
       }
+      e = tm.begin(st);
+      PU_DCT(rops.rows_plain(rl(st), g, prow.dev, rows_per_cta, r, spec, ctrl, rs, S_K2B));
+      tm.end(st, e, TK_K2B, it);
       e = tm.begin(st);
       PU_DCT(cops.cols(MODE_ITER, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, ctrl, rs, S_K3, it));
       tm.end(st, e, TK_K3, it);
@@ -611,7 +641,7 @@ int pu_weights_hpair(pu_handle* h, const void* x, const void* cv, const void* ch
                      void* stream) {
   PU_DISPATCH(h, {
     cudaEvent_t te_ = I.tm.begin(ST(stream));
-    k_weights_hpair<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(x), CP(cv), CP(ch), CP(gv), CP(gh),
+    k_weights_hpair_v<T><<<I.vec_grid(), 256, 0, ST(stream)>>>(I.g, CP(x), CP(cv), CP(ch), CP(gv), CP(gh),
                                                                   CP(wpv), CP(wph), MP(wv), MP(wh), MP(dv), MP(dh),
                                                                   I.rs, S_WH, out);
     PU_LAUNCH_CHECK();
@@ -645,7 +675,7 @@ int pu_candidate_step(pu_handle* h, const void* x, const void* wv, const void* w
   if (!(lipschitz > 0)) return fail(PU_ERR_ARG, "lipschitz constant must be positive");
   PU_DISPATCH(h, {
     cudaEvent_t te_ = I.tm.begin(ST(stream));
-    k_candidate<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(x), CP(wv), CP(wh), CP(gv), CP(gh), CP(cv),
+    k_candidate_v<T><<<I.vec_grid(), 256, 0, ST(stream)>>>(I.g, CP(x), CP(wv), CP(wh), CP(gv), CP(gh), CP(cv),
                                                               CP(ch), (T)(-1.0 / lipschitz), MP(out));
     PU_LAUNCH_CHECK();
     I.tm.end(ST(stream), te_, TK_CAND, -1);
@@ -657,7 +687,7 @@ int pu_hpair_states(pu_handle* h, const void* xa, const void* xb, const void* wv
                     const void* gh, const void* cv, const void* ch, double* out, void* stream) {
   PU_DISPATCH(h, {
     cudaEvent_t te_ = I.tm.begin(ST(stream));
-    k_hpair_states<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(xa), CP(xb), CP(wv), CP(wh), CP(gv),
+    k_hpair_states_v<T><<<I.vec_grid(), 256, 0, ST(stream)>>>(I.g, CP(xa), CP(xb), CP(wv), CP(wh), CP(gv),
                                                                  CP(gh), CP(cv), CP(ch), I.rs, S_HPAIR, out);
     PU_LAUNCH_CHECK();
     I.tm.end(ST(stream), te_, TK_HPAIR, -1);
@@ -671,7 +701,7 @@ int pu_accept_center(pu_handle* h, const void* xa, const void* xb, const double*
   if (dst == xa || dst == xb) return fail(PU_ERR_ARG, "dst must not alias xa or xb");
   PU_DISPATCH(h, {
     cudaEvent_t te_ = I.tm.begin(ST(stream));
-    k_accept<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(xa), CP(xb), sel, MP(dst), CP(wv), CP(wh),
+    k_accept_v<T><<<I.vec_grid(), 256, 0, ST(stream)>>>(I.g, CP(xa), CP(xb), sel, MP(dst), CP(wv), CP(wh),
                                                            CP(gv), CP(gh), CP(cv), CP(ch), I.rs, S_ACC, out);
     PU_LAUNCH_CHECK();
     I.tm.end(ST(stream), te_, TK_ACCEPT, -1);

@@ -23,16 +23,10 @@ struct DctLaunch {
   static cudaError_t set_attrs(size_t row_smem, size_t col_smem);
 
   static cudaError_t rows_plain(const XLaunch& c, const Grid& g, const FftPlan<T>& pl, int rpc, const T* src, T* out,
-                                RedScratch rs, int site);
-  static cudaError_t rows_init(const XLaunch& c, const Grid& g, const FftPlan<T>& pl, int rpc, T* out,
-                               const RowsPcg<T, false, false, MODE_INIT>& pol, RedScratch rs, int site);
-  static cudaError_t rows_update(const XLaunch& c, const Grid& g, const FftPlan<T>& pl, int rpc, T* out,
-                                 const RowsPcg<T, true, false, MODE_ITER>& pol, RedScratch rs, int site);
-  static cudaError_t rows_submean(const XLaunch& c, const Grid& g, const FftPlan<T>& pl, int rpc, T* out,
-                                  const RowsPcg<T, false, true, MODE_ITER>& pol, RedScratch rs, int site);
+                                const PcgCtrl* ctrl, RedScratch rs, int site);
   static cudaError_t rows_inv(const XLaunch& c, const Grid& g, const FftPlan<T>& pl, int rpc, const T* in, T* out,
                               const PcgCtrl* ctrl);
-  static cudaError_t cols(int mode, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const double* lam_cols,
+  static cudaError_t cols(int mode, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const T* lam_cols,
                           int cpc, T* data, PcgCtrl* ctrl, RedScratch rs, int site, int it);
 };
 
@@ -43,9 +37,6 @@ cudaError_t DctLaunch<T, LS>::set_attrs(size_t row_smem, size_t col_smem) {
 #define PU_ATTR(K, S) \
   if ((e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(S))) != cudaSuccess) return e;
   PU_ATTR((k_rows_fwd<T, EM, LS, RowsPlain<T>>), row_smem);
-  PU_ATTR((k_rows_fwd<T, EM, LS, RowsPcg<T, false, false, MODE_INIT>>), row_smem);
-  PU_ATTR((k_rows_fwd<T, EM, LS, RowsPcg<T, true, false, MODE_ITER>>), row_smem);
-  PU_ATTR((k_rows_fwd<T, EM, LS, RowsPcg<T, false, true, MODE_ITER>>), row_smem);
   PU_ATTR((k_rows_inv<T, EM, LS>), row_smem);
   PU_ATTR((k_cols_spec<T, EM, LS, MODE_API>), col_smem);
   PU_ATTR((k_cols_spec<T, EM, LS, MODE_INIT>), col_smem);
@@ -56,33 +47,9 @@ cudaError_t DctLaunch<T, LS>::set_attrs(size_t row_smem, size_t col_smem) {
 
 template <typename T, int LS>
 cudaError_t DctLaunch<T, LS>::rows_plain(const XLaunch& c, const Grid& g, const FftPlan<T>& pl, int rpc,
-                                         const T* src, T* out, RedScratch rs, int site) {
-  RowsPlain<T> pol{src};
+                                         const T* src, T* out, const PcgCtrl* ctrl, RedScratch rs, int site) {
+  RowsPlain<T> pol{src, ctrl};
   k_rows_fwd<T, EM, LS, RowsPlain<T>><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, rpc, out, pol, rs, site);
-  return cudaGetLastError();
-}
-
-template <typename T, int LS>
-cudaError_t DctLaunch<T, LS>::rows_init(const XLaunch& c, const Grid& g, const FftPlan<T>& pl, int rpc, T* out,
-                                        const RowsPcg<T, false, false, MODE_INIT>& pol, RedScratch rs, int site) {
-  k_rows_fwd<T, EM, LS, RowsPcg<T, false, false, MODE_INIT>><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, rpc, out, pol,
-                                                                                              rs, site);
-  return cudaGetLastError();
-}
-
-template <typename T, int LS>
-cudaError_t DctLaunch<T, LS>::rows_update(const XLaunch& c, const Grid& g, const FftPlan<T>& pl, int rpc, T* out,
-                                          const RowsPcg<T, true, false, MODE_ITER>& pol, RedScratch rs, int site) {
-  k_rows_fwd<T, EM, LS, RowsPcg<T, true, false, MODE_ITER>><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, rpc, out, pol,
-                                                                                             rs, site);
-  return cudaGetLastError();
-}
-
-template <typename T, int LS>
-cudaError_t DctLaunch<T, LS>::rows_submean(const XLaunch& c, const Grid& g, const FftPlan<T>& pl, int rpc, T* out,
-                                           const RowsPcg<T, false, true, MODE_ITER>& pol, RedScratch rs, int site) {
-  k_rows_fwd<T, EM, LS, RowsPcg<T, false, true, MODE_ITER>><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, rpc, out, pol,
-                                                                                             rs, site);
   return cudaGetLastError();
 }
 
@@ -95,7 +62,7 @@ cudaError_t DctLaunch<T, LS>::rows_inv(const XLaunch& c, const Grid& g, const Ff
 
 template <typename T, int LS>
 cudaError_t DctLaunch<T, LS>::cols(int mode, const XLaunch& c, const Grid& g, const FftPlan<T>& pl,
-                                   const double* lam_cols, int cpc, T* data, PcgCtrl* ctrl, RedScratch rs, int site,
+                                   const T* lam_cols, int cpc, T* data, PcgCtrl* ctrl, RedScratch rs, int site,
                                    int it) {
   if (mode == MODE_API)
     k_cols_spec<T, EM, LS, MODE_API><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it);

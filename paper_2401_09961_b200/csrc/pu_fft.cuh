@@ -21,15 +21,15 @@ namespace pu {
 
 // Per-instantiation launch bounds: a stage holds one whole sequence, so a CTA
 // needs L / EMAX threads; below that, 256 threads at <= 128 registers (two
-// CTAs per SM).  LS = 0 (runtime plan) allows 512 threads.
+// CTAs per SM).  LS = 0 (runtime plans: odd sizes, Bluestein) allows 1024.
 __host__ __device__ constexpr int fft_max_threads(int LS, int EMAX) {
-  return LS == 0 ? 512 : (LS / EMAX > 256 ? LS / EMAX : 256);
+  return LS == 0 ? 1024 : (LS / EMAX > 256 ? LS / EMAX : 256);
 }
 __host__ __device__ constexpr int fft_min_blocks(int LS, int EMAX) {
   return fft_max_threads(LS, EMAX) <= 256 ? 2 : 1;
 }
 
-// Runtime plan for one transform length (built on the host, pu_dct_plan.cu).
+// Plan for one transform length (built on the host, pu_api.cu HostPlan).
 template <typename T>
 struct FftPlan {
   int n;                  // transform length
@@ -39,12 +39,13 @@ struct FftPlan {
   int rad[PU_FFT_MAX_STAGES];
   int ldseq;              // shared-memory stride between sequences (padded)
   int cap;                // complex values per thread a stage can hold (min R*floor(EMAX/R))
-  const cplx<T>* tw;      // [L]  exp(-2 pi i k / L)
-  const cplx<T>* chirp;   // [n]  exp(-i pi k^2 / n)          (Bluestein)
-  const cplx<T>* filt;    // [L]  FFT_L(conj chirp, symmetric)/L (Bluestein)
-  const cplx<T>* dctw;    // [n]  (cos, sin)(pi k / 2n)
-  const T* scale;         // [n]  s_k: sqrt(1/n) for k = 0, sqrt(2/n) otherwise
-  const double* lam;      // [n]  2 - 2 cos(pi k / n), lam[0] = 0
+  const cplx<T>* tw;      // [L]  exp(-2 pi i k / L)                      (runtime plan)
+  const cplx<T>* stw;     // per-stage W_{NS R}^k, k < NS, of the static plan (stage >= 1)
+  const cplx<T>* chirp;   // [n]  exp(-i pi k^2 / n)                     (Bluestein)
+  const cplx<T>* filt;    // [L]  FFT_L(conj chirp, symmetric)/L          (Bluestein)
+  const cplx<T>* dct2w;   // [n]  s_k (cos, sin)(pi k / 2n)   DCT-II post, scale folded
+  const cplx<T>* dct3w;   // [n]  (cos, sin)(pi k / 2n) / (s_k n)  DCT-III pre, 1/n folded
+  const T* lam;           // [n]  2 - 2 cos(pi k / n) = 4 sin^2(pi k / 2n), lam[0] = 0
 };
 
 // Bank-conflict padding: one complex slot every 16.
@@ -286,8 +287,8 @@ __host__ __device__ constexpr int first_radix() {
   return rem == 1 ? big : rem;
 }
 
-template <typename T, int R, int EMAX, int L, int NS>
-__device__ __forceinline__ void fft_stage_s(cplx<T>* buf, int seq0, int nseq, const cplx<T>* __restrict__ tw) {
+template <typename T, int R, int EMAX, int L, int NS, int OFF>
+__device__ __forceinline__ void fft_stage_s(cplx<T>* buf, int seq0, int nseq, const cplx<T>* __restrict__ stw) {
   constexpr int Q = EMAX / R;
   constexpr int NB = L / R;
   constexpr int LD = ldseq_for(L);
@@ -314,11 +315,15 @@ __device__ __forceinline__ void fft_stage_s(cplx<T>* buf, int seq0, int nseq, co
         for (int r = 0; r < R; ++r) v[q][r] = buf[base + spad(j + r * NB)];
       }
       if constexpr (NS > 1) {
+        // twiddles W_{NS R}^{r k}: one table load (w = W^k), powers by a
+        // balanced product tree (depth <= log2 R, a few ulp)
         const int k = j % NS;
-        constexpr int TWS = L / (NS * R);
-        const cplx<T>* twk = tw + k * TWS;
+        cplx<T> w[R];
+        w[1] = __ldg(stw + OFF + k);
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[q][r] = cmul<T>(v[q][r], __ldg(twk + (r - 1) * k * TWS));
+        for (int r = 2; r < R; ++r) w[r] = cmul<T>(w[r / 2], w[r - r / 2]);
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[q][r] = cmul<T>(v[q][r], w[r]);
         ob[q] = (j - k) * R + k;
       } else {
         ob[q] = j * R;
@@ -349,12 +354,14 @@ __device__ __forceinline__ void fft_stage_s(cplx<T>* buf, int seq0, int nseq, co
   __syncthreads();
 }
 
-template <typename T, int EMAX, int L, int NS>
-__device__ __forceinline__ void fft_stages_s(cplx<T>* buf, int seq0, int nseq, const cplx<T>* tw) {
+// Stage s >= 1 of the static plan reads W_{NS R}^k, k < NS, from its block at
+// OFF; blocks are laid out in stage order (mirrored by HostPlan::build).
+template <typename T, int EMAX, int L, int NS, int OFF>
+__device__ __forceinline__ void fft_stages_s(cplx<T>* buf, int seq0, int nseq, const cplx<T>* stw) {
   if constexpr (NS < L) {
     constexpr int R = (NS == 1) ? first_radix<L, EMAX>() : (EMAX >= 16 ? 16 : 8);
-    fft_stage_s<T, R, EMAX, L, NS>(buf, seq0, nseq, tw);
-    fft_stages_s<T, EMAX, L, NS * R>(buf, seq0, nseq, tw);
+    fft_stage_s<T, R, EMAX, L, NS, OFF>(buf, seq0, nseq, stw);
+    fft_stages_s<T, EMAX, L, NS * R, (NS == 1 ? OFF : OFF + NS)>(buf, seq0, nseq, stw);
   }
 }
 
@@ -364,7 +371,7 @@ template <typename T, int EMAX, int LS>
 __device__ __forceinline__ void fft_internal(cplx<T>* buf, int nseq, const FftPlan<T>& pl) {
   if constexpr (LS > 0) {
     const int grp = max(1, (int)(blockDim.x * EMAX) / LS);
-    for (int sg = 0; sg < nseq; sg += grp) fft_stages_s<T, EMAX, LS, 1>(buf, sg, min(grp, nseq - sg), pl.tw);
+    for (int sg = 0; sg < nseq; sg += grp) fft_stages_s<T, EMAX, LS, 1, 0>(buf, sg, min(grp, nseq - sg), pl.stw);
   } else {
     fft_pow<T, EMAX>(buf, nseq, pl);
   }
@@ -415,39 +422,42 @@ __device__ __forceinline__ PairOut<T> dct2_post(cplx<T> zk, cplx<T> znk, int k, 
   const T h = (T)0.5;
   const T reA = h * (zk.x + znk.x), imA = h * (zk.y - znk.y);
   const T reB = h * (zk.y + znk.y), imB = -h * (zk.x - znk.x);
-  const cplx<T> wk = __ldg(pl.dctw + k), wn = __ldg(pl.dctw + nk);
-  const T sk = __ldg(pl.scale + k), sn = __ldg(pl.scale + nk);
+  const cplx<T> wk = __ldg(pl.dct2w + k), wn = __ldg(pl.dct2w + nk);  // s_k e^{i theta_k}
   PairOut<T> o;
-  o.a_k = sk * (wk.x * reA + wk.y * imA);
-  o.b_k = sk * (wk.x * reB + wk.y * imB);
-  o.a_nk = sn * (wn.x * reA - wn.y * imA);
-  o.b_nk = sn * (wn.x * reB - wn.y * imB);
+  o.a_k = wk.x * reA + wk.y * imA;
+  o.b_k = wk.x * reB + wk.y * imB;
+  o.a_nk = wn.x * reA - wn.y * imA;
+  o.b_nk = wn.x * reB - wn.y * imB;
   return o;
 }
 
 // DCT-III pre-processing: from orthonormal coefficients (a_k, a_nk, b_k, b_nk)
 // build conj(Z'_k), conj(Z'_nk) where Z' = V_a + i V_b and
-// V_k = e^{i pi k/2n} (Y_k - i Y_{n-k}), Y = X / s.  A forward FFT of the
-// conjugated data followed by conj()/n is the inverse FFT.
+// V_k = e^{i pi k/2n} (Y_k - i Y_{n-k}) / n, Y = X / s (s_k = s_{n-k} for
+// k >= 1; V_0 = Y_0 / n).  A forward FFT of the conjugated data is then
+// n * conj(IFFT), so the DCT-III output is (Re, -Im) of it directly.
 template <typename T>
 __device__ __forceinline__ void dct3_pre(T ak, T ank, T bk, T bnk, int k, int nk, const FftPlan<T>& pl,
                                          cplx<T>& out_k, cplx<T>& out_nk) {
-  const T isk = (T)1 / __ldg(pl.scale + k), isn = (T)1 / __ldg(pl.scale + nk);
-  const T yak = ak * isk, yank = ank * isn, ybk = bk * isk, ybnk = bnk * isn;
-  const cplx<T> wk = __ldg(pl.dctw + k), wn = __ldg(pl.dctw + nk);
+  const cplx<T> wk = __ldg(pl.dct3w + k);
   T vaRe, vaIm, vbRe, vbIm;
   if (k == 0) {
-    vaRe = yak; vaIm = 0; vbRe = ybk; vbIm = 0;
+    vaRe = ak * wk.x; vaIm = 0; vbRe = bk * wk.x; vbIm = 0;
   } else {
-    vaRe = wk.x * yak + wk.y * yank; vaIm = wk.y * yak - wk.x * yank;
-    vbRe = wk.x * ybk + wk.y * ybnk; vbIm = wk.y * ybk - wk.x * ybnk;
+    vaRe = wk.x * ak + wk.y * ank; vaIm = wk.y * ak - wk.x * ank;
+    vbRe = wk.x * bk + wk.y * bnk; vbIm = wk.y * bk - wk.x * bnk;
   }
   out_k = mk<T>(vaRe - vbIm, -(vaIm + vbRe));  // conj(Va + i Vb)
   if (nk != k) {
-    const T uaRe = wn.x * yank + wn.y * yak, uaIm = wn.y * yank - wn.x * yak;
-    const T ubRe = wn.x * ybnk + wn.y * ybk, ubIm = wn.y * ybnk - wn.x * ybk;
+    const cplx<T> wn = __ldg(pl.dct3w + nk);
+    const T uaRe = wn.x * ank + wn.y * ak, uaIm = wn.y * ank - wn.x * ak;
+    const T ubRe = wn.x * bnk + wn.y * bk, ubIm = wn.y * bnk - wn.x * bk;
     out_nk = mk<T>(uaRe - ubIm, -(uaIm + ubRe));
   }
 }
+
+// correctly rounded reciprocal
+__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
 
 }  // namespace pu

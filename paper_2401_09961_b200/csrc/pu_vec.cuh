@@ -1,0 +1,560 @@
+// Vectorised element-wise PCG kernels (sm_100a).
+//
+// Each thread owns a chunk of 4 consecutive cells of one row and moves every
+// plane as one 16-byte (fp32) or two 16-byte (fp64) accesses, so a warp keeps
+// ~20 independent loads in flight instead of one scalar chain per cell.  Pitch
+// padding (j >= m) is read as zero and written back as zero.
+//
+//   k_pcg_p_v     K1: p <- beta p + z (z at it = 0); A p from the stencil of the
+//                 new p (recomputed at the neighbours); p'Ap; alpha (pcg.py:82-89)
+//   k_pcg_r_v     K2a: x += alpha p; r -= alpha A p; optional mean re-projection;
+//                 ||r||; z_s = r_s / (d + 1/tau); rho_s (pcg.py:90-104,
+//                 preconditioner.py:115); the row DCT of r_u runs next (K2b)
+//   k_pcg_start_v x = x0, r = b - A x0, ||b||, ||r0|| (pcg.py:59-75)
+#pragma once
+
+#include "pu_kernels.cuh"
+
+namespace pu {
+
+template <typename T>
+struct Q4 {
+  T a[4];
+};
+
+__device__ __forceinline__ Q4<float> ld4(const float* p) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  return Q4<float>{{v.x, v.y, v.z, v.w}};
+}
+__device__ __forceinline__ Q4<double> ld4(const double* p) {
+  const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+  return Q4<double>{{a.x, a.y, b.x, b.y}};
+}
+__device__ __forceinline__ Q4<float> ldg4(const float* p) {
+  const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+  return Q4<float>{{v.x, v.y, v.z, v.w}};
+}
+__device__ __forceinline__ Q4<double> ldg4(const double* p) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  return Q4<double>{{a.x, a.y, b.x, b.y}};
+}
+__device__ __forceinline__ void st4(float* p, const Q4<float>& q) {
+  *reinterpret_cast<float4*>(p) = make_float4(q.a[0], q.a[1], q.a[2], q.a[3]);
+}
+__device__ __forceinline__ void st4(double* p, const Q4<double>& q) {
+  reinterpret_cast<double2*>(p)[0] = make_double2(q.a[0], q.a[1]);
+  reinterpret_cast<double2*>(p)[1] = make_double2(q.a[2], q.a[3]);
+}
+template <typename T>
+__device__ __forceinline__ Q4<T> zero4() {
+  return Q4<T>{{(T)0, (T)0, (T)0, (T)0}};
+}
+
+// chunk loop: chunk q covers cells (i, 4c .. 4c+3), c < cpr = ceil(m / 4)
+#define PU_FOR_CHUNKS(g, i, j0)                                                            \
+  for (long long q_ = (long long)blockIdx.x * blockDim.x + threadIdx.x,                   \
+                 cpr_ = ((g).m + 3) / 4, nq_ = (long long)(g).n * cpr_;                  \
+       q_ < nq_; q_ += (long long)gridDim.x * blockDim.x)                                   \
+    for (int i = (int)(q_ / cpr_), j0 = (int)(q_ - (long long)i * cpr_) * 4, once_ = 1; once_; once_ = 0)
+
+// A x at the 4 cells of a chunk given the chunk's x (centre, above, below,
+// left/right neighbours).  ok[k]: cell exists (j < m).
+template <typename T>
+struct Stencil4 {
+  Q4<T> u, v, h;      // x at (i, j0..j0+3)
+  Q4<T> ua, va;       // x_u, x_v at (i-1, .) (zero if i == 0)
+  Q4<T> ub;           // x_u at (i+1, .)      (zero if i == n-1)
+  T ul, ur, hl;       // x_u at (i, j0-1), (i, j0+4); x_h at (i, j0-1)
+};
+
+template <typename T>
+__device__ __forceinline__ void apply4(const Grid& g, int i, int j0, const Stencil4<T>& s, const Q4<T>& dv,
+                                       const Q4<T>& dh, Q4<T>& au, Q4<T>& av, Q4<T>& ah) {
+  const T inv = (T)g.inv_tau;
+  const bool hasv = i < g.n - 1, hasa = i > 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int j = j0 + k;
+    const T xu = s.u.a[k];
+    const T left = (k == 0) ? s.ul : s.u.a[k - 1];
+    const T right = (k == 3) ? s.ur : s.u.a[k + 1];
+    const T hleft = (k == 0) ? s.hl : s.h.a[k - 1];
+    T su = 0, rv = 0, rvm = 0, ut = 0, rh = 0, rhm = 0;
+    const bool hash = j < g.m - 1;
+    if (hasv) { su = s.ub.a[k] - xu; rv = su - s.v.a[k]; }
+    if (hasa) { rvm = (xu - s.ua.a[k]) - s.va.a[k]; }
+    if (hash) { ut = right - xu; rh = ut - s.h.a[k]; }
+    if (j > 0) { rhm = (xu - left) - hleft; }
+    const bool ok = j < g.m;
+    au.a[k] = ok ? inv * ((rvm - rv) + (rhm - rh)) : (T)0;
+    av.a[k] = (ok && hasv) ? dv.a[k] * s.v.a[k] + inv * (s.v.a[k] - su) : (T)0;
+    ah.a[k] = (ok && hash) ? dh.a[k] * s.h.a[k] + inv * (s.h.a[k] - ut) : (T)0;
+  }
+}
+
+// scalar neighbour load that tolerates the grid edge
+template <typename T>
+__device__ __forceinline__ T ldg_or0(const T* p, bool ok) { return ok ? __ldg(p) : (T)0; }
+
+// ---------------------------------------------------------------------------
+// K1
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) k_pcg_p_v(Grid g, const T* __restrict__ z, const T* __restrict__ pold,
+                                                 T* __restrict__ pnew, const T* __restrict__ dv,
+                                                 const T* __restrict__ dh, PcgCtrl* ctrl, RedScratch rs, int site,
+                                                 int it) {
+  if (ctrl->done) return;
+  const bool first = it == 0;
+  const T beta = (T)ctrl->beta;
+  const long long P = g.plane, ld = g.ld;
+  auto upd4 = [&](long long o) -> Q4<T> {  // p_new = beta p_old + z  (pcg.py:107-108)
+    Q4<T> zz = ldg4(z + o);
+    if (first) return zz;
+    const Q4<T> pp = ldg4(pold + o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) zz.a[k] = add_rn(mul_rn(beta, pp.a[k]), zz.a[k]);
+    return zz;
+  };
+  auto upd1 = [&](long long o, bool ok) -> T {
+    if (!ok) return (T)0;
+    const T zz = __ldg(z + o);
+    return first ? zz : add_rn(mul_rn(beta, __ldg(pold + o)), zz);
+  };
+  double acc[1] = {0.0};
+  PU_FOR_CHUNKS(g, i, j0) {
+    const long long o = (long long)i * ld + j0;
+    Stencil4<T> s;
+    s.u = upd4(o);
+    s.v = upd4(o + P);
+    s.h = upd4(o + 2 * P);
+    s.ua = i > 0 ? upd4(o - ld) : zero4<T>();
+    s.va = i > 0 ? upd4(o - ld + P) : zero4<T>();
+    s.ub = i < g.n - 1 ? upd4(o + ld) : zero4<T>();
+    s.ul = upd1(o - 1, j0 > 0);
+    s.hl = upd1(o - 1 + 2 * P, j0 > 0);
+    s.ur = upd1(o + 4, j0 + 4 < g.m);
+    const Q4<T> d1 = ldg4(dv + o), d2 = ldg4(dh + o);
+    Q4<T> au, av, ah;
+    apply4<T>(g, i, j0, s, d1, d2, au, av, ah);
+    st4(pnew + o, s.u);
+    st4(pnew + o + P, s.v);
+    st4(pnew + o + 2 * P, s.h);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      acc[0] += (double)s.u.a[k] * au.a[k] + (double)s.v.a[k] * av.a[k] + (double)s.h.a[k] * ah.a[k];
+  }
+  double tot[1];
+  if (grid_reduce<1>(acc, rs, site, tot) && threadIdx.x == 0) {
+    const double pap = tot[0];
+    ctrl->pap = pap;
+    if (!isfinite(pap)) {
+      ctrl->breakdown = it; ctrl->bkind = 1; ctrl->done = 1;
+    } else if (pap <= PU_TINY_CURVATURE) {
+      ctrl->converged = ctrl->rn <= ctrl->thr; ctrl->done = 1;
+    } else {
+      ctrl->alpha = ctrl->rho / pap;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2a: residual update + slack preconditioner + norms.
+// UPDATE: x += alpha p, r -= alpha A p.  SUBMEAN: r_u -= ctrl->mean_ru.
+// MODE_ITER finaliser: ||r|| exits (pcg.py:94-100); MODE_INIT: rho_s only.
+// ---------------------------------------------------------------------------
+template <typename T, bool UPDATE, bool SUBMEAN, int MODE>
+__global__ void __launch_bounds__(256) k_pcg_r_v(Grid g, const T* __restrict__ p, const T* __restrict__ dv,
+                                                 const T* __restrict__ dh, T* __restrict__ x, T* __restrict__ r,
+                                                 T* __restrict__ z, PcgCtrl* ctrl, double* res_norms, RedScratch rs,
+                                                 int site, int it) {
+  if (ctrl->done) return;
+  const long long P = g.plane, ld = g.ld;
+  const T alpha = (T)ctrl->alpha, nalpha = (T)(-ctrl->alpha);
+  const T mean = (T)ctrl->mean_ru;
+  const T inv = (T)g.inv_tau;
+  double acc[2] = {0.0, 0.0};
+  PU_FOR_CHUNKS(g, i, j0) {
+    const long long o = (long long)i * ld + j0;
+    Q4<T> ru, rv, rh;
+    const Q4<T> d1 = ldg4(dv + o), d2 = ldg4(dh + o);
+    if (UPDATE) {
+      Stencil4<T> s;
+      s.u = ldg4(p + o);
+      s.v = ldg4(p + o + P);
+      s.h = ldg4(p + o + 2 * P);
+      s.ua = i > 0 ? ldg4(p + o - ld) : zero4<T>();
+      s.va = i > 0 ? ldg4(p + o - ld + P) : zero4<T>();
+      s.ub = i < g.n - 1 ? ldg4(p + o + ld) : zero4<T>();
+      s.ul = ldg_or0(p + o - 1, j0 > 0);
+      s.hl = ldg_or0(p + o - 1 + 2 * P, j0 > 0);
+      s.ur = ldg_or0(p + o + 4, j0 + 4 < g.m);
+      Q4<T> au, av, ah;
+      apply4<T>(g, i, j0, s, d1, d2, au, av, ah);
+      Q4<T> xu = ld4(x + o), xv = ld4(x + o + P), xh = ld4(x + o + 2 * P);
+      ru = ld4(r + o); rv = ld4(r + o + P); rh = ld4(r + o + 2 * P);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {  // pcg.py:90-91
+        xu.a[k] = add_rn(xu.a[k], mul_rn(alpha, s.u.a[k]));
+        xv.a[k] = add_rn(xv.a[k], mul_rn(alpha, s.v.a[k]));
+        xh.a[k] = add_rn(xh.a[k], mul_rn(alpha, s.h.a[k]));
+        ru.a[k] = add_rn(ru.a[k], mul_rn(nalpha, au.a[k]));
+        rv.a[k] = add_rn(rv.a[k], mul_rn(nalpha, av.a[k]));
+        rh.a[k] = add_rn(rh.a[k], mul_rn(nalpha, ah.a[k]));
+      }
+      st4(x + o, xu); st4(x + o + P, xv); st4(x + o + 2 * P, xh);
+      st4(r + o + P, rv); st4(r + o + 2 * P, rh);
+      if (!SUBMEAN) st4(r + o, ru);
+    } else {
+      ru = ld4(r + o); rv = ld4(r + o + P); rh = ld4(r + o + 2 * P);
+    }
+    if (SUBMEAN) {  // pcg.py:92-93
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ru.a[k] = (j0 + k < g.m) ? ru.a[k] - mean : (T)0;
+      st4(r + o, ru);
+    }
+    Q4<T> zv, zh;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
+      zv.a[k] = (i < g.n - 1 && j < g.m) ? rv.a[k] / (d1.a[k] + inv) : (T)0;
+      zh.a[k] = (j < g.m - 1) ? rh.a[k] / (d2.a[k] + inv) : (T)0;
+      acc[0] += (double)ru.a[k] * ru.a[k] + (double)rv.a[k] * rv.a[k] + (double)rh.a[k] * rh.a[k];
+      acc[1] += (double)rv.a[k] * zv.a[k] + (double)rh.a[k] * zh.a[k];
+    }
+    st4(z + o + P, zv);
+    st4(z + o + 2 * P, zh);
+  }
+  double tot[2];
+  if (grid_reduce<2>(acc, rs, site, tot) && threadIdx.x == 0) {
+    ctrl->rho_s = tot[1];
+    if (MODE == 2 /* MODE_ITER */) {
+      const double rn = sqrt(tot[0]);
+      ctrl->rn = rn;
+      if (!isfinite(rn)) {
+        ctrl->breakdown = it + 1; ctrl->bkind = 2; ctrl->done = 1;
+      } else {
+        res_norms[it + 1] = rn;
+        ctrl->iterations = it + 1;
+        if (rn <= ctrl->thr) { ctrl->converged = 1; ctrl->done = 1; }
+      }
+    }
+  }
+}
+
+// update + sum(r_u) for the every-50 re-projection (the mean is subtracted by
+// k_pcg_r_v<false, true, ...> next)
+template <typename T>
+__global__ void __launch_bounds__(256) k_pcg_upd_sum_v(Grid g, const T* __restrict__ p, const T* __restrict__ dv,
+                                                       const T* __restrict__ dh, T* __restrict__ x,
+                                                       T* __restrict__ r, PcgCtrl* ctrl, RedScratch rs, int site) {
+  if (ctrl->done) return;
+  const long long P = g.plane, ld = g.ld;
+  const T alpha = (T)ctrl->alpha, nalpha = (T)(-ctrl->alpha);
+  double acc[1] = {0.0};
+  PU_FOR_CHUNKS(g, i, j0) {
+    const long long o = (long long)i * ld + j0;
+    const Q4<T> d1 = ldg4(dv + o), d2 = ldg4(dh + o);
+    Stencil4<T> s;
+    s.u = ldg4(p + o);
+    s.v = ldg4(p + o + P);
+    s.h = ldg4(p + o + 2 * P);
+    s.ua = i > 0 ? ldg4(p + o - ld) : zero4<T>();
+    s.va = i > 0 ? ldg4(p + o - ld + P) : zero4<T>();
+    s.ub = i < g.n - 1 ? ldg4(p + o + ld) : zero4<T>();
+    s.ul = ldg_or0(p + o - 1, j0 > 0);
+    s.hl = ldg_or0(p + o - 1 + 2 * P, j0 > 0);
+    s.ur = ldg_or0(p + o + 4, j0 + 4 < g.m);
+    Q4<T> au, av, ah;
+    apply4<T>(g, i, j0, s, d1, d2, au, av, ah);
+    Q4<T> xu = ld4(x + o), xv = ld4(x + o + P), xh = ld4(x + o + 2 * P);
+    Q4<T> ru = ld4(r + o), rv = ld4(r + o + P), rh = ld4(r + o + 2 * P);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      xu.a[k] = add_rn(xu.a[k], mul_rn(alpha, s.u.a[k]));
+      xv.a[k] = add_rn(xv.a[k], mul_rn(alpha, s.v.a[k]));
+      xh.a[k] = add_rn(xh.a[k], mul_rn(alpha, s.h.a[k]));
+      ru.a[k] = add_rn(ru.a[k], mul_rn(nalpha, au.a[k]));
+      rv.a[k] = add_rn(rv.a[k], mul_rn(nalpha, av.a[k]));
+      rh.a[k] = add_rn(rh.a[k], mul_rn(nalpha, ah.a[k]));
+      acc[0] += (double)ru.a[k];
+    }
+    st4(x + o, xu); st4(x + o + P, xv); st4(x + o + 2 * P, xh);
+    st4(r + o, ru); st4(r + o + P, rv); st4(r + o + 2 * P, rh);
+  }
+  double tot[1];
+  if (grid_reduce<1>(acc, rs, site, tot) && threadIdx.x == 0)
+    ctrl->mean_ru = tot[0] / ((double)g.n * (double)g.m);
+}
+
+// setup: x = x0, r = b - A x0, ||b||, ||r0|| (pcg.py:59-75)
+template <typename T>
+__global__ void __launch_bounds__(256) k_pcg_start_v(Grid g, const T* __restrict__ b, const T* __restrict__ x0,
+                                                     T* __restrict__ x, T* __restrict__ r, const T* __restrict__ dv,
+                                                     const T* __restrict__ dh, PcgCtrl* ctrl, double* res_norms,
+                                                     double rel_tol, int max_iters, RedScratch rs, int site) {
+  const long long P = g.plane, ld = g.ld;
+  double acc[2] = {0.0, 0.0};
+  PU_FOR_CHUNKS(g, i, j0) {
+    const long long o = (long long)i * ld + j0;
+    const Q4<T> d1 = ldg4(dv + o), d2 = ldg4(dh + o);
+    Stencil4<T> s;
+    s.u = ldg4(x0 + o);
+    s.v = ldg4(x0 + o + P);
+    s.h = ldg4(x0 + o + 2 * P);
+    s.ua = i > 0 ? ldg4(x0 + o - ld) : zero4<T>();
+    s.va = i > 0 ? ldg4(x0 + o - ld + P) : zero4<T>();
+    s.ub = i < g.n - 1 ? ldg4(x0 + o + ld) : zero4<T>();
+    s.ul = ldg_or0(x0 + o - 1, j0 > 0);
+    s.hl = ldg_or0(x0 + o - 1 + 2 * P, j0 > 0);
+    s.ur = ldg_or0(x0 + o + 4, j0 + 4 < g.m);
+    Q4<T> au, av, ah;
+    apply4<T>(g, i, j0, s, d1, d2, au, av, ah);
+    const Q4<T> bu = ldg4(b + o), bv = ldg4(b + o + P), bh = ldg4(b + o + 2 * P);
+    Q4<T> ru, rv, rh;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      ru.a[k] = add_rn(bu.a[k], -au.a[k]);
+      rv.a[k] = add_rn(bv.a[k], -av.a[k]);
+      rh.a[k] = add_rn(bh.a[k], -ah.a[k]);
+      acc[0] += (double)bu.a[k] * bu.a[k] + (double)bv.a[k] * bv.a[k] + (double)bh.a[k] * bh.a[k];
+      acc[1] += (double)ru.a[k] * ru.a[k] + (double)rv.a[k] * rv.a[k] + (double)rh.a[k] * rh.a[k];
+    }
+    st4(x + o, s.u); st4(x + o + P, s.v); st4(x + o + 2 * P, s.h);
+    st4(r + o, ru); st4(r + o + P, rv); st4(r + o + 2 * P, rh);
+  }
+  double tot[2];
+  if (grid_reduce<2>(acc, rs, site, tot) && threadIdx.x == 0) {
+    const double bn = sqrt(tot[0]);
+    const double rn = sqrt(tot[1]);
+    ctrl->bnorm = bn;
+    ctrl->thr = rel_tol * bn;
+    ctrl->rn = rn;
+    ctrl->max_iters = max_iters;
+    ctrl->breakdown = -1; ctrl->bkind = -1; ctrl->converged = 0; ctrl->done = 0;
+    ctrl->iterations = 0; ctrl->alpha = 0; ctrl->beta = 0; ctrl->rho = 0; ctrl->pap = 0;
+    res_norms[0] = rn;
+    if (!isfinite(rn)) {
+      ctrl->breakdown = 0; ctrl->bkind = 0; ctrl->done = 1;
+    } else if (rn <= ctrl->thr || max_iters == 0) {
+      ctrl->converged = rn <= ctrl->thr; ctrl->done = 1;
+    }
+  }
+}
+
+}  // namespace pu
+
+namespace pu {
+
+// ---------------------------------------------------------------------------
+// Vectorised outer-iteration kernels (irls.py:172-215).  Same per-cell
+// arithmetic as the scalar kernels in pu_kernels.cuh; slack terms are formed
+// in the storage precision T and accumulated in fp64.
+// ---------------------------------------------------------------------------
+
+// forward-difference penalty residuals of a 4-cell chunk:
+// rv = (u[i+1] - u[i]) - gv - vv, rh = (u[j+1] - u[j]) - gh - vh
+template <typename T>
+__device__ __forceinline__ void pen4(const Grid& g, int i, int j0, const Q4<T>& u, const Q4<T>& ub, T ur,
+                                     const Q4<T>& vv, const Q4<T>& vh, const Q4<T>& gv, const Q4<T>& gh, double& sv,
+                                     double& sh) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int j = j0 + k;
+    if (i < g.n - 1 && j < g.m) {
+      const double rv = ((double)ub.a[k] - (double)u.a[k]) - (double)gv.a[k] - (double)vv.a[k];
+      sv += rv * rv;
+    }
+    if (j < g.m - 1) {
+      const T right = (k == 3) ? ur : u.a[k + 1];
+      const double rh = ((double)right - (double)u.a[k]) - (double)gh.a[k] - (double)vh.a[k];
+      sh += rh * rh;
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ double slack4(T c, T v, T w, T d2) {
+  const T cv = c * v;
+  return (double)((cv * cv + d2) / w + w);
+}
+
+// w = sqrt((c v)^2 + delta^2), d = c^2 / w; H(x, w_prev), H(x, w)
+template <typename T>
+__global__ void __launch_bounds__(256) k_weights_hpair_v(Grid g, const T* __restrict__ x, const T* __restrict__ cv,
+                                                         const T* __restrict__ ch, const T* __restrict__ gv,
+                                                         const T* __restrict__ gh, const T* __restrict__ wpv,
+                                                         const T* __restrict__ wph, T* __restrict__ wv,
+                                                         T* __restrict__ wh, T* __restrict__ dv, T* __restrict__ dh,
+                                                         RedScratch rs, int site, double* out) {
+  const long long P = g.plane, ld = g.ld;
+  const T d2 = (T)(g.delta * g.delta);
+  const bool hasprev = wpv != nullptr;
+  double acc[6] = {0, 0, 0, 0, 0, 0};  // old_v, old_h, new_v, new_h, pen_v, pen_h
+  PU_FOR_CHUNKS(g, i, j0) {
+    const long long o = (long long)i * ld + j0;
+    const Q4<T> u = ldg4(x + o), vv = ldg4(x + o + P), vh = ldg4(x + o + 2 * P);
+    const Q4<T> ub = i < g.n - 1 ? ldg4(x + o + ld) : zero4<T>();
+    const T ur = ldg_or0(x + o + 4, j0 + 4 < g.m);
+    const Q4<T> c1 = ldg4(cv + o), c2 = ldg4(ch + o), g1 = ldg4(gv + o), g2 = ldg4(gh + o);
+    Q4<T> p1 = zero4<T>(), p2 = zero4<T>();
+    if (hasprev) { p1 = ldg4(wpv + o); p2 = ldg4(wph + o); }
+    Q4<T> w1, w2, e1, e2;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
+      const bool okv = i < g.n - 1 && j < g.m, okh = j < g.m - 1;
+      const T a = c1.a[k] * vv.a[k], b = c2.a[k] * vh.a[k];
+      const T wa = sqrt(a * a + d2), wb = sqrt(b * b + d2);
+      w1.a[k] = okv ? wa : (T)1;
+      w2.a[k] = okh ? wb : (T)1;
+      e1.a[k] = okv ? c1.a[k] * c1.a[k] / wa : (T)0;
+      e2.a[k] = okh ? c2.a[k] * c2.a[k] / wb : (T)0;
+      if (okv) {
+        acc[2] += slack4(c1.a[k], vv.a[k], wa, d2);
+        if (hasprev) acc[0] += slack4(c1.a[k], vv.a[k], p1.a[k], d2);
+      }
+      if (okh) {
+        acc[3] += slack4(c2.a[k], vh.a[k], wb, d2);
+        if (hasprev) acc[1] += slack4(c2.a[k], vh.a[k], p2.a[k], d2);
+      }
+    }
+    st4(wv + o, w1); st4(wh + o, w2); st4(dv + o, e1); st4(dh + o, e2);
+    pen4<T>(g, i, j0, u, ub, ur, vv, vh, g1, g2, acc[4], acc[5]);
+  }
+  double tot[6];
+  if (grid_reduce<6>(acc, rs, site, tot) && threadIdx.x == 0) {
+    const double pen = (tot[4] + tot[5]) / (2.0 * g.tau);
+    out[0] = (0.5 * tot[0] + 0.5 * tot[1]) + pen;
+    out[1] = (0.5 * tot[2] + 0.5 * tot[3]) + pen;
+  }
+}
+
+// H(xa, w), H(xb, w), mean u of the accepted one, acceptance flag
+template <typename T>
+__global__ void __launch_bounds__(256) k_hpair_states_v(Grid g, const T* __restrict__ xa, const T* __restrict__ xb,
+                                                        const T* __restrict__ wv, const T* __restrict__ wh,
+                                                        const T* __restrict__ gv, const T* __restrict__ gh,
+                                                        const T* __restrict__ cv, const T* __restrict__ ch,
+                                                        RedScratch rs, int site, double* out) {
+  const long long P = g.plane, ld = g.ld;
+  const T d2 = (T)(g.delta * g.delta);
+  double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  PU_FOR_CHUNKS(g, i, j0) {
+    const long long o = (long long)i * ld + j0;
+    const Q4<T> c1 = ldg4(cv + o), c2 = ldg4(ch + o), g1 = ldg4(gv + o), g2 = ldg4(gh + o);
+    const Q4<T> w1 = ldg4(wv + o), w2 = ldg4(wh + o);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const T* x = s ? xb : xa;
+      const Q4<T> u = ldg4(x + o), vv = ldg4(x + o + P), vh = ldg4(x + o + 2 * P);
+      const Q4<T> ub = i < g.n - 1 ? ldg4(x + o + ld) : zero4<T>();
+      const T ur = ldg_or0(x + o + 4, j0 + 4 < g.m);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = j0 + k;
+        if (i < g.n - 1 && j < g.m) acc[5 * s + 0] += slack4(c1.a[k], vv.a[k], w1.a[k], d2);
+        if (j < g.m - 1) acc[5 * s + 1] += slack4(c2.a[k], vh.a[k], w2.a[k], d2);
+        if (j < g.m) acc[5 * s + 4] += (double)u.a[k];
+      }
+      pen4<T>(g, i, j0, u, ub, ur, vv, vh, g1, g2, acc[5 * s + 2], acc[5 * s + 3]);
+    }
+  }
+  double tot[10];
+  if (grid_reduce<10>(acc, rs, site, tot) && threadIdx.x == 0) {
+    const double ha = (0.5 * tot[0] + 0.5 * tot[1]) + (tot[2] + tot[3]) / (2.0 * g.tau);
+    const double hb = (0.5 * tot[5] + 0.5 * tot[6]) + (tot[7] + tot[8]) / (2.0 * g.tau);
+    const bool take_a = ha <= hb;
+    out[0] = ha;
+    out[1] = hb;
+    out[2] = (take_a ? tot[4] : tot[9]) / ((double)g.n * (double)g.m);
+    out[3] = take_a ? 1.0 : 0.0;
+  }
+}
+
+// cand = x - (1/L) grad H(x, w)   (objective.py:108-125)
+template <typename T>
+__global__ void __launch_bounds__(256) k_candidate_v(Grid g, const T* __restrict__ x, const T* __restrict__ wv,
+                                                     const T* __restrict__ wh, const T* __restrict__ gv,
+                                                     const T* __restrict__ gh, const T* __restrict__ cv,
+                                                     const T* __restrict__ ch, T neg_inv_lip, T* __restrict__ out) {
+  const long long P = g.plane, ld = g.ld;
+  const T inv = (T)g.inv_tau;
+  PU_FOR_CHUNKS(g, i, j0) {
+    const long long o = (long long)i * ld + j0;
+    const Q4<T> u = ldg4(x + o), vv = ldg4(x + o + P), vh = ldg4(x + o + 2 * P);
+    const Q4<T> g1 = ldg4(gv + o), g2 = ldg4(gh + o);
+    const bool hasb = i < g.n - 1, hasa = i > 0;
+    const Q4<T> ub = hasb ? ldg4(x + o + ld) : zero4<T>();
+    const Q4<T> ua = hasa ? ldg4(x + o - ld) : zero4<T>();
+    const Q4<T> va = hasa ? ldg4(x + o - ld + P) : zero4<T>();
+    const Q4<T> ga = hasa ? ldg4(gv + o - ld) : zero4<T>();
+    const T ur = ldg_or0(x + o + 4, j0 + 4 < g.m);
+    const T ul = ldg_or0(x + o - 1, j0 > 0);
+    const T hl = ldg_or0(x + o - 1 + 2 * P, j0 > 0);
+    const T gl = ldg_or0(gh + o - 1, j0 > 0);
+    const Q4<T> c1 = ldg4(cv + o), c2 = ldg4(ch + o), w1 = ldg4(wv + o), w2 = ldg4(wh + o);
+    Q4<T> ou, ov, oh;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
+      const bool ok = j < g.m, hash = j < g.m - 1;
+      const T uo = u.a[k];
+      const T left = (k == 0) ? ul : u.a[k - 1];
+      const T right = (k == 3) ? ur : u.a[k + 1];
+      const T hleft = (k == 0) ? hl : vh.a[k - 1];
+      const T gleft = (k == 0) ? gl : g2.a[k - 1];
+      T rv = 0, rvm = 0, rh = 0, rhm = 0;
+      if (hasb) rv = ((ub.a[k] - uo) - g1.a[k]) - vv.a[k];
+      if (hasa) rvm = ((uo - ua.a[k]) - ga.a[k]) - va.a[k];
+      if (hash) rh = ((right - uo) - g2.a[k]) - vh.a[k];
+      if (j > 0) rhm = ((uo - left) - gleft) - hleft;
+      const T gu = inv * ((rvm - rv) + (rhm - rh));
+      ou.a[k] = ok ? add_rn(uo, mul_rn(neg_inv_lip, gu)) : (T)0;
+      const T gvv = c1.a[k] * c1.a[k] / w1.a[k] * vv.a[k] - inv * rv;
+      const T gvh = c2.a[k] * c2.a[k] / w2.a[k] * vh.a[k] - inv * rh;
+      ov.a[k] = (ok && hasb) ? add_rn(vv.a[k], mul_rn(neg_inv_lip, gvv)) : (T)0;
+      oh.a[k] = hash ? add_rn(vh.a[k], mul_rn(neg_inv_lip, gvh)) : (T)0;
+    }
+    st4(out + o, ou); st4(out + o + P, ov); st4(out + o + 2 * P, oh);
+  }
+}
+
+// dst = (sel[1] ? xa : xb) with u -= sel[0]; H(dst, w)   (irls.py:206-215)
+template <typename T>
+__global__ void __launch_bounds__(256) k_accept_v(Grid g, const T* __restrict__ xa, const T* __restrict__ xb,
+                                                  const double* sel, T* __restrict__ dst, const T* __restrict__ wv,
+                                                  const T* __restrict__ wh, const T* __restrict__ gv,
+                                                  const T* __restrict__ gh, const T* __restrict__ cv,
+                                                  const T* __restrict__ ch, RedScratch rs, int site, double* out) {
+  const long long P = g.plane, ld = g.ld;
+  const T* x = sel[1] != 0.0 ? xa : xb;
+  const T mean = (T)sel[0];
+  const T d2 = (T)(g.delta * g.delta);
+  double acc[4] = {0, 0, 0, 0};
+  PU_FOR_CHUNKS(g, i, j0) {
+    const long long o = (long long)i * ld + j0;
+    Q4<T> u = ldg4(x + o);
+    const Q4<T> vv = ldg4(x + o + P), vh = ldg4(x + o + 2 * P);
+    Q4<T> ub = i < g.n - 1 ? ldg4(x + o + ld) : zero4<T>();
+    T ur = ldg_or0(x + o + 4, j0 + 4 < g.m);
+    const Q4<T> c1 = ldg4(cv + o), c2 = ldg4(ch + o), g1 = ldg4(gv + o), g2 = ldg4(gh + o);
+    const Q4<T> w1 = ldg4(wv + o), w2 = ldg4(wh + o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
+      u.a[k] = (j < g.m) ? u.a[k] - mean : (T)0;
+      ub.a[k] = ub.a[k] - mean;
+      if (i < g.n - 1 && j < g.m) acc[0] += slack4(c1.a[k], vv.a[k], w1.a[k], d2);
+      if (j < g.m - 1) acc[1] += slack4(c2.a[k], vh.a[k], w2.a[k], d2);
+    }
+    ur = ur - mean;
+    pen4<T>(g, i, j0, u, ub, ur, vv, vh, g1, g2, acc[2], acc[3]);
+    st4(dst + o, u); st4(dst + o + P, vv); st4(dst + o + 2 * P, vh);
+  }
+  double tot[4];
+  if (grid_reduce<4>(acc, rs, site, tot) && threadIdx.x == 0)
+    out[0] = (0.5 * tot[0] + 0.5 * tot[1]) + (tot[2] + tot[3]) / (2.0 * g.tau);
+}
+
+}  // namespace pu

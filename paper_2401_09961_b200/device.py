@@ -152,8 +152,9 @@ class Workspace:
         return self.norms
 
     # ---- instrumentation ---------------------------------------------------
-    TIME_KINDS = ("pcg_start", "K1_p_Ap_pAp", "K2_update_rowdct", "K3_coldct_spectral", "K4_row_idct",
-                  "reproject_update", "weights_hpair", "candidate", "hpair_states", "accept_center")
+    TIME_KINDS = ("pcg_start", "K1_p_Ap_pAp", "K2a_update_norms", "K3_coldct_spectral", "K4_row_idct",
+                  "reproject_update", "weights_hpair", "candidate", "hpair_states", "accept_center",
+                  "K2b_row_dct")
 
     def timing(self, on: bool):
         nat.check(self.lib.pu_timing_enable(self.h, 1 if on else 0))
