@@ -207,8 +207,8 @@ struct HostPlan {
 template <typename T>
 struct DctOps {
   cudaError_t (*set_attrs)(size_t, size_t);
-  decltype(&DctLaunch<T, 0>::rows_plain) rows_plain;
-  decltype(&DctLaunch<T, 0>::rows_inv) rows_inv;
+  decltype(&DctLaunch<T, 0>::rows_pipe) rows_pipe;
+  decltype(&DctLaunch<T, 0>::rows_pipe_blocks_per_sm) rows_pipe_bps;
   decltype(&DctLaunch<T, 0>::cols) cols;
   int ls;
 };
@@ -216,7 +216,8 @@ struct DctOps {
 template <typename T, int LS>
 static DctOps<T> make_ops() {
   using D = DctLaunch<T, LS>;
-  return DctOps<T>{&D::set_attrs, &D::rows_plain, &D::rows_inv, &D::cols, LS};
+  return DctOps<T>{&D::set_attrs, &D::rows_pipe, &D::rows_pipe_blocks_per_sm,
+                   &D::cols, LS};
 }
 
 template <typename T>
@@ -295,10 +296,11 @@ template <typename T>
 struct Impl : HandleBase {
   Grid g{};
   HostPlan<T> prow, pcol;  // row transforms (length m), column transforms (length n)
-  int rows_per_cta = 2, row_threads = 64;
   int cols_per_cta = 2, col_threads = 64;
-  size_t row_smem = 0, col_smem = 0;
+  size_t col_smem = 0;
   int ew_grid = 1, ew_threads = 32;
+  int pipe_grid = 1, pipe_threads = 64;
+  size_t pipe_smem = 0;
   RedScratch rs{};
   int* pinned_done = nullptr;
   DctOps<T> rops{}, cops{};  // transform kernels for the row / column internal lengths
@@ -319,24 +321,18 @@ struct Impl : HandleBase {
     g.tau = tau; g.inv_tau = 1.0 / tau; g.delta = delta;
     int rc;
     if ((rc = prow.build(m)) || (rc = pcol.build(n))) return rc;
-    // row kernels: aim for ~8K (f32) / 4K (f64) complex per CTA but keep >= ~2 CTAs per SM
-    const int target = sizeof(T) == 4 ? 8192 : 4096;
-    const int seqs_total = (n + 1) / 2;
-    int c = std::max(1, target / prow.dev.L);
-    c = std::min(c, std::max(1, seqs_total / (2 * 148)));
-    while (c > 1 && (prow.threads_for(c) > prow.max_threads() || prow.smem_for(c) > kSmemLimit)) --c;
-    if (prow.threads_for(c) > prow.max_threads() || prow.smem_for(c) > kSmemLimit)
+    // row kernels (k_rows_pipe): one row pair per CTA, whole sequence in one group
+    if (prow.threads_for(1) > prow.max_threads() ||
+        rows_pipe_smem(prow.dev.n, sizeof(T), prow.dev.ldseq) > kSmemLimit)
       return fail(PU_ERR_UNSUPPORTED, "row length " + std::to_string(m) + " exceeds the shared-memory FFT limit");
-    rows_per_cta = 2 * c;
-    row_threads = prow.threads_for(c);
-    row_smem = prow.smem_for(c);
-    // column kernels: panel of W = 2c columns; prefer 32-byte row segments
-    // 2 sequences (W = 4 columns) per CTA keeps two CTAs resident per SM; the
-    // spectral plane is L2-resident between K2b and K4, so 16-byte (fp32) row
-    // segments cost L2, not HBM, efficiency
+    // column kernels (k_cols_spec): panel of W = 2 cc columns
+    // 2 sequences (W = 4 columns) per CTA, all in one thread group (<= 512
+    // threads) so two CTAs stay resident per SM; the spectral plane is
+    // L2-resident between K2b and K4, so 16-byte (fp32) row segments cost L2,
+    // not HBM, efficiency
     int cc = 2;
     cc = std::min(cc, std::max(1, (m + 1) / 2));
-    while (cc > 1 && (pcol.threads_for(cc) > pcol.max_threads() || pcol.smem_for(cc) > kSmemLimit)) --cc;
+    while (cc > 1 && (pcol.threads_for(cc) > 512 || pcol.smem_for(cc) > kSmemLimit)) --cc;
     if (pcol.threads_for(cc) > pcol.max_threads() || pcol.smem_for(cc) > kSmemLimit)
       return fail(PU_ERR_UNSUPPORTED, "column length " + std::to_string(n) + " exceeds the shared-memory FFT limit");
     cols_per_cta = 2 * cc;
@@ -345,8 +341,7 @@ struct Impl : HandleBase {
     // element-wise kernels: block-strided rows, thread-strided columns
     ew_threads = std::min(256, std::max(32, (m + 31) / 32 * 32));
     ew_grid = std::min(n, 148 * 8);
-    rs.stride = std::max(std::max(148 * 8, (n + rows_per_cta - 1) / rows_per_cta),
-                         (m + cols_per_cta - 1) / cols_per_cta) + 1;
+    rs.stride = std::max(148 * 8, (m + cols_per_cta - 1) / cols_per_cta) + 1;
     PU_CUDA(cudaMalloc(&rs.partials, sizeof(double) * PU_MAX_SUMS * rs.stride));
     PU_CUDA(cudaMalloc(&rs.ticket, sizeof(unsigned int) * 32));
     PU_CUDA(cudaMemset(rs.ticket, 0, sizeof(unsigned int) * 32));
@@ -363,20 +358,30 @@ struct Impl : HandleBase {
     // that handles of different sizes sharing an instantiation never shrink it
     PU_CUDA(rops.set_attrs(kSmemLimit, kSmemLimit));
     PU_CUDA(cops.set_attrs(kSmemLimit, kSmemLimit));
+    // persistent pipelined row kernels: one row pair per iteration
+    pipe_threads = prow.threads_for(1);
+    pipe_smem = rows_pipe_smem(prow.dev.n, sizeof(T), prow.dev.ldseq);
+    if (pipe_smem > kSmemLimit)
+      return fail(PU_ERR_UNSUPPORTED, "row length " + std::to_string(g.m) + " exceeds the row pipeline staging");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int bps = rops.rows_pipe_bps(pipe_threads, pipe_smem);
+    pipe_grid = std::max(1, (g.n + 1) / 2);  // one row pair per CTA
+    (void)bps;
     return PU_OK;
   }
 
-  XLaunch rl(cudaStream_t st) const { return XLaunch{row_grid(), row_threads, row_smem, st}; }
   XLaunch cl(cudaStream_t st) const { return XLaunch{col_grid(), col_threads, col_smem, st}; }
+  XLaunch pl_(cudaStream_t st) const { return XLaunch{pipe_grid, pipe_threads, pipe_smem, st}; }
 
-  int row_grid() const { return (g.n + rows_per_cta - 1) / rows_per_cta; }
   int col_grid() const { return (g.m + cols_per_cta - 1) / cols_per_cta; }
 
   // ---- preconditioner passes ----
   int sylvester(const T* r, T* z, T* spec, cudaStream_t st) {
-    PU_DCT(rops.rows_plain(rl(st), g, prow.dev, rows_per_cta, r, spec, nullptr, rs, S_K2));
+    PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, nullptr));
     PU_DCT(cops.cols(MODE_API, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, nullptr, rs, S_K3, 0));
-    PU_DCT(rops.rows_inv(rl(st), g, prow.dev, rows_per_cta, spec, z, nullptr));
+    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, z, nullptr));
     return PU_OK;
   }
 
@@ -401,13 +406,13 @@ struct Impl : HandleBase {
     PU_LAUNCH_CHECK();
     tm.end(st, e, TK_K2, -1);
     e = tm.begin(st);
-    PU_DCT(rops.rows_plain(rl(st), g, prow.dev, rows_per_cta, r, spec, ctrl, rs, S_K2B));
+    PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl));
     tm.end(st, e, TK_K2B, -1);
     e = tm.begin(st);
     PU_DCT(cops.cols(MODE_INIT, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, ctrl, rs, S_K3, -1));
     tm.end(st, e, TK_K3, -1);
     e = tm.begin(st);
-    PU_DCT(rops.rows_inv(rl(st), g, prow.dev, rows_per_cta, spec, z, ctrl));
+    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, z, ctrl));
     tm.end(st, e, TK_K4, -1);
     T* pbuf[2] = {p0, p1};
     const int chunk = 64;
@@ -439,13 +444,13 @@ struct Impl : HandleBase {
         tm.end(st, e, TK_K2, it);
       }
       e = tm.begin(st);
-      PU_DCT(rops.rows_plain(rl(st), g, prow.dev, rows_per_cta, r, spec, ctrl, rs, S_K2B));
+      PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl));
       tm.end(st, e, TK_K2B, it);
       e = tm.begin(st);
       PU_DCT(cops.cols(MODE_ITER, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, ctrl, rs, S_K3, it));
       tm.end(st, e, TK_K3, it);
       e = tm.begin(st);
-      PU_DCT(rops.rows_inv(rl(st), g, prow.dev, rows_per_cta, spec, z, ctrl));
+      PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, z, ctrl));
       tm.end(st, e, TK_K4, it);
     }
     return PU_OK;
@@ -536,11 +541,11 @@ int pu_describe(const pu_handle* h, char* buf, int cap) {
     std::snprintf(buf, cap,
                   "{\"n\":%d,\"m\":%d,\"ld\":%lld,\"dtype\":\"%s\",\"row_fft\":{\"n\":%d,\"L\":%d,\"bluestein\":%d,"
                   "\"stages\":%d},\"col_fft\":{\"n\":%d,\"L\":%d,\"bluestein\":%d,\"stages\":%d},"
-                  "\"rows_per_cta\":%d,\"row_threads\":%d,\"row_smem\":%zu,\"cols_per_cta\":%d,"
+                  "\"row_pipe_grid\":%d,\"row_threads\":%d,\"row_smem\":%zu,\"cols_per_cta\":%d,"
                   "\"col_threads\":%d,\"col_smem\":%zu,\"ew_grid\":%d,\"ew_threads\":%d}",
                   I.g.n, I.g.m, I.g.ld, h->dtype == PU_F32 ? "f32" : "f64", I.prow.dev.n, I.prow.dev.L,
                   I.prow.dev.bluestein, I.prow.dev.nst, I.pcol.dev.n, I.pcol.dev.L, I.pcol.dev.bluestein,
-                  I.pcol.dev.nst, I.rows_per_cta, I.row_threads, I.row_smem, I.cols_per_cta, I.col_threads,
+                  I.pcol.dev.nst, I.pipe_grid, I.pipe_threads, I.pipe_smem, I.cols_per_cta, I.col_threads,
                   I.col_smem, I.ew_grid, I.ew_threads);
   };
   if (h->dtype == PU_F32) fmt(*h->f); else fmt(*h->d);

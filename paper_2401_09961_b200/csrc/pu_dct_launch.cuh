@@ -5,7 +5,7 @@
 // for every other length.
 #pragma once
 
-#include "pu_pcg.cuh"
+#include "pu_pipe.cuh"
 
 namespace pu {
 
@@ -22,10 +22,10 @@ struct DctLaunch {
 
   static cudaError_t set_attrs(size_t row_smem, size_t col_smem);
 
-  static cudaError_t rows_plain(const XLaunch& c, const Grid& g, const FftPlan<T>& pl, int rpc, const T* src, T* out,
-                                const PcgCtrl* ctrl, RedScratch rs, int site);
-  static cudaError_t rows_inv(const XLaunch& c, const Grid& g, const FftPlan<T>& pl, int rpc, const T* in, T* out,
-                              const PcgCtrl* ctrl);
+  // pipelined persistent row transforms (pu_pipe.cuh); grid from occupancy
+  static cudaError_t rows_pipe(bool inv, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const T* in, T* out,
+                               const PcgCtrl* ctrl);
+  static int rows_pipe_blocks_per_sm(int threads, size_t smem);
   static cudaError_t cols(int mode, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const T* lam_cols,
                           int cpc, T* data, PcgCtrl* ctrl, RedScratch rs, int site, int it);
 };
@@ -36,8 +36,8 @@ cudaError_t DctLaunch<T, LS>::set_attrs(size_t row_smem, size_t col_smem) {
   cudaError_t e;
 #define PU_ATTR(K, S) \
   if ((e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(S))) != cudaSuccess) return e;
-  PU_ATTR((k_rows_fwd<T, EM, LS, RowsPlain<T>>), row_smem);
-  PU_ATTR((k_rows_inv<T, EM, LS>), row_smem);
+  PU_ATTR((k_rows_pipe<T, EM, LS, false>), row_smem);
+  PU_ATTR((k_rows_pipe<T, EM, LS, true>), row_smem);
   PU_ATTR((k_cols_spec<T, EM, LS, MODE_API>), col_smem);
   PU_ATTR((k_cols_spec<T, EM, LS, MODE_INIT>), col_smem);
   PU_ATTR((k_cols_spec<T, EM, LS, MODE_ITER>), col_smem);
@@ -46,18 +46,21 @@ cudaError_t DctLaunch<T, LS>::set_attrs(size_t row_smem, size_t col_smem) {
 }
 
 template <typename T, int LS>
-cudaError_t DctLaunch<T, LS>::rows_plain(const XLaunch& c, const Grid& g, const FftPlan<T>& pl, int rpc,
-                                         const T* src, T* out, const PcgCtrl* ctrl, RedScratch rs, int site) {
-  RowsPlain<T> pol{src, ctrl};
-  k_rows_fwd<T, EM, LS, RowsPlain<T>><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, rpc, out, pol, rs, site);
+cudaError_t DctLaunch<T, LS>::rows_pipe(bool inv, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const T* in,
+                                        T* out, const PcgCtrl* ctrl) {
+  if (inv)
+    k_rows_pipe<T, EM, LS, true><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, in, out, ctrl);
+  else
+    k_rows_pipe<T, EM, LS, false><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, in, out, ctrl);
   return cudaGetLastError();
 }
 
 template <typename T, int LS>
-cudaError_t DctLaunch<T, LS>::rows_inv(const XLaunch& c, const Grid& g, const FftPlan<T>& pl, int rpc, const T* in,
-                                       T* out, const PcgCtrl* ctrl) {
-  k_rows_inv<T, EM, LS><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, rpc, in, out, ctrl);
-  return cudaGetLastError();
+int DctLaunch<T, LS>::rows_pipe_blocks_per_sm(int threads, size_t smem) {
+  int a = 0, b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_rows_pipe<T, EM, LS, false>, threads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_rows_pipe<T, EM, LS, true>, threads, smem);
+  return std::max(1, std::min(a, b));
 }
 
 template <typename T, int LS>

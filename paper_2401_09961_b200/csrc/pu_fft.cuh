@@ -19,15 +19,12 @@ namespace pu {
 #define PU_FFT_MAX_STAGES 20
 #define PU_FFT_MAX_THREADS 1024  // absolute per-CTA thread cap of the transform kernels
 
-// Per-instantiation launch bounds: a stage holds one whole sequence, so a CTA
-// needs L / EMAX threads; below that, 256 threads at <= 128 registers (two
-// CTAs per SM).  LS = 0 (runtime plans: odd sizes, Bluestein) allows 1024.
-__host__ __device__ constexpr int fft_max_threads(int LS, int EMAX) {
-  return LS == 0 ? 1024 : (LS / EMAX > 256 ? LS / EMAX : 256);
-}
-__host__ __device__ constexpr int fft_min_blocks(int LS, int EMAX) {
-  return fft_max_threads(LS, EMAX) <= 256 ? 2 : 1;
-}
+// Per-instantiation launch bounds.  Transform kernels run every sequence of
+// the CTA in one group (no loop over sequence groups: ptxas hoists the
+// thread-invariant twiddles/addresses of such loops and spills), so a CTA
+// has nseq * L / EMAX threads, up to 1024, at <= 64 registers.
+__host__ __device__ constexpr int fft_max_threads(int LS, int EMAX) { return 1024; }
+__host__ __device__ constexpr int fft_min_blocks(int LS, int EMAX) { return 1; }
 
 // Plan for one transform length (built on the host, pu_api.cu HostPlan).
 template <typename T>
@@ -319,7 +316,11 @@ __device__ __forceinline__ void fft_stage_s(cplx<T>* buf, int seq0, int nseq, co
         // balanced product tree (depth <= log2 R, a few ulp)
         const int k = j % NS;
         cplx<T> w[R];
-        w[1] = __ldg(stw + OFF + k);
+        // opaque table pointer: keeps the (loop-invariant) twiddle loads and their
+        // power tree inside persistent loops instead of hoisted into registers
+        unsigned long long tp = reinterpret_cast<unsigned long long>(stw);
+        asm volatile("" : "+l"(tp));
+        w[1] = __ldg(reinterpret_cast<const cplx<T>*>(tp) + OFF + k);
 #pragma unroll
         for (int r = 2; r < R; ++r) w[r] = cmul<T>(w[r / 2], w[r - r / 2]);
 #pragma unroll
@@ -370,8 +371,8 @@ __device__ __forceinline__ void fft_stages_s(cplx<T>* buf, int seq0, int nseq, c
 template <typename T, int EMAX, int LS>
 __device__ __forceinline__ void fft_internal(cplx<T>* buf, int nseq, const FftPlan<T>& pl) {
   if constexpr (LS > 0) {
-    const int grp = max(1, (int)(blockDim.x * EMAX) / LS);
-    for (int sg = 0; sg < nseq; sg += grp) fft_stages_s<T, EMAX, LS, 1, 0>(buf, sg, min(grp, nseq - sg), pl.stw);
+    // the launch guarantees blockDim.x * EMAX >= nseq * LS: one group, no loop
+    fft_stages_s<T, EMAX, LS, 1, 0>(buf, 0, nseq, pl.stw);
   } else {
     fft_pow<T, EMAX>(buf, nseq, pl);
   }

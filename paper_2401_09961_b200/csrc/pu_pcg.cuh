@@ -6,11 +6,11 @@
 //   K2a k_pcg_r_v  x += alpha p; r -= alpha A p (A p recomputed from p);
 //                  ||r||^2; slack preconditioner z_s = r_s / (d + 1/tau); rho_s;
 //                  last block: ||r|| exits            (pu_vec.cuh)
-//   K2b k_rows_fwd row DCT-II of r_u -> spectral plane T
+//   K2b k_rows_pipe<false> row DCT-II of r_u -> spectral plane T (pu_pipe.cuh)
 //   K3 k_cols_spec column DCT-II, x tau/(lam_i + lam_j) with (0,0) -> 0,
 //                  rho_u = <r_hat, z_hat> (Parseval), column DCT-III;
 //                  last block: beta = (rho_s + rho_u) / rho
-//   K4 k_rows_inv  row DCT-III of T -> z_u
+//   K4 k_rows_pipe<true>  row DCT-III of T -> z_u (pu_pipe.cuh)
 // The standalone preconditioner (preconditioner.py:86-115) is K2..K4 with the
 // plain policies.  Every PCG kernel returns immediately once ctrl->done is set.
 #pragma once
@@ -20,185 +20,6 @@
 namespace pu {
 
 enum { MODE_API = 0, MODE_INIT = 1, MODE_ITER = 2 };
-
-// ---------------------------------------------------------------------------
-// Row-pass element policies for k_rows_fwd (value of r_u at (i, j) to be
-// transformed; side effects and partial sums for the PCG variants).
-// ---------------------------------------------------------------------------
-template <typename T>
-struct RowsPlain {
-  static constexpr int NS = 1;
-  static constexpr bool REDUCE = false;
-  static constexpr bool PLAIN = true;
-  const T* src;
-  const PcgCtrl* ctrl;  // optional: skip once the PCG loop has ended
-  __device__ __forceinline__ bool skip() const { return ctrl != nullptr && ctrl->done != 0; }
-  __device__ __forceinline__ T elem(const Grid& g, int i, int j, double (&acc)[NS]) const {
-    return src[(long long)i * g.ld + j];
-  }
-  __device__ __forceinline__ void finish(const Grid&, double (&)[NS]) const {}
-};
-
-// ---------------------------------------------------------------------------
-// Row staging: rows (i0 + 2s, i0 + 2s + 1) -> complex sequence s at the
-// Makhoul-permuted positions, moved as 4-cell vectors with UNR chunks per
-// thread in flight; and the inverse (Re/n, -Im/n) after a DCT-III FFT.
-// ---------------------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ void rows_stage_vec(const Grid& g, const FftPlan<T>& pl, const T* __restrict__ src, int i0,
-                                               int nrows, int nseq, cplx<T>* buf, const int n) {
-  const int cpr = (n + 3) >> 2;
-  const int items = nseq * cpr;
-  constexpr int UNR = 4;
-  for (int base = 0; base < items; base += UNR * blockDim.x) {
-    Q4<T> ra[UNR], rb[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int e = base + u * blockDim.x + threadIdx.x;
-      if (e < items) {
-        const int s = e / cpr, j0 = (e - s * cpr) * 4;
-        const long long oa = (long long)(i0 + 2 * s) * g.ld + j0;
-        ra[u] = ldg4(src + oa);
-        rb[u] = (2 * s + 1 < nrows) ? ldg4(src + oa + g.ld) : zero4<T>();
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int e = base + u * blockDim.x + threadIdx.x;
-      if (e < items) {
-        const int s = e / cpr, j0 = (e - s * cpr) * 4;
-        cplx<T>* sb = buf + s * pl.ldseq;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (j0 + k < n) sb[spad(mperm(j0 + k, n))] = mk<T>(ra[u].a[k], rb[u].a[k]);
-      }
-    }
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ void rows_unstage_vec(const Grid& g, const FftPlan<T>& pl, const cplx<T>* buf, T* out,
-                                                 int i0, int nrows, const int n) {
-  const int cpr = (n + 3) >> 2;
-  const int items = nrows * cpr;
-  for (int e = threadIdx.x; e < items; e += blockDim.x) {
-    const int rr = e / cpr, j0 = (e - rr * cpr) * 4;
-    const cplx<T>* sb = buf + (rr >> 1) * pl.ldseq;
-    Q4<T> o;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int j = j0 + k;
-      if (j < n) {
-        const cplx<T> v = sb[spad(mperm(j, n))];
-        o.a[k] = (rr & 1) ? -v.y : v.x;  // 1/n folded into dct3w
-      } else {
-        o.a[k] = (T)0;
-      }
-    }
-    st4(out + (long long)(i0 + rr) * g.ld + j0, o);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K2 family: element phase over `rows_per_cta` rows, then a row DCT-II of the
-// staged values.  Two rows share one complex FFT (real + imaginary part).
-// ---------------------------------------------------------------------------
-template <typename T, int EMAX, int LS, class Pol>
-__global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, EMAX)) k_rows_fwd(Grid g, FftPlan<T> pl, int rows_per_cta, T* out, Pol pol, RedScratch rs, int site) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  cplx<T>* buf = reinterpret_cast<cplx<T>*>(smraw);
-  if (pol.skip()) return;
-  const int n = LS > 0 ? LS : g.m;  // static plans are only used when n == L
-  const int i0 = blockIdx.x * rows_per_cta;
-  const int nrows = min(rows_per_cta, g.n - i0);
-  const int nseq = (nrows + 1) >> 1;
-  double acc[Pol::NS];
-#pragma unroll
-  for (int s = 0; s < Pol::NS; ++s) acc[s] = 0.0;
-  if constexpr (Pol::PLAIN) {
-    rows_stage_vec<T>(g, pl, pol.src, i0, nrows, nseq, buf, n);
-  } else {
-    for (int rr = 0; rr < 2 * nseq; ++rr) {
-      cplx<T>* sb = buf + (rr >> 1) * pl.ldseq;
-      for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        const T val = (rr < nrows) ? pol.elem(g, i0 + rr, j, acc) : (T)0;
-        T* slot = reinterpret_cast<T*>(sb + spad(mperm(j, n)));
-        slot[rr & 1] = val;
-      }
-    }
-  }
-  __syncthreads();
-  fft_n<T, EMAX, LS>(buf, nseq, pl);
-  const int half = n / 2 + 1;
-  for (int e = threadIdx.x; e < nseq * half; e += blockDim.x) {
-    const int s = e / half, k = e - s * half;
-    const int nk = (n - k) % n;
-    const cplx<T>* sb = buf + s * pl.ldseq;
-    const PairOut<T> q = dct2_post<T>(sb[spad(k)], sb[spad(nk)], k, nk, pl);
-    const long long oa = (long long)(i0 + 2 * s) * g.ld, ob = oa + g.ld;
-    const bool hasb = 2 * s + 1 < nrows;
-    out[oa + k] = q.a_k;
-    if (hasb) out[ob + k] = q.b_k;
-    if (nk != k) {
-      out[oa + nk] = q.a_nk;
-      if (hasb) out[ob + nk] = q.b_nk;
-    }
-  }
-  if constexpr (Pol::REDUCE) {
-    double tot[Pol::NS];
-    if (grid_reduce<Pol::NS>(acc, rs, site, tot) && threadIdx.x == 0) pol.finish(g, tot);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K4 / API: row DCT-III (orthonormal inverse) of `in` into `out`.
-// ---------------------------------------------------------------------------
-template <typename T, int EMAX, int LS>
-__global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, EMAX)) k_rows_inv(Grid g, FftPlan<T> pl, int rows_per_cta, const T* __restrict__ in, T* out,
-                           const PcgCtrl* ctrl) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  cplx<T>* buf = reinterpret_cast<cplx<T>*>(smraw);
-  if (ctrl && ctrl->done) return;
-  const int n = LS > 0 ? LS : g.m;  // static plans are only used when n == L
-  const int i0 = blockIdx.x * rows_per_cta;
-  const int nrows = min(rows_per_cta, g.n - i0);
-  const int nseq = (nrows + 1) >> 1;
-  const int half = n / 2 + 1;
-  constexpr int UNR = 4;  // pairs per thread with loads in flight together
-  for (int base = 0; base < nseq * half; base += UNR * blockDim.x) {
-    T ak[UNR], ank[UNR], bk[UNR], bnk[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int e = base + u * blockDim.x + threadIdx.x;
-      if (e < nseq * half) {
-        const int s = e / half, k = e - s * half;
-        const int nk = (n - k) % n;
-        const long long oa = (long long)(i0 + 2 * s) * g.ld, ob = oa + g.ld;
-        const bool hasb = 2 * s + 1 < nrows;
-        ak[u] = __ldg(in + oa + k);
-        ank[u] = __ldg(in + oa + nk);
-        bk[u] = hasb ? __ldg(in + ob + k) : (T)0;
-        bnk[u] = hasb ? __ldg(in + ob + nk) : (T)0;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int e = base + u * blockDim.x + threadIdx.x;
-      if (e < nseq * half) {
-        const int s = e / half, k = e - s * half;
-        const int nk = (n - k) % n;
-        cplx<T> ck, cnk;
-        dct3_pre<T>(ak[u], ank[u], bk[u], bnk[u], k, nk, pl, ck, cnk);
-        cplx<T>* sb = buf + s * pl.ldseq;
-        sb[spad(k)] = ck;
-        if (nk != k) sb[spad(nk)] = cnk;
-      }
-    }
-  }
-  __syncthreads();
-  fft_n<T, EMAX, LS>(buf, nseq, pl);
-  rows_unstage_vec<T>(g, pl, buf, out, i0, nrows, n);
-}
 
 // ---------------------------------------------------------------------------
 // Column-panel staging for K3.  A panel is W = 2 * nseq columns x n rows;
@@ -216,7 +37,7 @@ __device__ __forceinline__ void panel_load(const Grid& g, const FftPlan<T>& pl, 
                                            int W, int ncols, int nseq, cplx<T>* buf, const int n) {
   using V = typename V16<T>::type;
   constexpr int VN = V16<T>::N;
-  constexpr int UNR = 8;
+  constexpr int UNR = 4;
   if (ncols == W && W % VN == 0) {
     const int vpr = W / VN;
     const int items = n * vpr;

@@ -1,0 +1,153 @@
+// Pipelined row transforms (K2b: row DCT-II, K4: row DCT-III) on sm_100a.
+//
+// One CTA per row pair (one packed complex FFT).  The two raw rows are
+// fetched by the bulk-copy engine (TMA: cp.async.bulk + mbarrier transaction
+// counting) in one shot, without registers or per-thread loads; several CTAs
+// per SM overlap their copies with each other's FFTs.  (A persistent variant
+// that prefetched the next pair made ptxas hoist every thread-invariant
+// twiddle and address out of the loop and spill; one pair per CTA compiles to
+// 64 registers.)
+#pragma once
+
+#include "pu_pcg.cuh"
+
+namespace pu {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on *m
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "PU_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra PU_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(m)),
+      "r"(parity)
+      : "memory");
+}
+
+// Opaque copy of a pointer: stops the compiler from hoisting per-iteration
+// shared-memory addresses out of the persistent loop (it did, and spilled).
+template <typename P>
+__device__ __forceinline__ P* launder_ptr(P* p) {
+  unsigned long long v = reinterpret_cast<unsigned long long>(p);
+  asm volatile("" : "+l"(v));
+  return reinterpret_cast<P*>(v);
+}
+
+// bytes of one staged row (multiple of 16 for cp.async.bulk)
+__host__ __device__ constexpr unsigned stage_row_bytes(int n, int tsize) {
+  return ((unsigned)n * (unsigned)tsize + 15u) & ~15u;
+}
+// dynamic shared memory of k_rows_pipe
+__host__ __device__ constexpr size_t rows_pipe_smem(int n, int tsize, int ldseq) {
+  return 128 + 2 * (size_t)stage_row_bytes(n, tsize) + (size_t)ldseq * 2 * tsize;
+}
+
+template <typename T, int EMAX, int LS, bool INV>
+__global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, EMAX))
+    k_rows_pipe(Grid g, FftPlan<T> pl, const T* __restrict__ in, T* __restrict__ out, const PcgCtrl* ctrl) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  if (ctrl && ctrl->done) return;
+  const int n = LS > 0 ? LS : g.m;  // static plans only when n == L
+  const int S = (g.n + 1) >> 1;     // row pairs
+  const unsigned RB = stage_row_bytes(n, sizeof(T));
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw);
+  T* sa = reinterpret_cast<T*>(smraw + 128);
+  T* sb = reinterpret_cast<T*>(smraw + 128 + RB);
+  cplx<T>* buf0 = reinterpret_cast<cplx<T>*>(smraw + 128 + 2 * RB);
+  if (threadIdx.x == 0) {
+    mbar_init(mbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int seq) {  // one thread
+    const int ia = 2 * seq;
+    const bool hb = ia + 1 < g.n;
+    mbar_expect_tx(mbar, hb ? 2 * RB : RB);
+    bulk_g2s(sa, in + (long long)ia * g.ld, RB, mbar);
+    if (hb) bulk_g2s(sb, in + (long long)(ia + 1) * g.ld, RB, mbar);
+  };
+  const int s = blockIdx.x;
+  if (threadIdx.x == 0 && s < S) issue(s);
+  const int half = n / 2 + 1;
+  if (s < S) {
+    cplx<T>* buf = buf0;
+    mbar_wait(mbar, 0);
+    const int ia = 2 * s;
+    const bool hasb = ia + 1 < g.n;
+    if constexpr (!INV) {
+      // Makhoul permutation + (a + i b) packing
+      for (int j0 = 4 * threadIdx.x; j0 < n; j0 += 4 * blockDim.x) {
+        if (j0 + 4 <= n) {
+          const Q4<T> a = ld4(sa + j0);
+          const Q4<T> b = hasb ? ld4(sb + j0) : zero4<T>();
+#pragma unroll
+          for (int k = 0; k < 4; ++k) buf[spad(mperm(j0 + k, n))] = mk<T>(a.a[k], b.a[k]);
+        } else {
+          for (int j = j0; j < n; ++j) buf[spad(mperm(j, n))] = mk<T>(sa[j], hasb ? sb[j] : (T)0);
+        }
+      }
+    } else {
+      for (int k = threadIdx.x; k < half; k += blockDim.x) {
+        const int nk = (n - k) % n;
+        cplx<T> ck, cnk;
+        dct3_pre<T>(sa[k], sa[nk], hasb ? sb[k] : (T)0, hasb ? sb[nk] : (T)0, k, nk, pl, ck, cnk);
+        buf[spad(k)] = ck;
+        if (nk != k) buf[spad(nk)] = cnk;
+      }
+    }
+    __syncthreads();
+    fft_n<T, EMAX, LS>(buf, 1, pl);
+    const long long oa = (long long)ia * g.ld, ob = oa + g.ld;
+    if constexpr (!INV) {
+      for (int k = threadIdx.x; k < half; k += blockDim.x) {
+        const int nk = (n - k) % n;
+        const PairOut<T> q = dct2_post<T>(buf[spad(k)], buf[spad(nk)], k, nk, pl);
+        out[oa + k] = q.a_k;
+        if (hasb) out[ob + k] = q.b_k;
+        if (nk != k) {
+          out[oa + nk] = q.a_nk;
+          if (hasb) out[ob + nk] = q.b_nk;
+        }
+      }
+    } else {
+      const int cpr = (n + 3) >> 2;
+      for (int e = threadIdx.x; e < 2 * cpr; e += blockDim.x) {
+        const int rr = e >= cpr, j0 = (e - rr * cpr) * 4;
+        if (rr && !hasb) continue;
+        Q4<T> o;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int j = j0 + k;
+          if (j < n) {
+            const cplx<T> v = buf[spad(mperm(j, n))];
+            o.a[k] = rr ? -v.y : v.x;  // 1/n folded into dct3w
+          } else {
+            o.a[k] = (T)0;
+          }
+        }
+        st4(out + (rr ? ob : oa) + j0, o);
+      }
+    }
+  }
+}
+
+}  // namespace pu
