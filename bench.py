@@ -49,6 +49,31 @@ def peaks():
     return 6650.0, "fallback"
 
 
+NCU_NAME = {  # bench kernel kind -> kernel name prefix in the ncu captures under profiles/
+    "K1_p_Ap_pAp": "k_pcg_p_v<{t}>",
+    "K2a_update_norms": "k_pcg_r_v<{t}, 1, 0, 2>",
+    "K2b_row_dct": "k_rows_pipe<{t}, ",
+    "K3_coldct_spectral": "k_cols_spec<{t}, ",
+    "K4_row_idct": "k_rows_pipe<{t}, ",
+}
+
+
+def ncu_traffic(kind, dtype, n):
+    """DRAM bytes per launch of `kind` from the committed ncu capture (or None)."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path) or kind not in NCU_NAME or n != 4096:
+        return None
+    with open(path) as fh:
+        table = json.load(fh)["dram_bytes_per_launch"]
+    t = "float" if dtype == "fp32" else "double"
+    want = NCU_NAME[kind].format(t=t)
+    suffix = {"K2b_row_dct": ", 0>", "K4_row_idct": ", 1>", "K3_coldct_spectral": ", 2>"}.get(kind, "")
+    for k, v in table.items():
+        if k.startswith(want) and k.endswith(suffix or k[-1]):
+            return v
+    return None
+
+
 def algorithmic_bytes(n, m, e):
     """per-launch compulsory bytes of K1..K4 and of one PCG iteration."""
     u = n * m
@@ -329,7 +354,8 @@ def main():
         "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "bytes_per_launch": alg[dom],
         "avg_launch_ms": per_kind[dom]["avg_ms"], "share_of_kernel_time": per_kind[dom]["total_ms"] / timed_total,
-        "traffic": None,
+        "traffic": ncu_traffic(dom, args.dtype, n),
+        "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)",
         "pcg_iteration": {"bytes": alg["iteration"], "ms": iter_ms,
                           "achieved_gbs": alg["iteration"] / (iter_ms / 1e3) / 1e9 if iter_ms else None,
                           "frac": (alg["iteration"] / (iter_ms / 1e3) / 1e9) / hbm if iter_ms else None},
