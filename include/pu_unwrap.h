@@ -77,6 +77,8 @@ int pu_describe(const pu_handle* h, char* buf, int cap);
 /* Layout helpers: compact fp64 (rows x cols, pitch lds) <-> plane. */
 int pu_pack(pu_handle* h, const double* src, int64_t lds, int rows, int cols, void* dst, void* stream);
 int pu_unpack(pu_handle* h, const void* src, int rows, int cols, double* dst, void* stream);
+/* plane -> compact (rows x cols) array in the handle's dtype (for half-size D2H in fp32 mode). */
+int pu_unpack_native(pu_handle* h, const void* src, int rows, int cols, void* dst, void* stream);
 int pu_fill(pu_handle* h, void* dst, int nplanes, double value, void* stream);
 int pu_copy(pu_handle* h, const void* src, void* dst, int nplanes, void* stream);
 

@@ -30,6 +30,7 @@ SIGNATURES = {
     "pu_describe": (_i, [_vp, ctypes.c_char_p, _i]),
     "pu_pack": (_i, [_vp, _vp, _i64, _i, _i, _vp, _vp]),
     "pu_unpack": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
+    "pu_unpack_native": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
     "pu_fill": (_i, [_vp, _vp, _i, _d, _vp]),
     "pu_copy": (_i, [_vp, _vp, _vp, _i, _vp]),
     "pu_init_state": (_i, [_vp, _vp, _vp, _vp, _vp]),

@@ -563,7 +563,17 @@ int pu_pack(pu_handle* h, const double* src, int64_t lds, int rows, int cols, vo
 int pu_unpack(pu_handle* h, const void* src, int rows, int cols, double* dst, void* stream) {
   PU_DISPATCH(h, {
     if (rows > 0 && cols > 0) {
-      k_unpack<T><<<std::min(rows, 148 * 8), I.ew_threads, 0, ST(stream)>>>(I.g, CP(src), rows, cols, dst);
+      k_unpack<T, double><<<std::min(rows, 148 * 8), I.ew_threads, 0, ST(stream)>>>(I.g, CP(src), rows, cols, dst);
+      PU_LAUNCH_CHECK();
+    }
+  });
+  return PU_OK;
+}
+
+int pu_unpack_native(pu_handle* h, const void* src, int rows, int cols, void* dst, void* stream) {
+  PU_DISPATCH(h, {
+    if (rows > 0 && cols > 0) {
+      k_unpack<T, T><<<std::min(rows, 148 * 8), I.ew_threads, 0, ST(stream)>>>(I.g, CP(src), rows, cols, MP(dst));
       PU_LAUNCH_CHECK();
     }
   });

@@ -137,11 +137,11 @@ __global__ void k_pack(Grid g, const double* __restrict__ src, long long lds, in
   }
 }
 
-template <typename T>
-__global__ void k_unpack(Grid g, const T* __restrict__ src, int rows, int cols, double* dst) {
+template <typename T, typename D>
+__global__ void k_unpack(Grid g, const T* __restrict__ src, int rows, int cols, D* dst) {
   for (int i = blockIdx.x; i < rows; i += gridDim.x)
     for (int j = threadIdx.x; j < cols; j += blockDim.x)
-      dst[(long long)i * cols + j] = (double)src[(long long)i * g.ld + j];
+      dst[(long long)i * cols + j] = (D)src[(long long)i * g.ld + j];
 }
 
 template <typename T>

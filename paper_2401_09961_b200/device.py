@@ -130,6 +130,46 @@ class Workspace:
             self.call("pu_unpack", _ptr(src), rows, cols, _ptr(out), self.stream())
         return out
 
+    def pinned(self, name, shape, tdtype):
+        """Persistent page-locked host staging buffer (allocated once per workspace)."""
+        torch = _torch()
+        key = ("pin", name)
+        t = self._bufs.get(key)
+        if t is None or tuple(t.shape) != tuple(shape) or t.dtype != tdtype:
+            t = torch.empty(shape, dtype=tdtype, pin_memory=True)
+            self._bufs[key] = t
+        return t
+
+    def upload_grid(self, x):
+        """Host (numpy / CPU tensor) fp64 grid -> device, through pinned staging."""
+        torch = _torch()
+        src = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)) if isinstance(x, np.ndarray) else x
+        if not src.is_pinned():
+            stage = self.pinned("x_in", tuple(src.shape), torch.float64)
+            stage.copy_(src)  # multi-threaded host copy
+            src = stage
+        return src.to(self.device, non_blocking=True)
+
+    def download_system(self, x):
+        """Device system vector -> fresh host fp64 numpy (u, vv, vh).
+
+        The compact blocks move in the handle's dtype through persistent
+        pinned buffers (full link bandwidth; half the bytes in fp32 mode),
+        then one multi-threaded host copy widens them into new fp64 arrays."""
+        torch = _torch()
+        n, m = self.n, self.m
+        shapes = ((n, m), (n - 1, m), (n, m - 1))
+        outs = []
+        for idx, (r, c) in enumerate(shapes):
+            dev = torch.empty((max(r, 0), max(c, 0)), dtype=self.tdtype, device=self.device)
+            if r > 0 and c > 0:
+                self.call("pu_unpack_native", _ptr(x[idx]), r, c, _ptr(dev), self.stream())
+            pin = self.pinned(f"out{idx}", (max(r, 0), max(c, 0)), self.tdtype)
+            pin.copy_(dev, non_blocking=True)
+            outs.append(pin)
+        torch.cuda.current_stream(self.device).synchronize()
+        return tuple(torch.empty(p.shape, dtype=torch.float64).copy_(p).numpy() for p in outs)
+
     def to_system(self, u, vv, vh, dst=None):
         dst = dst if dst is not None else self.planes(3)
         keep = [self.pack(u, dst[0]), self.pack(vv, dst[1]), self.pack(vh, dst[2])]

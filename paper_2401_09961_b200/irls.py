@@ -135,21 +135,26 @@ def unwrap(x, c: WeightField | None = None, model: ModelParams | None = None, pa
     torch = _torch()
     dev = torch.device(device) if device is not None else (
         x.device if isinstance(x, torch.Tensor) and x.is_cuda else torch.device("cuda", torch.cuda.current_device()))
-    if isinstance(x, torch.Tensor):
-        if x.dim() != 2 or x.shape[0] < 1 or x.shape[1] < 1:
-            raise ValueError(f"phase grid must be 2-D and non-empty, got shape {tuple(x.shape)}")
-        # host (ideally pinned) tensors are copied first and validated on the device
-        x_dev = x.to(device=dev, dtype=torch.float64, non_blocking=True)
-        lo_hi = torch.stack([x_dev.min(), x_dev.max(), torch.isfinite(x_dev).all().to(torch.float64)]).cpu()
-        if lo_hi[2] != 1.0:
-            raise ValueError("phase grid contains non-finite values")
-        if float(lo_hi[0]) < 0.0 or float(lo_hi[1]) >= 2.0 * np.pi:
-            raise ValueError("wrapped phase values must lie in [0, 2*pi)")
-        n, m = x_dev.shape
+    if isinstance(x, np.ndarray) and not np.issubdtype(x.dtype, np.number):
+        raise ValueError("phase grid must be numeric")
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        x_dev = x.to(device=dev, dtype=torch.float64)
     else:
-        arr = validate_wrapped(x)
-        n, m = arr.shape
-        x_dev = torch.from_numpy(arr).to(dev)
+        arr = x if isinstance(x, torch.Tensor) else np.asarray(x, dtype=np.float64)
+        if arr.ndim != 2 or arr.shape[0] < 1 or arr.shape[1] < 1:
+            raise ValueError(f"phase grid must be 2-D and non-empty, got shape {tuple(arr.shape)}")
+        ws_in = Workspace.get(int(arr.shape[0]), int(arr.shape[1]), dtype, (model or ModelParams()).tau,
+                              (model or ModelParams()).delta, dev)
+        x_dev = ws_in.upload_grid(arr if isinstance(arr, torch.Tensor) else arr)
+    if x_dev.dim() != 2 or x_dev.shape[0] < 1 or x_dev.shape[1] < 1:
+        raise ValueError(f"phase grid must be 2-D and non-empty, got shape {tuple(x_dev.shape)}")
+    # phase.py:100-115 on the device: finite, within [0, 2pi)
+    chk = torch.stack([x_dev.min(), x_dev.max(), torch.isfinite(x_dev).all().to(torch.float64)]).cpu()
+    if chk[2] != 1.0:
+        raise ValueError("phase grid contains non-finite values")
+    if float(chk[0]) < 0.0 or float(chk[1]) >= 2.0 * np.pi:
+        raise ValueError("wrapped phase values must lie in [0, 2*pi)")
+    n, m = int(x_dev.shape[0]), int(x_dev.shape[1])
     model = model or ModelParams()
     params = params or IrlsParams()
     if c is not None and (c.cv.shape != (n - 1, m) or c.ch.shape != (n, m - 1)):
@@ -157,5 +162,5 @@ def unwrap(x, c: WeightField | None = None, model: ModelParams | None = None, pa
     if gradient_lo not in (0.0, 0, -np.pi):
         raise ValueError(f"lo must be 0 or -pi, got {gradient_lo!r}")
     run, trace = unwrap_device(x_dev, c, model, params, gradient_lo, dtype)
-    u, vv, vh = run.result_arrays()
-    return UnwrapResult(u=u.cpu().numpy(), vv=vv.cpu().numpy(), vh=vh.cpu().numpy(), trace=trace)
+    u, vv, vh = run.ws.download_system(run.S)
+    return UnwrapResult(u=u, vv=vv, vh=vh, trace=trace)
