@@ -379,9 +379,9 @@ struct Impl : HandleBase {
 
   // ---- preconditioner passes ----
   int sylvester(const T* r, T* z, T* spec, cudaStream_t st) {
-    PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, nullptr));
+    PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, nullptr, nullptr, 0));
     PU_DCT(cops.cols(MODE_API, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, nullptr, rs, S_K3, 0));
-    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, z, nullptr));
+    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, z, nullptr, nullptr, 0));
     return PU_OK;
   }
 
@@ -402,19 +402,20 @@ struct Impl : HandleBase {
     tm.end(st, e, TK_START, -1);
     // z = M r, rho = r.z (pcg.py:77-79)
     e = tm.begin(st);
-    k_pcg_r_v<T, false, false, MODE_INIT><<<vg, 256, 0, st>>>(g, nullptr, dv, dh, x, r, z, ctrl, norms, rs, S_K2, -1);
+    k_pcg_r_v<T, false, false, MODE_INIT><<<vg, 256, 0, st>>>(g, nullptr, dv, dh, x, r, ctrl, norms, rs, S_K2, -1);
     PU_LAUNCH_CHECK();
     tm.end(st, e, TK_K2, -1);
     e = tm.begin(st);
-    PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl));
+    PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl, nullptr, 0));
     tm.end(st, e, TK_K2B, -1);
     e = tm.begin(st);
     PU_DCT(cops.cols(MODE_INIT, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, ctrl, rs, S_K3, -1));
     tm.end(st, e, TK_K3, -1);
-    e = tm.begin(st);
-    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, z, ctrl));
-    tm.end(st, e, TK_K4, -1);
+    // p of iteration k lives in pbuf[k & 1]; K4 writes its u block (p = z at k = 0)
     T* pbuf[2] = {p0, p1};
+    e = tm.begin(st);
+    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, pbuf[0], ctrl, pbuf[1], 1));
+    tm.end(st, e, TK_K4, -1);
     const int chunk = 64;
     for (int it = 0; it < max_iters; ++it) {
       if (it > 0 && it % chunk == 0) {
@@ -425,7 +426,7 @@ struct Impl : HandleBase {
       T* pn = pbuf[it & 1];
       const T* po = pbuf[(it + 1) & 1];
       e = tm.begin(st);
-      k_pcg_p_v<T><<<vg, 256, 0, st>>>(g, z, po, pn, dv, dh, ctrl, rs, S_K1, it);
+      k_pcg_p_v<T><<<vg, 256, 0, st>>>(g, r, po, pn, dv, dh, ctrl, rs, S_K1, it);
       PU_LAUNCH_CHECK();
       tm.end(st, e, TK_K1, it);
       if ((it + 1) % 50 == 0) {
@@ -434,23 +435,23 @@ struct Impl : HandleBase {
         PU_LAUNCH_CHECK();
         tm.end(st, e, TK_UPD, it);
         e = tm.begin(st);
-        k_pcg_r_v<T, false, true, MODE_ITER><<<vg, 256, 0, st>>>(g, pn, dv, dh, x, r, z, ctrl, norms, rs, S_K2, it);
+        k_pcg_r_v<T, false, true, MODE_ITER><<<vg, 256, 0, st>>>(g, pn, dv, dh, x, r, ctrl, norms, rs, S_K2, it);
         PU_LAUNCH_CHECK();
         tm.end(st, e, TK_K2, it);
       } else {
         e = tm.begin(st);
-        k_pcg_r_v<T, true, false, MODE_ITER><<<vg, 256, 0, st>>>(g, pn, dv, dh, x, r, z, ctrl, norms, rs, S_K2, it);
+        k_pcg_r_v<T, true, false, MODE_ITER><<<vg, 256, 0, st>>>(g, pn, dv, dh, x, r, ctrl, norms, rs, S_K2, it);
         PU_LAUNCH_CHECK();
         tm.end(st, e, TK_K2, it);
       }
       e = tm.begin(st);
-      PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl));
+      PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl, nullptr, 0));
       tm.end(st, e, TK_K2B, it);
       e = tm.begin(st);
       PU_DCT(cops.cols(MODE_ITER, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, ctrl, rs, S_K3, it));
       tm.end(st, e, TK_K3, it);
-      e = tm.begin(st);
-      PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, z, ctrl));
+      e = tm.begin(st);  // u block of p for iteration it + 1: beta p_u + z_u
+      PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, pbuf[(it + 1) & 1], ctrl, pn, 0));
       tm.end(st, e, TK_K4, it);
     }
     return PU_OK;

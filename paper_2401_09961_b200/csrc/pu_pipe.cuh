@@ -61,9 +61,13 @@ __host__ __device__ constexpr size_t rows_pipe_smem(int n, int tsize, int ldseq)
   return 128 + 2 * (size_t)stage_row_bytes(n, tsize) + (size_t)ldseq * 2 * tsize;
 }
 
+// INV with `pold` != nullptr (PCG K4): out = beta * pold + DCT-III(in), i.e.
+// the u block of the next search direction (pcg.py:107-108); `first` gives
+// out = DCT-III(in) (p = z at iteration 0).
 template <typename T, int EMAX, int LS, bool INV>
 __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, EMAX))
-    k_rows_pipe(Grid g, FftPlan<T> pl, const T* __restrict__ in, T* __restrict__ out, const PcgCtrl* ctrl) {
+    k_rows_pipe(Grid g, FftPlan<T> pl, const T* __restrict__ in, T* __restrict__ out, const PcgCtrl* ctrl,
+                const T* __restrict__ pold, int first) {
   extern __shared__ __align__(128) unsigned char smraw[];
   if (ctrl && ctrl->done) return;
   const int n = LS > 0 ? LS : g.m;  // static plans only when n == L
@@ -130,6 +134,8 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
       }
     } else {
       const int cpr = (n + 3) >> 2;
+      const bool axpy = pold != nullptr && !first;
+      const T beta = axpy ? (T)ctrl->beta : (T)0;
       for (int e = threadIdx.x; e < 2 * cpr; e += blockDim.x) {
         const int rr = e >= cpr, j0 = (e - rr * cpr) * 4;
         if (rr && !hasb) continue;
@@ -144,7 +150,13 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
             o.a[k] = (T)0;
           }
         }
-        st4(out + (rr ? ob : oa) + j0, o);
+        const long long oo = (rr ? ob : oa) + j0;
+        if (axpy) {
+          const Q4<T> pp = ldg4(pold + oo);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) o.a[k] = (j0 + k < n) ? add_rn(mul_rn(beta, pp.a[k]), o.a[k]) : (T)0;
+        }
+        st4(out + oo, o);
       }
     }
   }

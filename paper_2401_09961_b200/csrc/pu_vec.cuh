@@ -5,10 +5,10 @@
 // ~20 independent loads in flight instead of one scalar chain per cell.  Pitch
 // padding (j >= m) is read as zero and written back as zero.
 //
-//   k_pcg_p_v     K1: p <- beta p + z (z at it = 0); A p from the stencil of the
-//                 new p (recomputed at the neighbours); p'Ap; alpha (pcg.py:82-89)
+//   k_pcg_p_v     K1: slack p_s <- beta p_s + r_s / (d + 1/tau) (p_u came from
+//                 K4); A p from the stencil of the new p; p'Ap; alpha (pcg.py:82-89)
 //   k_pcg_r_v     K2a: x += alpha p; r -= alpha A p; optional mean re-projection;
-//                 ||r||; z_s = r_s / (d + 1/tau); rho_s (pcg.py:90-104,
+//                 ||r||; rho_s = <r_s, r_s / (d + 1/tau)> (pcg.py:90-104,
 //                 preconditioner.py:115); the row DCT of r_u runs next (K2b)
 //   k_pcg_start_v x = x0, r = b - A x0, ||b||, ||r0|| (pcg.py:59-75)
 #pragma once
@@ -97,47 +97,60 @@ template <typename T>
 __device__ __forceinline__ T ldg_or0(const T* p, bool ok) { return ok ? __ldg(p) : (T)0; }
 
 // ---------------------------------------------------------------------------
-// K1
+// K1.  The u block of the new search direction, p_u = beta p_u_old + z_u, was
+// already written by the row DCT-III kernel (K4) of the previous iteration;
+// here the slack blocks follow: z_s = r_s / (d + 1/tau) (never stored) and
+// p_s = beta p_s_old + z_s (z_s at it = 0).  Then A p from the stencil of the
+// new p (neighbours recomputed the same way) and p'Ap.  (pcg.py:82-89, 102-108)
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(256) k_pcg_p_v(Grid g, const T* __restrict__ z, const T* __restrict__ pold,
-                                                 T* __restrict__ pnew, const T* __restrict__ dv,
-                                                 const T* __restrict__ dh, PcgCtrl* ctrl, RedScratch rs, int site,
-                                                 int it) {
+__global__ void __launch_bounds__(256, 4) k_pcg_p_v(Grid g, const T* __restrict__ r, const T* __restrict__ pold,
+                                                    T* __restrict__ pnew, const T* __restrict__ dv,
+                                                    const T* __restrict__ dh, PcgCtrl* ctrl, RedScratch rs, int site,
+                                                    int it) {
   if (ctrl->done) return;
   const bool first = it == 0;
   const T beta = (T)ctrl->beta;
+  const T inv = (T)g.inv_tau;
   const long long P = g.plane, ld = g.ld;
-  auto upd4 = [&](long long o) -> Q4<T> {  // p_new = beta p_old + z  (pcg.py:107-108)
-    Q4<T> zz = ldg4(z + o);
-    if (first) return zz;
-    const Q4<T> pp = ldg4(pold + o);
+  // slack p at 4 cells of row i (plane offset po, diagonal d), masked to valid arcs
+  auto ps4 = [&](long long o, long long po, const T* d, int i, int j0, bool vert) -> Q4<T> {
+    const Q4<T> rr = ldg4(r + o + po), dd = ldg4(d + o);
+    Q4<T> out;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) zz.a[k] = add_rn(mul_rn(beta, pp.a[k]), zz.a[k]);
-    return zz;
-  };
-  auto upd1 = [&](long long o, bool ok) -> T {
-    if (!ok) return (T)0;
-    const T zz = __ldg(z + o);
-    return first ? zz : add_rn(mul_rn(beta, __ldg(pold + o)), zz);
+    for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
+      const bool ok = vert ? (i < g.n - 1 && j < g.m) : (j < g.m - 1);
+      out.a[k] = ok ? rr.a[k] / (dd.a[k] + inv) : (T)0;
+    }
+    if (!first) {
+      const Q4<T> pp = ldg4(pold + o + po);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) out.a[k] = add_rn(mul_rn(beta, pp.a[k]), out.a[k]);
+    }
+    return out;
   };
   double acc[1] = {0.0};
   PU_FOR_CHUNKS(g, i, j0) {
     const long long o = (long long)i * ld + j0;
     Stencil4<T> s;
-    s.u = upd4(o);
-    s.v = upd4(o + P);
-    s.h = upd4(o + 2 * P);
-    s.ua = i > 0 ? upd4(o - ld) : zero4<T>();
-    s.va = i > 0 ? upd4(o - ld + P) : zero4<T>();
-    s.ub = i < g.n - 1 ? upd4(o + ld) : zero4<T>();
-    s.ul = upd1(o - 1, j0 > 0);
-    s.hl = upd1(o - 1 + 2 * P, j0 > 0);
-    s.ur = upd1(o + 4, j0 + 4 < g.m);
+    s.u = ldg4(pnew + o);
+    s.ua = i > 0 ? ldg4(pnew + o - ld) : zero4<T>();
+    s.ub = i < g.n - 1 ? ldg4(pnew + o + ld) : zero4<T>();
+    s.ul = ldg_or0(pnew + o - 1, j0 > 0);
+    s.ur = ldg_or0(pnew + o + 4, j0 + 4 < g.m);
+    s.v = ps4(o, P, dv, i, j0, true);
+    s.h = ps4(o, 2 * P, dh, i, j0, false);
+    s.va = i > 0 ? ps4(o - ld, P, dv, i - 1, j0, true) : zero4<T>();
+    if (j0 > 0) {  // p_h at (i, j0 - 1)
+      const T zr = (j0 - 1 < g.m - 1) ? __ldg(r + o - 1 + 2 * P) / (__ldg(dh + o - 1) + inv) : (T)0;
+      s.hl = first ? zr : add_rn(mul_rn(beta, __ldg(pold + o - 1 + 2 * P)), zr);
+    } else {
+      s.hl = (T)0;
+    }
     const Q4<T> d1 = ldg4(dv + o), d2 = ldg4(dh + o);
     Q4<T> au, av, ah;
     apply4<T>(g, i, j0, s, d1, d2, au, av, ah);
-    st4(pnew + o, s.u);
     st4(pnew + o + P, s.v);
     st4(pnew + o + 2 * P, s.h);
 #pragma unroll
@@ -164,10 +177,9 @@ __global__ void __launch_bounds__(256) k_pcg_p_v(Grid g, const T* __restrict__ z
 // MODE_ITER finaliser: ||r|| exits (pcg.py:94-100); MODE_INIT: rho_s only.
 // ---------------------------------------------------------------------------
 template <typename T, bool UPDATE, bool SUBMEAN, int MODE>
-__global__ void __launch_bounds__(256) k_pcg_r_v(Grid g, const T* __restrict__ p, const T* __restrict__ dv,
+__global__ void __launch_bounds__(256, 3) k_pcg_r_v(Grid g, const T* __restrict__ p, const T* __restrict__ dv,
                                                  const T* __restrict__ dh, T* __restrict__ x, T* __restrict__ r,
-                                                 T* __restrict__ z, PcgCtrl* ctrl, double* res_norms, RedScratch rs,
-                                                 int site, int it) {
+                                                 PcgCtrl* ctrl, double* res_norms, RedScratch rs, int site, int it) {
   if (ctrl->done) return;
   const long long P = g.plane, ld = g.ld;
   const T alpha = (T)ctrl->alpha, nalpha = (T)(-ctrl->alpha);
@@ -213,17 +225,14 @@ __global__ void __launch_bounds__(256) k_pcg_r_v(Grid g, const T* __restrict__ p
       for (int k = 0; k < 4; ++k) ru.a[k] = (j0 + k < g.m) ? ru.a[k] - mean : (T)0;
       st4(r + o, ru);
     }
-    Q4<T> zv, zh;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 4; ++k) {  // z_s = r_s / (d + 1/tau) (preconditioner.py:115), recomputed by K1
       const int j = j0 + k;
-      zv.a[k] = (i < g.n - 1 && j < g.m) ? rv.a[k] / (d1.a[k] + inv) : (T)0;
-      zh.a[k] = (j < g.m - 1) ? rh.a[k] / (d2.a[k] + inv) : (T)0;
+      const T zv = (i < g.n - 1 && j < g.m) ? rv.a[k] / (d1.a[k] + inv) : (T)0;
+      const T zh = (j < g.m - 1) ? rh.a[k] / (d2.a[k] + inv) : (T)0;
       acc[0] += (double)ru.a[k] * ru.a[k] + (double)rv.a[k] * rv.a[k] + (double)rh.a[k] * rh.a[k];
-      acc[1] += (double)rv.a[k] * zv.a[k] + (double)rh.a[k] * zh.a[k];
+      acc[1] += (double)rv.a[k] * zv + (double)rh.a[k] * zh;
     }
-    st4(z + o + P, zv);
-    st4(z + o + 2 * P, zh);
   }
   double tot[2];
   if (grid_reduce<2>(acc, rs, site, tot) && threadIdx.x == 0) {
@@ -381,7 +390,7 @@ __device__ __forceinline__ double slack4(T c, T v, T w, T d2) {
 
 // w = sqrt((c v)^2 + delta^2), d = c^2 / w; H(x, w_prev), H(x, w)
 template <typename T>
-__global__ void __launch_bounds__(256) k_weights_hpair_v(Grid g, const T* __restrict__ x, const T* __restrict__ cv,
+__global__ void __launch_bounds__(256, 3) k_weights_hpair_v(Grid g, const T* __restrict__ x, const T* __restrict__ cv,
                                                          const T* __restrict__ ch, const T* __restrict__ gv,
                                                          const T* __restrict__ gh, const T* __restrict__ wpv,
                                                          const T* __restrict__ wph, T* __restrict__ wv,
@@ -432,7 +441,7 @@ __global__ void __launch_bounds__(256) k_weights_hpair_v(Grid g, const T* __rest
 
 // H(xa, w), H(xb, w), mean u of the accepted one, acceptance flag
 template <typename T>
-__global__ void __launch_bounds__(256) k_hpair_states_v(Grid g, const T* __restrict__ xa, const T* __restrict__ xb,
+__global__ void __launch_bounds__(256, 3) k_hpair_states_v(Grid g, const T* __restrict__ xa, const T* __restrict__ xb,
                                                         const T* __restrict__ wv, const T* __restrict__ wh,
                                                         const T* __restrict__ gv, const T* __restrict__ gh,
                                                         const T* __restrict__ cv, const T* __restrict__ ch,
@@ -474,7 +483,7 @@ __global__ void __launch_bounds__(256) k_hpair_states_v(Grid g, const T* __restr
 
 // cand = x - (1/L) grad H(x, w)   (objective.py:108-125)
 template <typename T>
-__global__ void __launch_bounds__(256) k_candidate_v(Grid g, const T* __restrict__ x, const T* __restrict__ wv,
+__global__ void __launch_bounds__(256, 3) k_candidate_v(Grid g, const T* __restrict__ x, const T* __restrict__ wv,
                                                      const T* __restrict__ wh, const T* __restrict__ gv,
                                                      const T* __restrict__ gh, const T* __restrict__ cv,
                                                      const T* __restrict__ ch, T neg_inv_lip, T* __restrict__ out) {
@@ -522,7 +531,7 @@ __global__ void __launch_bounds__(256) k_candidate_v(Grid g, const T* __restrict
 
 // dst = (sel[1] ? xa : xb) with u -= sel[0]; H(dst, w)   (irls.py:206-215)
 template <typename T>
-__global__ void __launch_bounds__(256) k_accept_v(Grid g, const T* __restrict__ xa, const T* __restrict__ xb,
+__global__ void __launch_bounds__(256, 3) k_accept_v(Grid g, const T* __restrict__ xa, const T* __restrict__ xb,
                                                   const double* sel, T* __restrict__ dst, const T* __restrict__ wv,
                                                   const T* __restrict__ wh, const T* __restrict__ gv,
                                                   const T* __restrict__ gh, const T* __restrict__ cv,
