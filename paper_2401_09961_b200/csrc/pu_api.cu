@@ -300,6 +300,7 @@ struct Impl : HandleBase {
   size_t col_smem = 0;
   int ew_grid = 1, ew_threads = 32;
   int pipe_grid = 1, pipe_threads = 64;
+  bool col_is_static = false;
   size_t pipe_smem = 0;
   RedScratch rs{};
   int* pinned_done = nullptr;
@@ -330,11 +331,17 @@ struct Impl : HandleBase {
     // threads) so two CTAs stay resident per SM; the spectral plane is
     // L2-resident between K2b and K4, so 16-byte (fp32) row segments cost L2,
     // not HBM, efficiency
-    int cc = 2;
-    cc = std::min(cc, std::max(1, (m + 1) / 2));
-    while (cc > 1 && (pcol.threads_for(cc) > 512 || pcol.smem_for(cc) > kSmemLimit)) --cc;
+    // static plans use PU_PANEL_COLS (2 packed sequences) in one thread group;
+    // runtime plans (odd sizes, Bluestein) fall back to 1 sequence if needed
+    const bool col_static = !pcol.dev.bluestein && (pcol.dev.L & (pcol.dev.L - 1)) == 0 && pcol.dev.L >= 512 &&
+                            pcol.dev.L <= (sizeof(T) == 4 ? 16384 : 8192) &&
+                            (long long)(PU_PANEL_COLS / 2) * pcol.dev.L <= 1024LL * pcol.seq_capacity &&
+                            pcol.smem_for(PU_PANEL_COLS / 2) <= kSmemLimit;
+    int cc = PU_PANEL_COLS / 2;
+    if (!col_static && pcol.smem_for(cc) > kSmemLimit) cc = 1;
     if (pcol.threads_for(cc) > pcol.max_threads() || pcol.smem_for(cc) > kSmemLimit)
       return fail(PU_ERR_UNSUPPORTED, "column length " + std::to_string(n) + " exceeds the shared-memory FFT limit");
+    col_is_static = col_static;
     cols_per_cta = 2 * cc;
     col_threads = pcol.threads_for(cc);
     col_smem = pcol.smem_for(cc);
@@ -353,7 +360,7 @@ struct Impl : HandleBase {
 
   int set_smem_attrs() {
     rops = ops_for<T>(prow.dev.bluestein ? 0 : prow.dev.L);
-    cops = ops_for<T>(pcol.dev.bluestein ? 0 : pcol.dev.L);
+    cops = ops_for<T>(col_is_static ? pcol.dev.L : 0);
     // the attribute is per kernel (process-wide): always raise it to the cap so
     // that handles of different sizes sharing an instantiation never shrink it
     PU_CUDA(rops.set_attrs(kSmemLimit, kSmemLimit));

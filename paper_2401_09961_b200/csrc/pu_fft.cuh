@@ -17,6 +17,7 @@
 namespace pu {
 
 #define PU_FFT_MAX_STAGES 20
+#define PU_PANEL_COLS 4  // columns per CTA of the column-transform kernel (2 packed sequences)
 #define PU_FFT_MAX_THREADS 1024  // absolute per-CTA thread cap of the transform kernels
 
 // Per-instantiation launch bounds.  Transform kernels run every sequence of
@@ -456,6 +457,10 @@ __device__ __forceinline__ void dct3_pre(T ak, T ank, T bk, T bnk, int k, int nk
     out_nk = mk<T>(uaRe - ubIm, -(uaIm + ubRe));
   }
 }
+
+// division for the spectral scaling: fast (2 ulp) in fp32, rcp-based in fp64
+__device__ __forceinline__ float fast_div(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double fast_div(double a, double b) { return a * __drcp_rn(b); }
 
 // correctly rounded reciprocal
 __device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }

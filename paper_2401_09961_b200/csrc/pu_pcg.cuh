@@ -34,7 +34,7 @@ template <> struct V16<double> { using type = double2; static constexpr int N = 
 
 template <typename T>
 __device__ __forceinline__ void panel_load(const Grid& g, const FftPlan<T>& pl, const T* __restrict__ data, int j0,
-                                           int W, int ncols, int nseq, cplx<T>* buf, const int n) {
+                                           const int W, int ncols, int nseq, cplx<T>* buf, const int n) {
   using V = typename V16<T>::type;
   constexpr int VN = V16<T>::N;
   constexpr int UNR = 4;
@@ -121,14 +121,15 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   cplx<T>* buf = reinterpret_cast<cplx<T>*>(smraw);
   if (MODE != MODE_API && ctrl->done) return;
   const int n = LS > 0 ? LS : g.n;  // static plans are only used when n == L
-  const int W = cols_per_cta;
+  // static plans: compile-time panel width; runtime plans: 4 or 2 (smem)
+  const int W = LS > 0 ? PU_PANEL_COLS : cols_per_cta;
   const int j0 = blockIdx.x * W;
   const int ncols = min(W, g.m - j0);
   const int nseq = (ncols + 1) >> 1;
   panel_load<T>(g, pl, data, j0, W, ncols, nseq, buf, n);
   __syncthreads();
   fft_n<T, EMAX, LS>(buf, nseq, pl);
-  double acc[1] = {0.0};
+  T accT = (T)0;  // per-thread partial of rho_u in T (a few dozen terms), fp64 across threads
   const int half = n / 2 + 1;
   const double tau = g.tau;
   for (int e = threadIdx.x; e < nseq * half; e += blockDim.x) {
@@ -142,14 +143,14 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
     const T la = __ldg(lam_cols + ja), lb = hasb ? __ldg(lam_cols + jb) : (T)0;
     // preconditioner.py:96-99: z = tau * r / (lam_s + lam_t), (0,0) -> 0
     const T ttau = (T)tau;
-    auto sdiv = [&](T v, T den) -> T { return den == (T)0 ? (T)0 : (ttau * v) * rcp_rn(den); };
+    auto sdiv = [&](T v, T den) -> T { return den == (T)0 ? (T)0 : fast_div(ttau * v, den); };
     const T zak = sdiv(q.a_k, lk + la), zbk = hasb ? sdiv(q.b_k, lk + lb) : (T)0;
     T zank = 0, zbnk = 0;
-    acc[0] += (double)q.a_k * zak + (hasb ? (double)q.b_k * zbk : 0.0);
+    accT += q.a_k * zak + q.b_k * zbk;
     if (nk != k) {
       zank = sdiv(q.a_nk, lnk + la);
       zbnk = hasb ? sdiv(q.b_nk, lnk + lb) : (T)0;
-      acc[0] += (double)q.a_nk * zank + (hasb ? (double)q.b_nk * zbnk : 0.0);
+      accT += q.a_nk * zank + q.b_nk * zbnk;
     } else {
       zank = zak; zbnk = zbk;
     }
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   fft_n<T, EMAX, LS>(buf, nseq, pl);
   panel_store<T>(g, pl, data, j0, W, ncols, nseq, buf, n);
   if (MODE != MODE_API) {
+    double acc[1] = {(double)accT};
     double tot[1];
     if (grid_reduce<1>(acc, rs, site, tot) && threadIdx.x == 0) {
       const double rho_next = ctrl->rho_s + tot[0];
