@@ -364,8 +364,9 @@ def main():
     # objective of the result (device eval_f) against the reference's F
     f_out = None
     try:
-        ws.call("pu_eval_f", pu.device._ptr(run.S), pu.device._ptr(run.G[0]), pu.device._ptr(run.G[1]),
-                pu.device._ptr(run.W[0]), pu.device._ptr(run.W[1]), ws.sp(ws.S_F), ws.stream())
+        cw = run.weight_planes()
+        ws.call("pu_eval_f", pu.device._ptr(run.state), pu.device._ptr(run.G[0]), pu.device._ptr(run.G[1]),
+                pu.device._ptr(cw[0]), pu.device._ptr(cw[1]), ws.sp(ws.S_F), ws.stream())
         f_out = float(ws.read_block()[0][ws.S_F])
     except Exception:
         pass

@@ -112,7 +112,7 @@ int pu_apply_preconditioner(pu_handle* h, const void* r, const void* dv, const v
 
 /* objective.py:92-100 update_weights + irls.py:191 (d = c^2 / w) and the
  * H_delta pair of irls.py:176-177: out[0] = H(x, w_prev) (if wpv != NULL),
- * out[1] = H(x, w). */
+ * out[1] = H(x, w).  cv/ch may both be NULL (uniform unit weights). */
 int pu_weights_hpair(pu_handle* h, const void* x, const void* cv, const void* ch, const void* gv,
                      const void* gh, const void* wpv, const void* wph, void* wv, void* wh, void* dv, void* dh,
                      double* out, void* stream);
@@ -140,8 +140,28 @@ int pu_accept_center(pu_handle* h, const void* xa, const void* xb, const double*
                      const void* wv, const void* wh, const void* gv, const void* gh, const void* cv,
                      const void* ch, double* out, void* stream);
 
+/* One IRLS inner step, irls.py:191-205: the explicit gradient candidate of
+ * `state` (objective.py:118-125) -> cand, the PCG solve warm-started from
+ * `state` and run IN PLACE on it (it becomes the proposal; the candidate and
+ * the start-up residual share one pass over the state), then
+ * out[0] = H(proposal, w), out[1] = H(cand, w), out[2] = mean u of the
+ * accepted one, out[3] = 1.0 if the proposal is accepted.  cv/ch may both be
+ * NULL for uniform unit weights.  PCG scratch and ctrl as in pu_pcg_solve. */
+int pu_irls_step(pu_handle* h, void* state, const void* b, const void* gv, const void* gh, const void* cv,
+                 const void* ch, const void* wv, const void* wh, const void* dv, const void* dh, double lipschitz,
+                 int max_iters, double rel_tol, void* cand, void* r, void* p0, void* p1, void* spec, void* ctrl,
+                 double* res_norms, double* out, void* stream);
+
+/* irls.py:206-215 fused with the next iteration's irls.py:173-177:
+ * dst = (sel[1] ? xa : xb) with u -= sel[0]; w_next, d from dst;
+ * out[0] = H(dst, w_k), out[1] = H(dst, w_next).  dst must not alias xa/xb. */
+int pu_accept_weights(pu_handle* h, const void* xa, const void* xb, const double* sel, void* dst, const void* gv,
+                      const void* gh, const void* cv, const void* ch, const void* wkv, const void* wkh, void* wnv,
+                      void* wnh, void* dv, void* dh, double* out, void* stream);
+
 /* pcg.py:47-116 pcg_solve with apply_system and apply_preconditioner fused
- * in (5 kernels per iteration).  x = x0 on entry; x0 is not modified.
+ * in (5 kernels per iteration).  x = x0 on entry (x may alias x0: solve in
+ * place); otherwise x0 is not modified.  z is unused (kept for ABI stability).
  * r, z, p0, p1: system-vector scratch; spec: one plane.  ctrl: device
  * pu_pcg_ctrl; res_norms: device fp64 [max_iters + 1].  Enqueues without
  * synchronising when max_iters <= 64; longer budgets poll ctrl->done

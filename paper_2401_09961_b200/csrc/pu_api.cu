@@ -401,10 +401,17 @@ struct Impl : HandleBase {
   // K1 p/Ap/p'Ap, K2a residual update + slack precond + norms, K2b row DCT-II,
   // K3 column DCT pair + spectral division + rho, K4 row DCT-III.
   int pcg(const T* b, const T* x0, T* x, const T* dv, const T* dh, T* r, T* z, T* p0, T* p1, T* spec,
-          int max_iters, double rel_tol, PcgCtrl* ctrl, double* norms, cudaStream_t st) {
+          int max_iters, double rel_tol, PcgCtrl* ctrl, double* norms, cudaStream_t st,
+          const CandArgs<T>* cand = nullptr) {
     const int vg = vec_grid();
     cudaEvent_t e = tm.begin(st);
-    k_pcg_start_v<T><<<vg, 256, 0, st>>>(g, b, x0, x, r, dv, dh, ctrl, norms, rel_tol, max_iters, rs, S_START);
+    if (cand) {
+      k_pcg_start_v<T, true><<<vg, 256, 0, st>>>(g, b, x0, x, r, dv, dh, ctrl, norms, rel_tol, max_iters, rs, S_START,
+                                                  *cand);
+    } else {
+      k_pcg_start_v<T, false><<<vg, 256, 0, st>>>(g, b, x0, x, r, dv, dh, ctrl, norms, rel_tol, max_iters, rs,
+                                                   S_START, CandArgs<T>{});
+    }
     PU_LAUNCH_CHECK();
     tm.end(st, e, TK_START, -1);
     // z = M r, rho = r.z (pcg.py:77-79)
@@ -732,6 +739,44 @@ int pu_accept_center(pu_handle* h, const void* xa, const void* xb, const double*
   return PU_OK;
 }
 
+int pu_irls_step(pu_handle* h, void* state, const void* b, const void* gv, const void* gh, const void* cv,
+                 const void* ch, const void* wv, const void* wh, const void* dv, const void* dh, double lipschitz,
+                 int max_iters, double rel_tol, void* cand, void* r, void* p0, void* p1, void* spec, void* ctrl,
+                 double* res_norms, double* out, void* stream) {
+  if (max_iters < 0) return fail(PU_ERR_ARG, "max_iters must be >= 0");
+  if (rel_tol < 0) return fail(PU_ERR_ARG, "rel_tol must be >= 0");
+  if (!(lipschitz > 0)) return fail(PU_ERR_ARG, "lipschitz constant must be positive");
+  if ((cv == nullptr) != (ch == nullptr)) return fail(PU_ERR_ARG, "cv and ch must both be given or both NULL");
+  PU_DISPATCH(h, {
+    const CandArgs<T> ca{CP(gv), CP(gh), CP(cv), CP(ch), CP(wv), CP(wh), (T)(-1.0 / lipschitz), MP(cand)};
+    int rc = I.pcg(CP(b), CP(state), MP(state), CP(dv), CP(dh), MP(r), nullptr, MP(p0), MP(p1), MP(spec), max_iters,
+                   rel_tol, reinterpret_cast<PcgCtrl*>(ctrl), res_norms, ST(stream), &ca);
+    if (rc != PU_OK) return rc;
+    cudaEvent_t te_ = I.tm.begin(ST(stream));
+    k_hpair_states_v<T><<<I.vec_grid(), 256, 0, ST(stream)>>>(I.g, CP(state), CP(cand), CP(wv), CP(wh), CP(gv),
+                                                             CP(gh), CP(cv), CP(ch), I.rs, S_HPAIR, out);
+    PU_LAUNCH_CHECK();
+    I.tm.end(ST(stream), te_, TK_HPAIR, -1);
+  });
+  return PU_OK;
+}
+
+int pu_accept_weights(pu_handle* h, const void* xa, const void* xb, const double* sel, void* dst, const void* gv,
+                      const void* gh, const void* cv, const void* ch, const void* wkv, const void* wkh, void* wnv,
+                      void* wnh, void* dv, void* dh, double* out, void* stream) {
+  if (dst == xa || dst == xb) return fail(PU_ERR_ARG, "dst must not alias xa or xb");
+  if ((cv == nullptr) != (ch == nullptr)) return fail(PU_ERR_ARG, "cv and ch must both be given or both NULL");
+  PU_DISPATCH(h, {
+    cudaEvent_t te_ = I.tm.begin(ST(stream));
+    k_accept_weights_v<T><<<I.vec_grid(), 256, 0, ST(stream)>>>(I.g, CP(xa), CP(xb), sel, MP(dst), CP(gv), CP(gh),
+                                                               CP(cv), CP(ch), CP(wkv), CP(wkh), MP(wnv), MP(wnh),
+                                                               MP(dv), MP(dh), I.rs, S_ACC, out);
+    PU_LAUNCH_CHECK();
+    I.tm.end(ST(stream), te_, TK_ACCEPT, -1);
+  });
+  return PU_OK;
+}
+
 int pu_timing_enable(pu_handle* h, int on) {
   PU_DISPATCH(h, { I.tm.on = on != 0; });
   return PU_OK;
@@ -747,7 +792,6 @@ int pu_pcg_solve(pu_handle* h, const void* b, const void* x0, void* x, const voi
                  void* stream) {
   if (max_iters < 0) return fail(PU_ERR_ARG, "max_iters must be >= 0");
   if (rel_tol < 0) return fail(PU_ERR_ARG, "rel_tol must be >= 0");
-  if (x == x0) return fail(PU_ERR_ARG, "x must not alias x0");
   PU_DISPATCH(h, {
     return I.pcg(CP(b), CP(x0), MP(x), CP(dv), CP(dh), MP(r), MP(z), MP(p0), MP(p1), MP(spec), max_iters, rel_tol,
                  reinterpret_cast<PcgCtrl*>(ctrl), res_norms, ST(stream));

@@ -49,6 +49,10 @@ template <typename T>
 __device__ __forceinline__ Q4<T> zero4() {
   return Q4<T>{{(T)0, (T)0, (T)0, (T)0}};
 }
+template <typename T>
+__device__ __forceinline__ Q4<T> ones4() {
+  return Q4<T>{{(T)1, (T)1, (T)1, (T)1}};
+}
 
 // chunk loop: chunk q covers cells (i, 4c .. 4c+3), c < cpr = ceil(m / 4)
 #define PU_FOR_CHUNKS(g, i, j0)                                                            \
@@ -92,6 +96,12 @@ __device__ __forceinline__ void apply4(const Grid& g, int i, int j0, const Stenc
   }
 }
 
+// slack block of the preconditioner, z = r / (d + 1/tau) (preconditioner.py:115):
+// fast division in fp32 mode (K1 and K2a use the same expression, so rho and
+// p stay consistent), IEEE division in fp64 mode (parity with the reference)
+__device__ __forceinline__ float slack_div(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double slack_div(double a, double b) { return a / b; }
+
 // scalar neighbour load that tolerates the grid edge
 template <typename T>
 __device__ __forceinline__ T ldg_or0(const T* p, bool ok) { return ok ? __ldg(p) : (T)0; }
@@ -121,7 +131,7 @@ __global__ void __launch_bounds__(256, 4) k_pcg_p_v(Grid g, const T* __restrict_
     for (int k = 0; k < 4; ++k) {
       const int j = j0 + k;
       const bool ok = vert ? (i < g.n - 1 && j < g.m) : (j < g.m - 1);
-      out.a[k] = ok ? rr.a[k] / (dd.a[k] + inv) : (T)0;
+      out.a[k] = ok ? slack_div(rr.a[k], dd.a[k] + inv) : (T)0;
     }
     if (!first) {
       const Q4<T> pp = ldg4(pold + o + po);
@@ -143,7 +153,7 @@ __global__ void __launch_bounds__(256, 4) k_pcg_p_v(Grid g, const T* __restrict_
     s.h = ps4(o, 2 * P, dh, i, j0, false);
     s.va = i > 0 ? ps4(o - ld, P, dv, i - 1, j0, true) : zero4<T>();
     if (j0 > 0) {  // p_h at (i, j0 - 1)
-      const T zr = (j0 - 1 < g.m - 1) ? __ldg(r + o - 1 + 2 * P) / (__ldg(dh + o - 1) + inv) : (T)0;
+      const T zr = (j0 - 1 < g.m - 1) ? slack_div(__ldg(r + o - 1 + 2 * P), __ldg(dh + o - 1) + inv) : (T)0;
       s.hl = first ? zr : add_rn(mul_rn(beta, __ldg(pold + o - 1 + 2 * P)), zr);
     } else {
       s.hl = (T)0;
@@ -228,8 +238,8 @@ __global__ void __launch_bounds__(256, 3) k_pcg_r_v(Grid g, const T* __restrict_
 #pragma unroll
     for (int k = 0; k < 4; ++k) {  // z_s = r_s / (d + 1/tau) (preconditioner.py:115), recomputed by K1
       const int j = j0 + k;
-      const T zv = (i < g.n - 1 && j < g.m) ? rv.a[k] / (d1.a[k] + inv) : (T)0;
-      const T zh = (j < g.m - 1) ? rh.a[k] / (d2.a[k] + inv) : (T)0;
+      const T zv = (i < g.n - 1 && j < g.m) ? slack_div(rv.a[k], d1.a[k] + inv) : (T)0;
+      const T zh = (j < g.m - 1) ? slack_div(rh.a[k], d2.a[k] + inv) : (T)0;
       acc[0] += (double)ru.a[k] * ru.a[k] + (double)rv.a[k] * rv.a[k] + (double)rh.a[k] * rh.a[k];
       acc[1] += (double)rv.a[k] * zv + (double)rh.a[k] * zh;
     }
@@ -296,13 +306,24 @@ __global__ void __launch_bounds__(256) k_pcg_upd_sum_v(Grid g, const T* __restri
     ctrl->mean_ru = tot[0] / ((double)g.n * (double)g.m);
 }
 
-// setup: x = x0, r = b - A x0, ||b||, ||r0|| (pcg.py:59-75)
+// setup: x = x0 (skipped when x aliases x0), r = b - A x0, ||b||, ||r0||
+// (pcg.py:59-75).  CAND: also the explicit gradient step of the same state,
+// cand = x0 - (1/L) grad H(x0, w) (objective.py:108-125), from the same loads.
+// cv/ch == nullptr means uniform unit arc weights.
 template <typename T>
-__global__ void __launch_bounds__(256) k_pcg_start_v(Grid g, const T* __restrict__ b, const T* __restrict__ x0,
-                                                     T* __restrict__ x, T* __restrict__ r, const T* __restrict__ dv,
-                                                     const T* __restrict__ dh, PcgCtrl* ctrl, double* res_norms,
-                                                     double rel_tol, int max_iters, RedScratch rs, int site) {
+struct CandArgs {
+  const T* gv; const T* gh; const T* cv; const T* ch; const T* wv; const T* wh; T neg_inv_lip; T* out;
+};
+
+template <typename T, bool CAND>
+__global__ void __launch_bounds__(256, 3) k_pcg_start_v(Grid g, const T* __restrict__ b, const T* x0, T* x,
+                                                        T* __restrict__ r, const T* __restrict__ dv,
+                                                        const T* __restrict__ dh, PcgCtrl* ctrl, double* res_norms,
+                                                        double rel_tol, int max_iters, RedScratch rs, int site,
+                                                        CandArgs<T> ca) {
   const long long P = g.plane, ld = g.ld;
+  const bool copy = x != x0;
+  const T inv = (T)g.inv_tau;
   double acc[2] = {0.0, 0.0};
   PU_FOR_CHUNKS(g, i, j0) {
     const long long o = (long long)i * ld + j0;
@@ -329,8 +350,41 @@ __global__ void __launch_bounds__(256) k_pcg_start_v(Grid g, const T* __restrict
       acc[0] += (double)bu.a[k] * bu.a[k] + (double)bv.a[k] * bv.a[k] + (double)bh.a[k] * bh.a[k];
       acc[1] += (double)ru.a[k] * ru.a[k] + (double)rv.a[k] * rv.a[k] + (double)rh.a[k] * rh.a[k];
     }
-    st4(x + o, s.u); st4(x + o + P, s.v); st4(x + o + 2 * P, s.h);
+    if (copy) { st4(x + o, s.u); st4(x + o + P, s.v); st4(x + o + 2 * P, s.h); }
     st4(r + o, ru); st4(r + o + P, rv); st4(r + o + 2 * P, rh);
+    if constexpr (CAND) {
+      const Q4<T> g1 = ldg4(ca.gv + o), g2 = ldg4(ca.gh + o);
+      const Q4<T> ga = i > 0 ? ldg4(ca.gv + o - ld) : zero4<T>();
+      const T gl = ldg_or0(ca.gh + o - 1, j0 > 0);
+      const Q4<T> w1 = ldg4(ca.wv + o), w2 = ldg4(ca.wh + o);
+      Q4<T> c1, c2;
+      if (ca.cv) { c1 = ldg4(ca.cv + o); c2 = ldg4(ca.ch + o); }
+      const bool hasb = i < g.n - 1, hasa = i > 0;
+      Q4<T> ou, ov, oh;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = j0 + k;
+        const bool ok = j < g.m, hash = j < g.m - 1;
+        const T uo = s.u.a[k];
+        const T left = (k == 0) ? s.ul : s.u.a[k - 1];
+        const T right = (k == 3) ? s.ur : s.u.a[k + 1];
+        const T hleft = (k == 0) ? s.hl : s.h.a[k - 1];
+        const T gleft = (k == 0) ? gl : g2.a[k - 1];
+        T rvv = 0, rvm = 0, rhh = 0, rhm = 0;
+        if (hasb) rvv = ((s.ub.a[k] - uo) - g1.a[k]) - s.v.a[k];
+        if (hasa) rvm = ((uo - s.ua.a[k]) - ga.a[k]) - s.va.a[k];
+        if (hash) rhh = ((right - uo) - g2.a[k]) - s.h.a[k];
+        if (j > 0) rhm = ((uo - left) - gleft) - hleft;
+        const T gu = inv * ((rvm - rvv) + (rhm - rhh));
+        const T cv2 = ca.cv ? c1.a[k] * c1.a[k] : (T)1, ch2 = ca.cv ? c2.a[k] * c2.a[k] : (T)1;
+        const T gvv = cv2 / w1.a[k] * s.v.a[k] - inv * rvv;
+        const T gvh = ch2 / w2.a[k] * s.h.a[k] - inv * rhh;
+        ou.a[k] = ok ? add_rn(uo, mul_rn(ca.neg_inv_lip, gu)) : (T)0;
+        ov.a[k] = (ok && hasb) ? add_rn(s.v.a[k], mul_rn(ca.neg_inv_lip, gvv)) : (T)0;
+        oh.a[k] = hash ? add_rn(s.h.a[k], mul_rn(ca.neg_inv_lip, gvh)) : (T)0;
+      }
+      st4(ca.out + o, ou); st4(ca.out + o + P, ov); st4(ca.out + o + 2 * P, oh);
+    }
   }
   double tot[2];
   if (grid_reduce<2>(acc, rs, site, tot) && threadIdx.x == 0) {
@@ -405,7 +459,9 @@ __global__ void __launch_bounds__(256, 3) k_weights_hpair_v(Grid g, const T* __r
     const Q4<T> u = ldg4(x + o), vv = ldg4(x + o + P), vh = ldg4(x + o + 2 * P);
     const Q4<T> ub = i < g.n - 1 ? ldg4(x + o + ld) : zero4<T>();
     const T ur = ldg_or0(x + o + 4, j0 + 4 < g.m);
-    const Q4<T> c1 = ldg4(cv + o), c2 = ldg4(ch + o), g1 = ldg4(gv + o), g2 = ldg4(gh + o);
+    const Q4<T> g1 = ldg4(gv + o), g2 = ldg4(gh + o);
+    Q4<T> c1 = ones4<T>(), c2 = ones4<T>();
+    if (cv) { c1 = ldg4(cv + o); c2 = ldg4(ch + o); }
     Q4<T> p1 = zero4<T>(), p2 = zero4<T>();
     if (hasprev) { p1 = ldg4(wpv + o); p2 = ldg4(wph + o); }
     Q4<T> w1, w2, e1, e2;
@@ -451,7 +507,9 @@ __global__ void __launch_bounds__(256, 3) k_hpair_states_v(Grid g, const T* __re
   double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   PU_FOR_CHUNKS(g, i, j0) {
     const long long o = (long long)i * ld + j0;
-    const Q4<T> c1 = ldg4(cv + o), c2 = ldg4(ch + o), g1 = ldg4(gv + o), g2 = ldg4(gh + o);
+    const Q4<T> g1 = ldg4(gv + o), g2 = ldg4(gh + o);
+    Q4<T> c1 = ones4<T>(), c2 = ones4<T>();
+    if (cv) { c1 = ldg4(cv + o); c2 = ldg4(ch + o); }
     const Q4<T> w1 = ldg4(wv + o), w2 = ldg4(wh + o);
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
@@ -564,6 +622,70 @@ __global__ void __launch_bounds__(256, 3) k_accept_v(Grid g, const T* __restrict
   double tot[4];
   if (grid_reduce<4>(acc, rs, site, tot) && threadIdx.x == 0)
     out[0] = (0.5 * tot[0] + 0.5 * tot[1]) + (tot[2] + tot[3]) / (2.0 * g.tau);
+}
+
+// Acceptance and centring of iteration k fused with the weight refresh of
+// iteration k + 1 (irls.py:206-215 then 173-177): dst = (sel[1] ? xa : xb)
+// with u -= sel[0]; w_next = sqrt((c v)^2 + delta^2), d = c^2 / w_next;
+// out[0] = H(dst, w_k) (the trace value and the next h_old), out[1] =
+// H(dst, w_next) (the next h_new).  cv/ch == nullptr: unit weights.
+template <typename T>
+__global__ void __launch_bounds__(256, 3) k_accept_weights_v(Grid g, const T* __restrict__ xa,
+                                                             const T* __restrict__ xb, const double* sel,
+                                                             T* __restrict__ dst, const T* __restrict__ gv,
+                                                             const T* __restrict__ gh, const T* __restrict__ cv,
+                                                             const T* __restrict__ ch, const T* __restrict__ wkv,
+                                                             const T* __restrict__ wkh, T* __restrict__ wnv,
+                                                             T* __restrict__ wnh, T* __restrict__ dv, T* __restrict__ dh,
+                                                             RedScratch rs, int site, double* out) {
+  const long long P = g.plane, ld = g.ld;
+  const T* x = sel[1] != 0.0 ? xa : xb;
+  const T mean = (T)sel[0];
+  const T d2 = (T)(g.delta * g.delta);
+  double acc[6] = {0, 0, 0, 0, 0, 0};  // old_v, old_h, new_v, new_h, pen_v, pen_h
+  PU_FOR_CHUNKS(g, i, j0) {
+    const long long o = (long long)i * ld + j0;
+    Q4<T> u = ldg4(x + o);
+    const Q4<T> vv = ldg4(x + o + P), vh = ldg4(x + o + 2 * P);
+    Q4<T> ub = i < g.n - 1 ? ldg4(x + o + ld) : zero4<T>();
+    T ur = ldg_or0(x + o + 4, j0 + 4 < g.m);
+    const Q4<T> g1 = ldg4(gv + o), g2 = ldg4(gh + o);
+    Q4<T> c1 = ones4<T>(), c2 = ones4<T>();
+    if (cv) { c1 = ldg4(cv + o); c2 = ldg4(ch + o); }
+    const Q4<T> p1 = ldg4(wkv + o), p2 = ldg4(wkh + o);
+    Q4<T> w1, w2, e1, e2;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
+      const bool okv = i < g.n - 1 && j < g.m, okh = j < g.m - 1;
+      u.a[k] = (j < g.m) ? u.a[k] - mean : (T)0;
+      ub.a[k] = ub.a[k] - mean;
+      const T a = c1.a[k] * vv.a[k], bb = c2.a[k] * vh.a[k];
+      const T wa = sqrt(a * a + d2), wb = sqrt(bb * bb + d2);
+      w1.a[k] = okv ? wa : (T)1;
+      w2.a[k] = okh ? wb : (T)1;
+      e1.a[k] = okv ? c1.a[k] * c1.a[k] / wa : (T)0;
+      e2.a[k] = okh ? c2.a[k] * c2.a[k] / wb : (T)0;
+      if (okv) {
+        acc[0] += slack4(c1.a[k], vv.a[k], p1.a[k], d2);
+        acc[2] += slack4(c1.a[k], vv.a[k], wa, d2);
+      }
+      if (okh) {
+        acc[1] += slack4(c2.a[k], vh.a[k], p2.a[k], d2);
+        acc[3] += slack4(c2.a[k], vh.a[k], wb, d2);
+      }
+    }
+    ur = ur - mean;
+    pen4<T>(g, i, j0, u, ub, ur, vv, vh, g1, g2, acc[4], acc[5]);
+    st4(dst + o, u); st4(dst + o + P, vv); st4(dst + o + 2 * P, vh);
+    st4(wnv + o, w1); st4(wnh + o, w2); st4(dv + o, e1); st4(dh + o, e2);
+  }
+  double tot[6];
+  if (grid_reduce<6>(acc, rs, site, tot) && threadIdx.x == 0) {
+    const double pen = (tot[4] + tot[5]) / (2.0 * g.tau);
+    out[0] = (0.5 * tot[0] + 0.5 * tot[1]) + pen;
+    out[1] = (0.5 * tot[2] + 0.5 * tot[3]) + pen;
+  }
 }
 
 }  // namespace pu

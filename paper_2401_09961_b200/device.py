@@ -36,7 +36,8 @@ class Workspace:
     _lock = threading.Lock()
 
     # scalar slots (fp64) in the device scalar block
-    S_HOLD, S_HNEW, S_HPROP, S_HCAND, S_MEAN, S_TAKE, S_HACC, S_F, S_L1, S_DOT, S_EVH = range(11)
+    (S_HOLD, S_HNEW, S_HPROP, S_HCAND, S_MEAN, S_TAKE, S_HACC, S_HNEXT, S_F, S_L1, S_DOT,
+     S_EVH) = range(12)
     NSCAL = 16
 
     @classmethod

@@ -15,7 +15,7 @@ import numpy as np
 from .device import Workspace, _ptr
 from .params import (BudgetDecision, IrlsParams, IrlsTrace, IterationRecord, ModelParams,  # noqa: F401
                      UnwrapResult, cg_budget_update, lipschitz_constant, relative_improvement)
-from .pcg import pcg_device, raise_if_breakdown
+from .pcg import raise_if_breakdown
 from .phase import WeightField, validate_wrapped
 
 
@@ -25,55 +25,84 @@ def _torch():
 
 
 class DeviceUnwrap:
-    """Resident buffers and launch sequence of one unwrap (one stream)."""
+    """Resident buffers and launch sequence of one unwrap (one stream).
+
+    Per outer iteration k two fused C-ABI calls run on the device:
+      pu_irls_step      candidate step + warm-started PCG in place on the state
+                        + H(proposal), H(cand)               (irls.py:191-205)
+      pu_accept_weights select + centre + H(accepted, w_k), then the weights
+                        of iteration k+1 and H(accepted, w_{k+1})
+                        (irls.py:206-215, 173-177)
+    so the host reads one scalar block per iteration for the budget rule.
+    """
 
     def __init__(self, ws: Workspace):
         self.ws = ws
-        self.S = ws.buf("state", 3)      # accepted state
-        self.X = ws.buf("proposal", 3)   # PCG iterate / proposal
+        self.S = [ws.buf("state0", 3), ws.buf("state1", 3)]  # state ping-pong
         self.C = ws.buf("cand", 3)       # explicit-gradient candidate
         self.B = ws.buf("rhs", 3)
         self.G = ws.buf("grad", 2)       # gv, gh
-        self.W = ws.buf("cw", 2)         # cv, ch
+        self.W = None                    # arc weights cv, ch (None: uniform)
         self.Wt = [ws.buf("w0", 2), ws.buf("w1", 2)]
         self.D = ws.buf("diag", 2)       # dv, dh
+        self.R = ws.buf("pcg_r", 3)
+        self.P = [ws.buf("pcg_p0", 3), ws.buf("pcg_p1", 3)]
+        self.spec = ws.buf("spec", 1)
+        self.cur = 0
+
+    def _c(self):
+        return (None, None) if self.W is None else (_ptr(self.W[0]), _ptr(self.W[1]))
 
     def load(self, x_dev, c: WeightField | None, lo):
         ws, st = self.ws, self.ws.stream()
         torch = _torch()
         if c is None:
-            ws.call("pu_fill", _ptr(self.W), 2, 1.0, st)
-            self._keep = None
+            self.W, self._keep = None, None
         else:
+            self.W = ws.buf("cw", 2)
             self._keep = [ws.pack(c.cv, self.W[0]), ws.pack(c.ch, self.W[1])]
         x64 = x_dev if x_dev.dtype == torch.float64 else x_dev.to(torch.float64)
         self._x = x64.contiguous()
         ws.call("pu_wrapped_gradients", _ptr(self._x), int(self._x.shape[1]), _ptr(self.G[0]), _ptr(self.G[1]),
                 float(lo), st)
         ws.call("pu_build_rhs", _ptr(self.G[0]), _ptr(self.G[1]), _ptr(self.B), st)
-        ws.call("pu_init_state", _ptr(self.G[0]), _ptr(self.G[1]), _ptr(self.S), st)
-
-    def weights(self, k):
-        """update_weights + H(state, w_prev), H(state, w) -> scal[S_HOLD:S_HNEW+1]."""
-        ws, w, wp = self.ws, self.Wt[k & 1], (self.Wt[(k + 1) & 1] if k > 0 else None)
-        ws.call("pu_weights_hpair", _ptr(self.S), _ptr(self.W[0]), _ptr(self.W[1]), _ptr(self.G[0]),
-                _ptr(self.G[1]), _ptr(wp[0]) if wp is not None else None, _ptr(wp[1]) if wp is not None else None,
-                _ptr(w[0]), _ptr(w[1]), _ptr(self.D[0]), _ptr(self.D[1]), ws.sp(ws.S_HOLD), ws.stream())
+        ws.call("pu_init_state", _ptr(self.G[0]), _ptr(self.G[1]), _ptr(self.S[0]), st)
+        self.cur = 0
+        cv, ch = self._c()
+        w = self.Wt[0]  # w_0, d_0 (irls.py:173, 191)
+        ws.call("pu_weights_hpair", _ptr(self.S[0]), cv, ch, _ptr(self.G[0]), _ptr(self.G[1]), None, None,
+                _ptr(w[0]), _ptr(w[1]), _ptr(self.D[0]), _ptr(self.D[1]), ws.sp(ws.S_HOLD), st)
 
     def step(self, k, m_cg, params: IrlsParams, lip):
-        """PCG + candidate + safeguard + centring (irls.py:191-215), all enqueued."""
-        ws, st, w = self.ws, self.ws.stream(), self.Wt[k & 1]
-        pcg_device(ws, self.B, self.S, self.X, self.D[0], self.D[1], m_cg, params.cg_rel_tol)
-        ws.call("pu_candidate_step", _ptr(self.S), _ptr(w[0]), _ptr(w[1]), _ptr(self.G[0]), _ptr(self.G[1]),
-                _ptr(self.W[0]), _ptr(self.W[1]), float(lip), _ptr(self.C), st)
-        ws.call("pu_hpair_states", _ptr(self.X), _ptr(self.C), _ptr(w[0]), _ptr(w[1]), _ptr(self.G[0]),
-                _ptr(self.G[1]), _ptr(self.W[0]), _ptr(self.W[1]), ws.sp(ws.S_HPROP), st)
-        ws.call("pu_accept_center", _ptr(self.X), _ptr(self.C), ws.sp(ws.S_MEAN), _ptr(self.S), _ptr(w[0]),
-                _ptr(w[1]), _ptr(self.G[0]), _ptr(self.G[1]), _ptr(self.W[0]), _ptr(self.W[1]),
-                ws.sp(ws.S_HACC), st)
+        """irls.py:191-215 for iteration k, then the weights of k + 1."""
+        ws, st = self.ws, self.ws.stream()
+        cv, ch = self._c()
+        cur, nxt = self.S[self.cur], self.S[1 - self.cur]
+        w, wn = self.Wt[k & 1], self.Wt[(k + 1) & 1]
+        norms = ws.ensure_norms(m_cg)
+        ws.call("pu_irls_step", _ptr(cur), _ptr(self.B), _ptr(self.G[0]), _ptr(self.G[1]), cv, ch, _ptr(w[0]),
+                _ptr(w[1]), _ptr(self.D[0]), _ptr(self.D[1]), float(lip), int(m_cg), float(params.cg_rel_tol),
+                _ptr(self.C), _ptr(self.R), _ptr(self.P[0]), _ptr(self.P[1]), _ptr(self.spec), _ptr(ws.ctrl),
+                _ptr(norms), ws.sp(ws.S_HPROP), st)
+        ws.call("pu_accept_weights", _ptr(cur), _ptr(self.C), ws.sp(ws.S_MEAN), _ptr(nxt), _ptr(self.G[0]),
+                _ptr(self.G[1]), cv, ch, _ptr(w[0]), _ptr(w[1]), _ptr(wn[0]), _ptr(wn[1]), _ptr(self.D[0]),
+                _ptr(self.D[1]), ws.sp(ws.S_HACC), st)
+        self.cur = 1 - self.cur
+
+    @property
+    def state(self):
+        return self.S[self.cur]
 
     def result_arrays(self):
-        return self.ws.from_system(self.S)
+        return self.ws.from_system(self.state)
+
+    def weight_planes(self):
+        """(cv, ch) device planes; a filled unit plane pair for uniform weights."""
+        if self.W is not None:
+            return self.W
+        ones = self.ws.buf("ones", 2)
+        self.ws.call("pu_fill", _ptr(ones), 2, 1.0, self.ws.stream())
+        return ones
 
 
 def _record(k, m_cg, delta_rel, scal, ctrl, ws):
@@ -97,13 +126,13 @@ def unwrap_device(x_dev, c: WeightField | None, model: ModelParams, params: Irls
     m_history = [params.max_iter_cg_start]
     pending = None  # (k, m_cg, delta_rel) of the enqueued iteration awaiting its scalars
     for k in range(params.max_outer_iters):
-        run.weights(k)
         delta_rel = None
         if k >= 1:
             scal, ctrl = ws.read_block()                     # the one sync of this iteration
             trace.append(_record(*pending, scal, ctrl, ws))
             pending = None
-            h_old, h_new = float(scal[ws.S_HOLD]), float(scal[ws.S_HNEW])
+            # H(state_k, w_{k-1}) is the accepted value of k-1; H(state_k, w_k) its refresh
+            h_old, h_new = float(scal[ws.S_HACC]), float(scal[ws.S_HNEXT])
             delta_rel = 0.0 if h_old == 0 else relative_improvement(h_old, h_new)
             m_prev = m_history[k - 1]
             m_prev2 = m_history[k - 2] if k >= 2 else m_prev
@@ -162,5 +191,5 @@ def unwrap(x, c: WeightField | None = None, model: ModelParams | None = None, pa
     if gradient_lo not in (0.0, 0, -np.pi):
         raise ValueError(f"lo must be 0 or -pi, got {gradient_lo!r}")
     run, trace = unwrap_device(x_dev, c, model, params, gradient_lo, dtype)
-    u, vv, vh = run.ws.download_system(run.S)
+    u, vv, vh = run.ws.download_system(run.state)
     return UnwrapResult(u=u, vv=vv, vh=vh, trace=trace)
