@@ -37,6 +37,8 @@ WORKLOAD = {
     "c1": "512x512 gaussian-bumps(40,32,seed 1) + noise 0.5 (seed 1001)",
     "c2": "2048x2048 gaussian-bumps(100,128,seed 2) + noise 0.5 (seed 1002)",
     "c3": "4096x4096 InSAR-like: bumps(150,256,seed 3) + tapered fault 0->4pi (scale 512) + noise 0.5 (seed 1003)",
+    "c5": "batch of 64 independent 1024x1024 interferograms, bumps(60,64,seed 100+b) + noise 0.5 (seed 2000+b), "
+          "sharded round-robin over the ranks",
 }
 
 
@@ -217,6 +219,10 @@ def cpu_info():
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
+    if args.config not in REF_COUNTS:
+        print(json.dumps({"impl": "reference", "unavailable": f"no reference iteration counts recorded for "
+                                                              f"{args.config}; run --config c1|c2|c3"}), flush=True)
+        return 0
     from paper_2401_09961_b200.synth import config_scene
     _, x = config_scene(args.config)
     n, m = x.shape
@@ -253,7 +259,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=("c1", "c2", "c3"), default="c3")
+    ap.add_argument("--config", choices=("c1", "c2", "c3", "c5"), default="c3")
     ap.add_argument("--dtype", choices=("fp32", "fp64"), default="fp32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0,
@@ -273,6 +279,7 @@ def main():
     from paper_2401_09961_b200 import _native
     from paper_2401_09961_b200.device import Workspace
     from paper_2401_09961_b200.irls import unwrap_device
+    from paper_2401_09961_b200.batch import max_over_ranks, shard_indices
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -280,14 +287,22 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     lib = _native.ensure()
 
-    _, x = pu.config_scene(args.config)
+    # this rank's images: one C1-C3 image per rank, or its shard of the 64 C5 images
+    if args.config == "c5":
+        mine = shard_indices(64, rank, world)
+        xs = [pu.config_scene("c5", b)[1] for b in mine]
+    else:
+        xs = [pu.config_scene(args.config)[1]]
+    n_img = len(xs)
+    x = xs[0]
     n, m = x.shape
     model, params = pu.ModelParams(), pu.IrlsParams()
     ws = Workspace.get(n, m, args.dtype, model.tau, model.delta, dev)
-    x_dev = torch.from_numpy(x).to(dev)
+    x_devs = [torch.from_numpy(xi).to(dev) for xi in xs]
 
     def one_unwrap():
-        run, trace = unwrap_device(x_dev, None, model, params, -np.pi, args.dtype, ws)
+        for x_dev in x_devs:
+            run, trace = unwrap_device(x_dev, None, model, params, -np.pi, args.dtype, ws)
         return run, trace
 
     if args.profile_steps:
@@ -324,12 +339,8 @@ def main():
     launches = lib.pu_launch_count() - launches0
     ws.timing(False)
     kinds, its, ms = ws.read_timing()
-    step_ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
-        t = torch.tensor([step_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms = float(t.item())
-    value = world * n * m / (step_ms / 1e3) / 1e6
+    step_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, device=dev)
+    value = world * n_img * n * m / (step_ms / 1e3) / 1e6
 
     # per-kernel statistics (skip launches that returned early after PCG exit)
     e = 4 if args.dtype == "fp32" else 8
@@ -344,14 +355,15 @@ def main():
                           "avg_ms": float(ran.mean()) if ran.size else 0.0}
     timed_total = sum(v["total_ms"] for v in per_kind.values())
     dom = max((k for k in per_kind if k in alg), key=lambda k: per_kind[k]["total_ms"])
-    achieved = alg[dom] / (per_kind[dom]["avg_ms"] / 1e3) / 1e9
-    n_pcg = sum(r.cg_iters for r in traces[-1].records)
+    achieved = alg[dom] / (per_kind[dom]["avg_ms"] / 1e3) / 1e9 if per_kind[dom]["avg_ms"] > 0 else None
+    n_pcg = sum(r.cg_iters for r in traces[-1].records)     # per image
     n_outer = len(traces[-1].records)
     iter_ms = sum(per_kind[k]["total_ms"] for k in ("K1_p_Ap_pAp", "K2a_update_norms", "K2b_row_dct",
                                                     "K3_coldct_spectral", "K4_row_idct", "reproject_update")
-                  if k in per_kind) / max(1, args.steps * n_pcg)
+                  if k in per_kind) / max(1, args.steps * n_img * n_pcg)
     roofline = {
-        "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+        "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+        "frac": achieved / hbm if achieved else None,
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "bytes_per_launch": alg[dom],
         "avg_launch_ms": per_kind[dom]["avg_ms"], "share_of_kernel_time": per_kind[dom]["total_ms"] / timed_total,
         "traffic": ncu_traffic(dom, args.dtype, n),
@@ -372,26 +384,23 @@ def main():
         pass
 
     # ---- end to end through the public API: pinned host input -> host result ----
-    x_pin = torch.from_numpy(x).pin_memory()
+    x_pins = [torch.from_numpy(xi).pin_memory() for xi in xs]
     e2e_ms = []
     for i in range(args.steps + 1):
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = pu.unwrap(x_pin, dtype=args.dtype)
+        for x_pin in x_pins:
+            res = pu.unwrap(x_pin, dtype=args.dtype)
         t1 = time.perf_counter()
         if i > 0:
             e2e_ms.append((t1 - t0) * 1e3)
-    e2e_step = statistics.mean(e2e_ms)
-    if world > 1:
-        t = torch.tensor([e2e_step], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_step = float(t.item())
-    h2d = n * m * 8
-    d2h = (res.u.size + res.vv.size + res.vh.size) * 8
+    e2e_step = max_over_ranks(statistics.mean(e2e_ms), device=dev)
+    h2d = n_img * n * m * 8
+    d2h = n_img * (res.u.size + res.vv.size + res.vh.size) * 8
 
     cpu_base = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config != "c5":
         model_name, cores = cpu_info()
         smp = cpu_reference_sample(x, n_outer, n_pcg)
         cpu_base = {"value": smp["mpix_s"], "unit": UNIT, "cores": cores, "kind": "port", "sample": smp["sample"],
@@ -403,19 +412,19 @@ def main():
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: {WORKLOAD[args.config]}", "n": n, "m": m,
-                       "per_rank": "one independent image per GPU",
+                       "per_rank": f"{n_img} independent image(s) per GPU per step",
                        "l2": "inputs larger than L2 (~1.6 GB resident working set vs 126 MB L2)",
                        "plan": ws.describe()},
             "unwrap_s": step_ms / 1e3,
             "pcg_iters_per_step": n_pcg, "outer_iters_per_step": n_outer,
-            "pcg_iters_per_s": world * n_pcg / (step_ms / 1e3),
+            "pcg_iters_per_s": world * n_img * n_pcg / (step_ms / 1e3),
             "roofline": roofline,
             "kernels": per_kind,
             "objective": {"F": f_out, "F_reference": REF_F.get(args.config),
                           "rel": (abs(f_out - REF_F[args.config]) / REF_F[args.config])
                           if f_out is not None and args.config in REF_F else None},
             "cpu_baseline": cpu_base,
-            "e2e": {"value": world * n * m / (e2e_step / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "e2e": {"value": world * n_img * n * m / (e2e_step / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step},
             "clocks": clocks.summary(),
             "gpu_launches": int(launches),

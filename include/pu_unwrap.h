@@ -152,6 +152,11 @@ int pu_irls_step(pu_handle* h, void* state, const void* b, const void* gv, const
                  int max_iters, double rel_tol, void* cand, void* r, void* p0, void* p1, void* spec, void* ctrl,
                  double* res_norms, double* out, void* stream);
 
+/* CUDA-graph replay of pu_irls_step (default on): each (budget, pointers,
+ * scalars) combination is captured once and relaunched as one graph when the
+ * stream is not the legacy default stream and the budget is <= 64. */
+int pu_set_graphs(pu_handle* h, int on);
+
 /* irls.py:206-215 fused with the next iteration's irls.py:173-177:
  * dst = (sel[1] ? xa : xb) with u -= sel[0]; w_next, d from dst;
  * out[0] = H(dst, w_k), out[1] = H(dst, w_next).  dst must not alias xa/xb. */

@@ -49,6 +49,7 @@ SIGNATURES = {
     "pu_pcg_solve": (_i, [_vp] + [_vp] * 10 + [_i, _d, _vp, _vp, _vp]),
     "pu_irls_step": (_i, [_vp] + [_vp] * 10 + [_d, _i, _d] + [_vp] * 7 + [_vp, _vp]),
     "pu_accept_weights": (_i, [_vp] + [_vp] * 15 + [_vp]),
+    "pu_set_graphs": (_i, [_vp, _i]),
     "pu_timing_enable": (_i, [_vp, _i]),
     "pu_timing_read": (_i, [_vp, _vp, _vp, _vp, _i]),
 }

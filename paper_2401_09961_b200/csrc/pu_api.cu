@@ -8,6 +8,7 @@
 #include <complex>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -240,26 +241,34 @@ static DctOps<T> ops_for(int L) {  // L = internal length of a non-Bluestein pla
 // taken from these, on the launching stream).
 struct Timer {
   bool on = false;
-  struct Rec { int kind, it; cudaEvent_t a, b; };
+  struct Rec { int kind, it; cudaEvent_t a, b; bool pooled; };
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
+  std::vector<Rec>* sink = nullptr;  // set while a CUDA graph is being captured
   cudaEvent_t get() {
     cudaEvent_t e = nullptr;
-    if (!pool.empty()) { e = pool.back(); pool.pop_back(); }
+    if (sink == nullptr && !pool.empty()) { e = pool.back(); pool.pop_back(); }
     else cudaEventCreate(&e);
     return e;
+  }
+  // during stream capture a plain cudaEventRecord only orders streams; the
+  // External flag makes it a real event-record node of the graph
+  void record(cudaEvent_t e, cudaStream_t st) {
+    if (sink) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    else cudaEventRecord(e, st);
   }
   cudaEvent_t begin(cudaStream_t st) {
     if (!on) return nullptr;
     cudaEvent_t a = get();
-    cudaEventRecord(a, st);
+    record(a, st);
     return a;
   }
   void end(cudaStream_t st, cudaEvent_t a, int kind, int it) {
     if (!on || !a) return;
     cudaEvent_t b = get();
-    cudaEventRecord(b, st);
-    recs.push_back(Rec{kind, it, a, b});
+    record(b, st);
+    // events recorded during capture become graph nodes owned by the graph cache
+    (sink ? *sink : recs).push_back(Rec{kind, it, a, b, sink == nullptr});
   }
   int read(int* kinds, int* its, float* ms, int cap) {
     int n = 0;
@@ -269,16 +278,41 @@ struct Timer {
       cudaEventElapsedTime(&t, r.a, r.b);
       if (n < cap) { kinds[n] = r.kind; its[n] = r.it; ms[n] = t; }
       ++n;
-      pool.push_back(r.a);
-      pool.push_back(r.b);
+      if (r.pooled) {
+        pool.push_back(r.a);
+        pool.push_back(r.b);
+      }
     }
     recs.clear();
     return std::min(n, cap);
   }
   ~Timer() {
-    for (auto& r : recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto& r : recs)
+      if (r.pooled) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : pool) cudaEventDestroy(e);
   }
+};
+
+// Captured CUDA graphs of whole IRLS inner steps (candidate + PCG budget +
+// H pair), keyed by budget, pointers and scalars.  A PCG budget is hundreds
+// of small launches; one graph launch removes the per-kernel host cost that
+// dominates grids of 1024^2 and below.
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<Timer::Rec> timed;  // event pairs captured inside the graph
+  long long kernels = 0;          // kernels per replay (for pu_launch_count)
+};
+
+struct GraphCache {
+  std::map<std::vector<unsigned long long>, GraphEntry> m;
+  void clear() {
+    for (auto& kv : m) {
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      for (auto& r : kv.second.timed) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    }
+    m.clear();
+  }
+  ~GraphCache() { clear(); }
 };
 
 enum TimeKind { TK_START = 0, TK_K1, TK_K2, TK_K3, TK_K4, TK_UPD, TK_WEIGHTS, TK_CAND, TK_HPAIR, TK_ACCEPT, TK_K2B };
@@ -306,6 +340,8 @@ struct Impl : HandleBase {
   int* pinned_done = nullptr;
   DctOps<T> rops{}, cops{};  // transform kernels for the row / column internal lengths
   Timer tm;
+  GraphCache graphs;
+  bool use_graphs = true;
 
   ~Impl() override {
     prow.release();
@@ -748,15 +784,64 @@ int pu_irls_step(pu_handle* h, void* state, const void* b, const void* gv, const
   if (!(lipschitz > 0)) return fail(PU_ERR_ARG, "lipschitz constant must be positive");
   if ((cv == nullptr) != (ch == nullptr)) return fail(PU_ERR_ARG, "cv and ch must both be given or both NULL");
   PU_DISPATCH(h, {
-    const CandArgs<T> ca{CP(gv), CP(gh), CP(cv), CP(ch), CP(wv), CP(wh), (T)(-1.0 / lipschitz), MP(cand)};
-    int rc = I.pcg(CP(b), CP(state), MP(state), CP(dv), CP(dh), MP(r), nullptr, MP(p0), MP(p1), MP(spec), max_iters,
-                   rel_tol, reinterpret_cast<PcgCtrl*>(ctrl), res_norms, ST(stream), &ca);
-    if (rc != PU_OK) return rc;
-    cudaEvent_t te_ = I.tm.begin(ST(stream));
-    k_hpair_states_v<T><<<I.vec_grid(), 256, 0, ST(stream)>>>(I.g, CP(state), CP(cand), CP(wv), CP(wh), CP(gv),
-                                                             CP(gh), CP(cv), CP(ch), I.rs, S_HPAIR, out);
-    PU_LAUNCH_CHECK();
-    I.tm.end(ST(stream), te_, TK_HPAIR, -1);
+    cudaStream_t st = ST(stream);
+    auto body = [&]() -> int {
+      const CandArgs<T> ca{CP(gv), CP(gh), CP(cv), CP(ch), CP(wv), CP(wh), (T)(-1.0 / lipschitz), MP(cand)};
+      int rc = I.pcg(CP(b), CP(state), MP(state), CP(dv), CP(dh), MP(r), nullptr, MP(p0), MP(p1), MP(spec),
+                     max_iters, rel_tol, reinterpret_cast<PcgCtrl*>(ctrl), res_norms, st, &ca);
+      if (rc != PU_OK) return rc;
+      cudaEvent_t te_ = I.tm.begin(st);
+      k_hpair_states_v<T><<<I.vec_grid(), 256, 0, st>>>(I.g, CP(state), CP(cand), CP(wv), CP(wh), CP(gv), CP(gh),
+                                                         CP(cv), CP(ch), I.rs, S_HPAIR, out);
+      PU_LAUNCH_CHECK();
+      I.tm.end(st, te_, TK_HPAIR, -1);
+      return PU_OK;
+    };
+    // graphs need a capturable (non-legacy) stream and a budget that the
+    // enqueue loop runs without polling (<= 64 iterations)
+    if (!I.use_graphs || st == nullptr || max_iters > 64) return body();
+    union { double d; unsigned long long u; } lp{lipschitz}, tl{rel_tol};
+    const std::vector<unsigned long long> key = {
+        (unsigned long long)max_iters, lp.u, tl.u, (unsigned long long)I.tm.on,
+        (unsigned long long)(uintptr_t)state, (unsigned long long)(uintptr_t)b, (unsigned long long)(uintptr_t)gv,
+        (unsigned long long)(uintptr_t)gh, (unsigned long long)(uintptr_t)cv, (unsigned long long)(uintptr_t)ch,
+        (unsigned long long)(uintptr_t)wv, (unsigned long long)(uintptr_t)wh, (unsigned long long)(uintptr_t)dv,
+        (unsigned long long)(uintptr_t)dh, (unsigned long long)(uintptr_t)cand, (unsigned long long)(uintptr_t)r,
+        (unsigned long long)(uintptr_t)p0, (unsigned long long)(uintptr_t)p1, (unsigned long long)(uintptr_t)spec,
+        (unsigned long long)(uintptr_t)ctrl, (unsigned long long)(uintptr_t)res_norms, (unsigned long long)(uintptr_t)out,
+        (unsigned long long)(uintptr_t)st};
+    auto found = I.graphs.m.find(key);
+    if (found == I.graphs.m.end()) {
+      if (I.graphs.m.size() >= 64) I.graphs.clear();
+      GraphEntry ent;
+      I.tm.sink = &ent.timed;
+      PU_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      const long long l0 = g_launches.load();
+      const int rc = body();
+      ent.kernels = g_launches.load() - l0;
+      g_launches.fetch_sub(ent.kernels);  // counted per replay below
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+      I.tm.sink = nullptr;
+      if (rc != PU_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
+      PU_CUDA(ce);
+      const cudaError_t ie = cudaGraphInstantiate(&ent.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      PU_CUDA(ie);
+      found = I.graphs.m.emplace(key, std::move(ent)).first;
+    }
+    PU_CUDA(cudaGraphLaunch(found->second.exec, st));
+    g_launches.fetch_add(found->second.kernels);
+    if (I.tm.on)
+      for (const auto& rec : found->second.timed) I.tm.recs.push_back(Timer::Rec{rec.kind, rec.it, rec.a, rec.b, false});
+  });
+  return PU_OK;
+}
+
+int pu_set_graphs(pu_handle* h, int on) {
+  PU_DISPATCH(h, {
+    I.use_graphs = on != 0;
+    if (!I.use_graphs) I.graphs.clear();
   });
   return PU_OK;
 }

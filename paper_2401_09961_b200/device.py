@@ -92,6 +92,14 @@ class Workspace:
     def stream(self):
         return ctypes.c_void_p(_torch().cuda.current_stream(self.device).cuda_stream)
 
+    def solve_stream(self):
+        """Dedicated non-default stream for unwraps (graph capture needs one)."""
+        s = self._bufs.get(("stream",))
+        if s is None:
+            s = _torch().cuda.Stream(device=self.device)
+            self._bufs[("stream",)] = s
+        return s
+
     def describe(self):
         buf = ctypes.create_string_buffer(1024)
         nat.check(self.lib.pu_describe(self.h, buf, 1024))

@@ -115,9 +115,24 @@ def _record(k, m_cg, delta_rel, scal, ctrl, ws):
 
 def unwrap_device(x_dev, c: WeightField | None, model: ModelParams, params: IrlsParams, gradient_lo,
                   dtype="fp64", ws: Workspace | None = None):
-    """Run the loop on a device fp64 grid; returns (DeviceUnwrap, IrlsTrace)."""
+    """Run the loop on a device fp64 grid; returns (DeviceUnwrap, IrlsTrace).
+
+    The loop runs on the workspace's own stream (CUDA graphs cannot capture
+    the legacy default stream), ordered after and before the caller's stream.
+    """
     n, m = int(x_dev.shape[0]), int(x_dev.shape[1])
     ws = ws or Workspace.get(n, m, dtype, model.tau, model.delta, x_dev.device)
+    torch = _torch()
+    caller = torch.cuda.current_stream(ws.device)
+    s = ws.solve_stream()
+    s.wait_stream(caller)
+    with torch.cuda.stream(s):
+        out = _unwrap_loop(ws, x_dev, c, model, params, gradient_lo)
+    caller.wait_stream(s)
+    return out
+
+
+def _unwrap_loop(ws, x_dev, c, model, params, gradient_lo):
     run = DeviceUnwrap(ws)
     run.load(x_dev, c, gradient_lo)
     cmax = 1.0 if c is None else c.max_weight
