@@ -55,12 +55,27 @@ def up_to_date():
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
+def _includes(path, seen=None):
+    """Transitive closure of the quoted #includes of `path` (csrc/ and include/)."""
+    import re
+    seen = set() if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    for name in re.findall(r'^\s*#include\s+"([^"]+)"', open(path).read(), re.M):
+        for d in (os.path.dirname(path), CSRC, INCLUDE):
+            cand = os.path.join(d, name)
+            if os.path.exists(cand):
+                _includes(cand, seen)
+                break
+    return seen
+
+
 def _obj_fresh(src, obj):
     if not os.path.exists(obj):
         return False
-    hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(INCLUDE, "pu_unwrap.h")]
     t = os.path.getmtime(obj)
-    return all(os.path.getmtime(p) <= t for p in [src, *hdrs])
+    return all(os.path.getmtime(p) <= t for p in _includes(src))
 
 
 def _compile(job):

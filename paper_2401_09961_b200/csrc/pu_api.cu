@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "pu_dct_launch.cuh"
+#include "pu_vec.cuh"
 
 namespace pu {
 

@@ -458,8 +458,14 @@ __device__ __forceinline__ void dct3_pre(T ak, T ank, T bk, T bnk, int k, int nk
   }
 }
 
-// division for the spectral scaling: fast (2 ulp) in fp32, rcp-based in fp64
-__device__ __forceinline__ float fast_div(float a, float b) { return __fdividef(a, b); }
+// division for the spectral scaling: a * MUFU reciprocal (~1 ulp) in fp32,
+// rcp-based in fp64; deterministic, so repeated applications agree bitwise
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fast_div(float a, float b) { return a * rcp_approx(b); }
 __device__ __forceinline__ double fast_div(double a, double b) { return a * __drcp_rn(b); }
 
 // correctly rounded reciprocal

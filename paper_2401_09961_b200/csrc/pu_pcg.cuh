@@ -15,7 +15,8 @@
 // plain policies.  Every PCG kernel returns immediately once ctrl->done is set.
 #pragma once
 
-#include "pu_vec.cuh"
+#include "pu_kernels.cuh"
+#include "pu_q4.cuh"
 
 namespace pu {
 

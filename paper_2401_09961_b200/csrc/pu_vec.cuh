@@ -14,45 +14,10 @@
 #pragma once
 
 #include "pu_kernels.cuh"
+#include "pu_q4.cuh"
+#include "pu_fft.cuh"
 
 namespace pu {
-
-template <typename T>
-struct Q4 {
-  T a[4];
-};
-
-__device__ __forceinline__ Q4<float> ld4(const float* p) {
-  const float4 v = *reinterpret_cast<const float4*>(p);
-  return Q4<float>{{v.x, v.y, v.z, v.w}};
-}
-__device__ __forceinline__ Q4<double> ld4(const double* p) {
-  const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
-  return Q4<double>{{a.x, a.y, b.x, b.y}};
-}
-__device__ __forceinline__ Q4<float> ldg4(const float* p) {
-  const float4 v = __ldg(reinterpret_cast<const float4*>(p));
-  return Q4<float>{{v.x, v.y, v.z, v.w}};
-}
-__device__ __forceinline__ Q4<double> ldg4(const double* p) {
-  const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-  return Q4<double>{{a.x, a.y, b.x, b.y}};
-}
-__device__ __forceinline__ void st4(float* p, const Q4<float>& q) {
-  *reinterpret_cast<float4*>(p) = make_float4(q.a[0], q.a[1], q.a[2], q.a[3]);
-}
-__device__ __forceinline__ void st4(double* p, const Q4<double>& q) {
-  reinterpret_cast<double2*>(p)[0] = make_double2(q.a[0], q.a[1]);
-  reinterpret_cast<double2*>(p)[1] = make_double2(q.a[2], q.a[3]);
-}
-template <typename T>
-__device__ __forceinline__ Q4<T> zero4() {
-  return Q4<T>{{(T)0, (T)0, (T)0, (T)0}};
-}
-template <typename T>
-__device__ __forceinline__ Q4<T> ones4() {
-  return Q4<T>{{(T)1, (T)1, (T)1, (T)1}};
-}
 
 // chunk loop: chunk q covers cells (i, 4c .. 4c+3), c < cpr = ceil(m / 4)
 #define PU_FOR_CHUNKS(g, i, j0)                                                            \
@@ -99,7 +64,7 @@ __device__ __forceinline__ void apply4(const Grid& g, int i, int j0, const Stenc
 // slack block of the preconditioner, z = r / (d + 1/tau) (preconditioner.py:115):
 // fast division in fp32 mode (K1 and K2a use the same expression, so rho and
 // p stay consistent), IEEE division in fp64 mode (parity with the reference)
-__device__ __forceinline__ float slack_div(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ float slack_div(float a, float b) { return a * rcp_approx(b); }
 __device__ __forceinline__ double slack_div(double a, double b) { return a / b; }
 
 // scalar neighbour load that tolerates the grid edge
