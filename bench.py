@@ -319,11 +319,9 @@ def main():
         if world > 1:
             dist.barrier()
 
-    # ---- timed region: device-resident input ----
-    ws.timing(True)
-    ws.read_timing()  # drain
+    # ---- timed region: device-resident input, CUDA graphs, no instrumentation ----
+    ws.timing(False)
     launches0 = lib.pu_launch_count()
-    kind_ms = {}
     traces = []
     with ClockSampler(local_rank) as clocks:
         barrier()
@@ -337,10 +335,26 @@ def main():
         torch.cuda.synchronize()
         barrier()
     launches = lib.pu_launch_count() - launches0
-    ws.timing(False)
-    kinds, its, ms = ws.read_timing()
     step_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, device=dev)
     value = world * n_img * n * m / (step_ms / 1e3) / 1e6
+
+    # ---- kernel timing pass: the same K steps again with a CUDA-event pair
+    # around every launch on the launching stream (graphs off: event nodes
+    # inside graphs perturb the step by ~25%); feeds `roofline` / `kernels`
+    lib.pu_set_graphs(ws.h, 0)
+    ws.timing(True)
+    ws.read_timing()  # drain
+    torch.cuda.synchronize()
+    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev2.record()
+    for _ in range(args.steps):
+        one_unwrap()
+    ev3.record()
+    torch.cuda.synchronize()
+    ws.timing(False)
+    lib.pu_set_graphs(ws.h, 1)
+    kinds, its, ms = ws.read_timing()
+    instrumented_ms = ev2.elapsed_time(ev3) / args.steps
 
     # per-kernel statistics (skip launches that returned early after PCG exit)
     e = 4 if args.dtype == "fp32" else 8
@@ -361,6 +375,17 @@ def main():
     iter_ms = sum(per_kind[k]["total_ms"] for k in ("K1_p_Ap_pAp", "K2a_update_norms", "K2b_row_dct",
                                                     "K3_coldct_spectral", "K4_row_idct", "reproject_update")
                   if k in per_kind) / max(1, args.steps * n_img * n_pcg)
+    # per-iteration time implied by the clean timed step: step time minus the
+    # (event-timed) once-per-outer-iteration kernels, over the PCG iterations
+    outer_kinds = ("pcg_start", "weights_hpair", "candidate", "hpair_states", "accept_center")
+    outer_ms = sum(per_kind[k]["total_ms"] for k in outer_kinds if k in per_kind) / args.steps
+    init_ms = 0.0  # the start-up preconditioner applications (iteration index -1)
+    for kd, itv, t in zip(kinds, its, ms):
+        if itv == -1 and Workspace.TIME_KINDS[kd] in ("K2a_update_norms", "K2b_row_dct", "K3_coldct_spectral",
+                                                      "K4_row_idct"):
+            init_ms += t
+    init_ms /= args.steps
+    pcg_ms_from_step = (step_ms - outer_ms - init_ms) / max(1, n_img * n_pcg)
     roofline = {
         "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
         "frac": achieved / hbm if achieved else None,
@@ -369,8 +394,12 @@ def main():
         "traffic": ncu_traffic(dom, args.dtype, n),
         "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)",
         "pcg_iteration": {"bytes": alg["iteration"], "ms": iter_ms,
+                          "how": "sum of the per-iteration kernels' event-timed durations",
                           "achieved_gbs": alg["iteration"] / (iter_ms / 1e3) / 1e9 if iter_ms else None,
-                          "frac": (alg["iteration"] / (iter_ms / 1e3) / 1e9) / hbm if iter_ms else None},
+                          "frac": (alg["iteration"] / (iter_ms / 1e3) / 1e9) / hbm if iter_ms else None,
+                          "ms_from_step": pcg_ms_from_step,
+                          "frac_from_step": ((alg["iteration"] / (pcg_ms_from_step / 1e3) / 1e9) / hbm
+                                             if pcg_ms_from_step else None)},
     }
 
     # objective of the result (device eval_f) against the reference's F
@@ -416,6 +445,8 @@ def main():
                        "l2": "inputs larger than L2 (~1.6 GB resident working set vs 126 MB L2)",
                        "plan": ws.describe()},
             "unwrap_s": step_ms / 1e3,
+            "kernel_timing": {"how": "CUDA events around every launch on its stream, second pass of the same "
+                                     f"{args.steps} steps with graphs off", "ms_per_step": instrumented_ms},
             "pcg_iters_per_step": n_pcg, "outer_iters_per_step": n_outer,
             "pcg_iters_per_s": world * n_img * n_pcg / (step_ms / 1e3),
             "roofline": roofline,

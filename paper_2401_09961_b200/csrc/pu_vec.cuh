@@ -128,9 +128,10 @@ __global__ void __launch_bounds__(256, 4) k_pcg_p_v(Grid g, const T* __restrict_
     apply4<T>(g, i, j0, s, d1, d2, au, av, ah);
     st4(pnew + o + P, s.v);
     st4(pnew + o + 2 * P, s.h);
+    T part = (T)0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      acc[0] += (double)s.u.a[k] * au.a[k] + (double)s.v.a[k] * av.a[k] + (double)s.h.a[k] * ah.a[k];
+    for (int k = 0; k < 4; ++k) part += s.u.a[k] * au.a[k] + s.v.a[k] * av.a[k] + s.h.a[k] * ah.a[k];
+    acc[0] += (double)part;
   }
   double tot[1];
   if (grid_reduce<1>(acc, rs, site, tot) && threadIdx.x == 0) {
@@ -200,14 +201,17 @@ __global__ void __launch_bounds__(256, 3) k_pcg_r_v(Grid g, const T* __restrict_
       for (int k = 0; k < 4; ++k) ru.a[k] = (j0 + k < g.m) ? ru.a[k] - mean : (T)0;
       st4(r + o, ru);
     }
+    T prr = (T)0, prz = (T)0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {  // z_s = r_s / (d + 1/tau) (preconditioner.py:115), recomputed by K1
       const int j = j0 + k;
       const T zv = (i < g.n - 1 && j < g.m) ? slack_div(rv.a[k], d1.a[k] + inv) : (T)0;
       const T zh = (j < g.m - 1) ? slack_div(rh.a[k], d2.a[k] + inv) : (T)0;
-      acc[0] += (double)ru.a[k] * ru.a[k] + (double)rv.a[k] * rv.a[k] + (double)rh.a[k] * rh.a[k];
-      acc[1] += (double)rv.a[k] * zv + (double)rh.a[k] * zh;
+      prr += ru.a[k] * ru.a[k] + rv.a[k] * rv.a[k] + rh.a[k] * rh.a[k];
+      prz += rv.a[k] * zv + rh.a[k] * zh;
     }
+    acc[0] += (double)prr;  // chunk partials in T, grid sums in fp64
+    acc[1] += (double)prz;
   }
   double tot[2];
   if (grid_reduce<2>(acc, rs, site, tot) && threadIdx.x == 0) {
@@ -307,14 +311,17 @@ __global__ void __launch_bounds__(256, 3) k_pcg_start_v(Grid g, const T* __restr
     apply4<T>(g, i, j0, s, d1, d2, au, av, ah);
     const Q4<T> bu = ldg4(b + o), bv = ldg4(b + o + P), bh = ldg4(b + o + 2 * P);
     Q4<T> ru, rv, rh;
+    T pb = (T)0, pr = (T)0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       ru.a[k] = add_rn(bu.a[k], -au.a[k]);
       rv.a[k] = add_rn(bv.a[k], -av.a[k]);
       rh.a[k] = add_rn(bh.a[k], -ah.a[k]);
-      acc[0] += (double)bu.a[k] * bu.a[k] + (double)bv.a[k] * bv.a[k] + (double)bh.a[k] * bh.a[k];
-      acc[1] += (double)ru.a[k] * ru.a[k] + (double)rv.a[k] * rv.a[k] + (double)rh.a[k] * rh.a[k];
+      pb += bu.a[k] * bu.a[k] + bv.a[k] * bv.a[k] + bh.a[k] * bh.a[k];
+      pr += ru.a[k] * ru.a[k] + rv.a[k] * rv.a[k] + rh.a[k] * rh.a[k];
     }
+    acc[0] += (double)pb;  // chunk partials in T, grid sums in fp64
+    acc[1] += (double)pr;
     if (copy) { st4(x + o, s.u); st4(x + o + P, s.v); st4(x + o + 2 * P, s.h); }
     st4(r + o, ru); st4(r + o + P, rv); st4(r + o + 2 * P, rh);
     if constexpr (CAND) {
@@ -342,8 +349,8 @@ __global__ void __launch_bounds__(256, 3) k_pcg_start_v(Grid g, const T* __restr
         if (j > 0) rhm = ((uo - left) - gleft) - hleft;
         const T gu = inv * ((rvm - rvv) + (rhm - rhh));
         const T cv2 = ca.cv ? c1.a[k] * c1.a[k] : (T)1, ch2 = ca.cv ? c2.a[k] * c2.a[k] : (T)1;
-        const T gvv = cv2 / w1.a[k] * s.v.a[k] - inv * rvv;
-        const T gvh = ch2 / w2.a[k] * s.h.a[k] - inv * rhh;
+        const T gvv = slack_div(cv2, w1.a[k]) * s.v.a[k] - inv * rvv;
+        const T gvh = slack_div(ch2, w2.a[k]) * s.h.a[k] - inv * rhh;
         ou.a[k] = ok ? add_rn(uo, mul_rn(ca.neg_inv_lip, gu)) : (T)0;
         ov.a[k] = (ok && hasb) ? add_rn(s.v.a[k], mul_rn(ca.neg_inv_lip, gvv)) : (T)0;
         oh.a[k] = hash ? add_rn(s.h.a[k], mul_rn(ca.neg_inv_lip, gvh)) : (T)0;
@@ -380,31 +387,37 @@ namespace pu {
 // in the storage precision T and accumulated in fp64.
 // ---------------------------------------------------------------------------
 
-// forward-difference penalty residuals of a 4-cell chunk:
-// rv = (u[i+1] - u[i]) - gv - vv, rh = (u[j+1] - u[j]) - gh - vh
+// forward-difference penalty residuals of a 4-cell chunk, squared and summed
+// in the storage precision T (fp32 partials of 4 terms in fp32 mode; the
+// grid-wide sums are fp64):  rv = (u[i+1] - u[i]) - gv - vv,
+// rh = (u[j+1] - u[j]) - gh - vh
 template <typename T>
 __device__ __forceinline__ void pen4(const Grid& g, int i, int j0, const Q4<T>& u, const Q4<T>& ub, T ur,
                                      const Q4<T>& vv, const Q4<T>& vh, const Q4<T>& gv, const Q4<T>& gh, double& sv,
                                      double& sh) {
+  T pv = (T)0, ph = (T)0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int j = j0 + k;
     if (i < g.n - 1 && j < g.m) {
-      const double rv = ((double)ub.a[k] - (double)u.a[k]) - (double)gv.a[k] - (double)vv.a[k];
-      sv += rv * rv;
+      const T rv = ((ub.a[k] - u.a[k]) - gv.a[k]) - vv.a[k];
+      pv += rv * rv;
     }
     if (j < g.m - 1) {
       const T right = (k == 3) ? ur : u.a[k + 1];
-      const double rh = ((double)right - (double)u.a[k]) - (double)gh.a[k] - (double)vh.a[k];
-      sh += rh * rh;
+      const T rh = ((right - u.a[k]) - gh.a[k]) - vh.a[k];
+      ph += rh * rh;
     }
   }
+  sv += (double)pv;
+  sh += (double)ph;
 }
 
+// slack term of H_delta for one arc: ((c v)^2 + delta^2) / w + w
 template <typename T>
-__device__ __forceinline__ double slack4(T c, T v, T w, T d2) {
+__device__ __forceinline__ T slack4(T c, T v, T w, T d2) {
   const T cv = c * v;
-  return (double)((cv * cv + d2) / w + w);
+  return slack_div(cv * cv + d2, w) + w;
 }
 
 // w = sqrt((c v)^2 + delta^2), d = c^2 / w; H(x, w_prev), H(x, w)
@@ -430,6 +443,7 @@ __global__ void __launch_bounds__(256, 3) k_weights_hpair_v(Grid g, const T* __r
     Q4<T> p1 = zero4<T>(), p2 = zero4<T>();
     if (hasprev) { p1 = ldg4(wpv + o); p2 = ldg4(wph + o); }
     Q4<T> w1, w2, e1, e2;
+    T part[4] = {(T)0, (T)0, (T)0, (T)0};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int j = j0 + k;
@@ -441,14 +455,16 @@ __global__ void __launch_bounds__(256, 3) k_weights_hpair_v(Grid g, const T* __r
       e1.a[k] = okv ? c1.a[k] * c1.a[k] / wa : (T)0;
       e2.a[k] = okh ? c2.a[k] * c2.a[k] / wb : (T)0;
       if (okv) {
-        acc[2] += slack4(c1.a[k], vv.a[k], wa, d2);
-        if (hasprev) acc[0] += slack4(c1.a[k], vv.a[k], p1.a[k], d2);
+        part[2] += slack4(c1.a[k], vv.a[k], wa, d2);
+        if (hasprev) part[0] += slack4(c1.a[k], vv.a[k], p1.a[k], d2);
       }
       if (okh) {
-        acc[3] += slack4(c2.a[k], vh.a[k], wb, d2);
-        if (hasprev) acc[1] += slack4(c2.a[k], vh.a[k], p2.a[k], d2);
+        part[3] += slack4(c2.a[k], vh.a[k], wb, d2);
+        if (hasprev) part[1] += slack4(c2.a[k], vh.a[k], p2.a[k], d2);
       }
     }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] += (double)part[q];
     st4(wv + o, w1); st4(wh + o, w2); st4(dv + o, e1); st4(dh + o, e2);
     pen4<T>(g, i, j0, u, ub, ur, vv, vh, g1, g2, acc[4], acc[5]);
   }
@@ -482,13 +498,17 @@ __global__ void __launch_bounds__(256, 3) k_hpair_states_v(Grid g, const T* __re
       const Q4<T> u = ldg4(x + o), vv = ldg4(x + o + P), vh = ldg4(x + o + 2 * P);
       const Q4<T> ub = i < g.n - 1 ? ldg4(x + o + ld) : zero4<T>();
       const T ur = ldg_or0(x + o + 4, j0 + 4 < g.m);
+      T pv = (T)0, ph = (T)0, pu = (T)0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int j = j0 + k;
-        if (i < g.n - 1 && j < g.m) acc[5 * s + 0] += slack4(c1.a[k], vv.a[k], w1.a[k], d2);
-        if (j < g.m - 1) acc[5 * s + 1] += slack4(c2.a[k], vh.a[k], w2.a[k], d2);
-        if (j < g.m) acc[5 * s + 4] += (double)u.a[k];
+        if (i < g.n - 1 && j < g.m) pv += slack4(c1.a[k], vv.a[k], w1.a[k], d2);
+        if (j < g.m - 1) ph += slack4(c2.a[k], vh.a[k], w2.a[k], d2);
+        if (j < g.m) pu += u.a[k];
       }
+      acc[5 * s + 0] += (double)pv;
+      acc[5 * s + 1] += (double)ph;
+      acc[5 * s + 4] += (double)pu;
       pen4<T>(g, i, j0, u, ub, ur, vv, vh, g1, g2, acc[5 * s + 2], acc[5 * s + 3]);
     }
   }
@@ -572,14 +592,17 @@ __global__ void __launch_bounds__(256, 3) k_accept_v(Grid g, const T* __restrict
     T ur = ldg_or0(x + o + 4, j0 + 4 < g.m);
     const Q4<T> c1 = ldg4(cv + o), c2 = ldg4(ch + o), g1 = ldg4(gv + o), g2 = ldg4(gh + o);
     const Q4<T> w1 = ldg4(wv + o), w2 = ldg4(wh + o);
+    T pv = (T)0, ph = (T)0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int j = j0 + k;
       u.a[k] = (j < g.m) ? u.a[k] - mean : (T)0;
       ub.a[k] = ub.a[k] - mean;
-      if (i < g.n - 1 && j < g.m) acc[0] += slack4(c1.a[k], vv.a[k], w1.a[k], d2);
-      if (j < g.m - 1) acc[1] += slack4(c2.a[k], vh.a[k], w2.a[k], d2);
+      if (i < g.n - 1 && j < g.m) pv += slack4(c1.a[k], vv.a[k], w1.a[k], d2);
+      if (j < g.m - 1) ph += slack4(c2.a[k], vh.a[k], w2.a[k], d2);
     }
+    acc[0] += (double)pv;
+    acc[1] += (double)ph;
     ur = ur - mean;
     pen4<T>(g, i, j0, u, ub, ur, vv, vh, g1, g2, acc[2], acc[3]);
     st4(dst + o, u); st4(dst + o + P, vv); st4(dst + o + 2 * P, vh);
@@ -619,6 +642,7 @@ __global__ void __launch_bounds__(256, 3) k_accept_weights_v(Grid g, const T* __
     if (cv) { c1 = ldg4(cv + o); c2 = ldg4(ch + o); }
     const Q4<T> p1 = ldg4(wkv + o), p2 = ldg4(wkh + o);
     Q4<T> w1, w2, e1, e2;
+    T part[4] = {(T)0, (T)0, (T)0, (T)0};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int j = j0 + k;
@@ -632,14 +656,16 @@ __global__ void __launch_bounds__(256, 3) k_accept_weights_v(Grid g, const T* __
       e1.a[k] = okv ? c1.a[k] * c1.a[k] / wa : (T)0;
       e2.a[k] = okh ? c2.a[k] * c2.a[k] / wb : (T)0;
       if (okv) {
-        acc[0] += slack4(c1.a[k], vv.a[k], p1.a[k], d2);
-        acc[2] += slack4(c1.a[k], vv.a[k], wa, d2);
+        part[0] += slack4(c1.a[k], vv.a[k], p1.a[k], d2);
+        part[2] += slack4(c1.a[k], vv.a[k], wa, d2);
       }
       if (okh) {
-        acc[1] += slack4(c2.a[k], vh.a[k], p2.a[k], d2);
-        acc[3] += slack4(c2.a[k], vh.a[k], wb, d2);
+        part[1] += slack4(c2.a[k], vh.a[k], p2.a[k], d2);
+        part[3] += slack4(c2.a[k], vh.a[k], wb, d2);
       }
     }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] += (double)part[q];
     ur = ur - mean;
     pen4<T>(g, i, j0, u, ub, ur, vv, vh, g1, g2, acc[4], acc[5]);
     st4(dst + o, u); st4(dst + o + P, vv); st4(dst + o + 2 * P, vh);

@@ -177,7 +177,15 @@ class Workspace:
             pin.copy_(dev, non_blocking=True)
             outs.append(pin)
         torch.cuda.current_stream(self.device).synchronize()
-        return tuple(torch.empty(p.shape, dtype=torch.float64).copy_(p).numpy() for p in outs)
+        res = []
+        for p in outs:
+            # numpy's allocator madvises huge pages for large arrays (few page
+            # faults); torch's multi-threaded copy widens fp32 -> fp64 into it
+            a = np.empty(tuple(p.shape), dtype=np.float64)
+            if a.size:
+                torch.from_numpy(a).copy_(p)
+            res.append(a)
+        return tuple(res)
 
     def to_system(self, u, vv, vh, dst=None):
         dst = dst if dst is not None else self.planes(3)
