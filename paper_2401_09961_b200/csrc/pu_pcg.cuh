@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   const double tau = g.tau;
   for (int e = threadIdx.x; e < nseq * half; e += blockDim.x) {
     const int s = e / half, k = e - s * half;
-    const int nk = (n - k) % n;
+    const int nk = k == 0 ? 0 : n - k;
     cplx<T>* sb = buf + s * pl.ldseq;
     const PairOut<T> q = dct2_post<T>(sb[spad(k)], sb[spad(nk)], k, nk, pl);
     const int ja = j0 + 2 * s, jb = ja + 1;

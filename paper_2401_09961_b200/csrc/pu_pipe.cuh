@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
       }
     } else {
       for (int k = threadIdx.x; k < half; k += blockDim.x) {
-        const int nk = (n - k) % n;
+        const int nk = k == 0 ? 0 : n - k;
         cplx<T> ck, cnk;
         dct3_pre<T>(sa[k], sa[nk], hasb ? sb[k] : (T)0, hasb ? sb[nk] : (T)0, k, nk, pl, ck, cnk);
         buf[spad(k)] = ck;
@@ -119,11 +119,19 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
       }
     }
     __syncthreads();
+    const bool axpy = INV && pold != nullptr && !first;
+    if (axpy && threadIdx.x == 0) {
+      // staging is free now: fetch the old search direction rows behind the FFT
+      fence_proxy_async();
+      mbar_expect_tx(mbar, hasb ? 2 * RB : RB);
+      bulk_g2s(sa, pold + (long long)ia * g.ld, RB, mbar);
+      if (hasb) bulk_g2s(sb, pold + (long long)(ia + 1) * g.ld, RB, mbar);
+    }
     fft_n<T, EMAX, LS>(buf, 1, pl);
     const long long oa = (long long)ia * g.ld, ob = oa + g.ld;
     if constexpr (!INV) {
       for (int k = threadIdx.x; k < half; k += blockDim.x) {
-        const int nk = (n - k) % n;
+        const int nk = k == 0 ? 0 : n - k;
         const PairOut<T> q = dct2_post<T>(buf[spad(k)], buf[spad(nk)], k, nk, pl);
         out[oa + k] = q.a_k;
         if (hasb) out[ob + k] = q.b_k;
@@ -134,8 +142,8 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
       }
     } else {
       const int cpr = (n + 3) >> 2;
-      const bool axpy = pold != nullptr && !first;
       const T beta = axpy ? (T)ctrl->beta : (T)0;
+      if (axpy) mbar_wait(mbar, 1);
       for (int e = threadIdx.x; e < 2 * cpr; e += blockDim.x) {
         const int rr = e >= cpr, j0 = (e - rr * cpr) * 4;
         if (rr && !hasb) continue;
@@ -152,7 +160,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
         }
         const long long oo = (rr ? ob : oa) + j0;
         if (axpy) {
-          const Q4<T> pp = ldg4(pold + oo);
+          const Q4<T> pp = ld4((rr ? sb : sa) + j0);
 #pragma unroll
           for (int k = 0; k < 4; ++k) o.a[k] = (j0 + k < n) ? add_rn(mul_rn(beta, pp.a[k]), o.a[k]) : (T)0;
         }
