@@ -37,6 +37,7 @@ WORKLOAD = {
     "c1": "512x512 gaussian-bumps(40,32,seed 1) + noise 0.5 (seed 1001)",
     "c2": "2048x2048 gaussian-bumps(100,128,seed 2) + noise 0.5 (seed 1002)",
     "c3": "4096x4096 InSAR-like: bumps(150,256,seed 3) + tapered fault 0->4pi (scale 512) + noise 0.5 (seed 1003)",
+    "c4": "16384x16384 InSAR-like: bumps(600,1024,seed 4) + tapered fault 0->4pi (scale 2048) + noise 0.5 (seed 1004)",
     "c5": "batch of 64 independent 1024x1024 interferograms, bumps(60,64,seed 100+b) + noise 0.5 (seed 2000+b), "
           "sharded round-robin over the ranks",
 }
@@ -259,7 +260,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=("c1", "c2", "c3", "c5"), default="c3")
+    ap.add_argument("--config", choices=("c1", "c2", "c3", "c4", "c5"), default="c3")
     ap.add_argument("--dtype", choices=("fp32", "fp64"), default="fp32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0,

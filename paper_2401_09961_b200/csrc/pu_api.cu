@@ -360,8 +360,9 @@ struct Impl : HandleBase {
     int rc;
     if ((rc = prow.build(m)) || (rc = pcol.build(n))) return rc;
     // row kernels (k_rows_pipe): one row pair per CTA, whole sequence in one group
+    if (rows_pipe_smem(prow.dev.n, sizeof(T), prow.dev.ldseq) > kSmemLimit) prow.dev.stage1 = 1;
     if (prow.threads_for(1) > prow.max_threads() ||
-        rows_pipe_smem(prow.dev.n, sizeof(T), prow.dev.ldseq) > kSmemLimit)
+        rows_pipe_smem(prow.dev.n, sizeof(T), prow.dev.ldseq, prow.dev.stage1 ? 1 : 2) > kSmemLimit)
       return fail(PU_ERR_UNSUPPORTED, "row length " + std::to_string(m) + " exceeds the shared-memory FFT limit");
     // column kernels (k_cols_spec): panel of W = 2 cc columns
     // 2 sequences (W = 4 columns) per CTA, all in one thread group (<= 512
@@ -370,11 +371,12 @@ struct Impl : HandleBase {
     // not HBM, efficiency
     // static plans use PU_PANEL_COLS (2 packed sequences) in one thread group;
     // runtime plans (odd sizes, Bluestein) fall back to 1 sequence if needed
+    const int scc = static_panel_cols(pcol.dev.L, EM) / 2;  // sequences per CTA of a static plan
     const bool col_static = !pcol.dev.bluestein && (pcol.dev.L & (pcol.dev.L - 1)) == 0 && pcol.dev.L >= 512 &&
-                            pcol.dev.L <= (sizeof(T) == 4 ? 16384 : 8192) &&
-                            (long long)(PU_PANEL_COLS / 2) * pcol.dev.L <= 1024LL * pcol.seq_capacity &&
-                            pcol.smem_for(PU_PANEL_COLS / 2) <= kSmemLimit;
-    int cc = PU_PANEL_COLS / 2;
+                            pcol.dev.L <= (sizeof(T) == 4 ? 16384 : 8192) && pcol.seq_capacity == EM &&
+                            (long long)scc * pcol.dev.L <= 1024LL * pcol.seq_capacity &&
+                            pcol.smem_for(scc) <= kSmemLimit;
+    int cc = col_static ? scc : PU_PANEL_COLS / 2;
     if (!col_static && pcol.smem_for(cc) > kSmemLimit) cc = 1;
     if (pcol.threads_for(cc) > pcol.max_threads() || pcol.smem_for(cc) > kSmemLimit)
       return fail(PU_ERR_UNSUPPORTED, "column length " + std::to_string(n) + " exceeds the shared-memory FFT limit");
@@ -404,7 +406,7 @@ struct Impl : HandleBase {
     PU_CUDA(cops.set_attrs(kSmemLimit, kSmemLimit));
     // persistent pipelined row kernels: one row pair per iteration
     pipe_threads = prow.threads_for(1);
-    pipe_smem = rows_pipe_smem(prow.dev.n, sizeof(T), prow.dev.ldseq);
+    pipe_smem = rows_pipe_smem(prow.dev.n, sizeof(T), prow.dev.ldseq, prow.dev.stage1 ? 1 : 2);
     if (pipe_smem > kSmemLimit)
       return fail(PU_ERR_UNSUPPORTED, "row length " + std::to_string(g.m) + " exceeds the row pipeline staging");
     int dev = 0, sms = 148;

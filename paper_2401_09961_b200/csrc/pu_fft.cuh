@@ -18,6 +18,11 @@ namespace pu {
 
 #define PU_FFT_MAX_STAGES 20
 #define PU_PANEL_COLS 4  // columns per CTA of the column-transform kernel (2 packed sequences)
+// columns per CTA of a static column plan: 2 packed sequences while they fit
+// one 1024-thread group, else 1 (L / EMAX = 1024 threads, e.g. 16384 fp32)
+__host__ __device__ constexpr int static_panel_cols(int L, int emax) {
+  return 2 * L <= 1024 * emax ? PU_PANEL_COLS : PU_PANEL_COLS / 2;
+}
 #define PU_FFT_MAX_THREADS 1024  // absolute per-CTA thread cap of the transform kernels
 
 // Per-instantiation launch bounds.  Transform kernels run every sequence of
@@ -44,6 +49,7 @@ struct FftPlan {
   const cplx<T>* dct2w;   // [n]  s_k (cos, sin)(pi k / 2n)   DCT-II post, scale folded
   const cplx<T>* dct3w;   // [n]  (cos, sin)(pi k / 2n) / (s_k n)  DCT-III pre, 1/n folded
   const T* lam;           // [n]  2 - 2 cos(pi k / n) = 4 sin^2(pi k / 2n), lam[0] = 0
+  int stage1;             // row pipeline stages one row at a time (long rows, pu_pipe.cuh)
 };
 
 // Bank-conflict padding: one complex slot every 16.

@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   if (MODE != MODE_API && ctrl->done) return;
   const int n = LS > 0 ? LS : g.n;  // static plans are only used when n == L
   // static plans: compile-time panel width; runtime plans: 4 or 2 (smem)
-  const int W = LS > 0 ? PU_PANEL_COLS : cols_per_cta;
+  const int W = LS > 0 ? static_panel_cols(LS, EMAX) : cols_per_cta;
   const int j0 = blockIdx.x * W;
   const int ncols = min(W, g.m - j0);
   const int nseq = (ncols + 1) >> 1;

@@ -56,11 +56,16 @@ __device__ __forceinline__ P* launder_ptr(P* p) {
 __host__ __device__ constexpr unsigned stage_row_bytes(int n, int tsize) {
   return ((unsigned)n * (unsigned)tsize + 15u) & ~15u;
 }
-// dynamic shared memory of k_rows_pipe
-__host__ __device__ constexpr size_t rows_pipe_smem(int n, int tsize, int ldseq) {
-  return 128 + 2 * (size_t)stage_row_bytes(n, tsize) + (size_t)ldseq * 2 * tsize;
+// dynamic shared memory of k_rows_pipe (`rows_staged` = 2, or 1 for pl.stage1)
+__host__ __device__ constexpr size_t rows_pipe_smem(int n, int tsize, int ldseq, int rows_staged = 2) {
+  return 128 + (size_t)rows_staged * stage_row_bytes(n, tsize) + (size_t)ldseq * 2 * tsize;
 }
 
+// pl.stage1 (rows too long for two staged rows next to the FFT buffer, e.g.
+// 16384 fp32): one staging row; row b is fetched after row a has been packed
+// (its half of the packing is linear, so the sum is bitwise the same), and
+// K4 reads the old direction straight from global memory.
+//
 // INV with `pold` != nullptr (PCG K4): out = beta * pold + DCT-III(in), i.e.
 // the u block of the next search direction (pcg.py:107-108); `first` gives
 // out = DCT-III(in) (p = z at iteration 0).
@@ -75,8 +80,9 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   const unsigned RB = stage_row_bytes(n, sizeof(T));
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw);
   T* sa = reinterpret_cast<T*>(smraw + 128);
-  T* sb = reinterpret_cast<T*>(smraw + 128 + RB);
-  cplx<T>* buf0 = reinterpret_cast<cplx<T>*>(smraw + 128 + 2 * RB);
+  const bool one = pl.stage1 != 0;
+  T* sb = one ? sa : reinterpret_cast<T*>(smraw + 128 + RB);
+  cplx<T>* buf0 = reinterpret_cast<cplx<T>*>(smraw + 128 + (one ? 1 : 2) * RB);
   if (threadIdx.x == 0) {
     mbar_init(mbar, 1);
     fence_mbar_init();
@@ -85,9 +91,24 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   auto issue = [&](int seq) {  // one thread
     const int ia = 2 * seq;
     const bool hb = ia + 1 < g.n;
+    if (one) {
+      mbar_expect_tx(mbar, RB);
+      bulk_g2s(sa, in + (long long)ia * g.ld, RB, mbar);
+      return;
+    }
     mbar_expect_tx(mbar, hb ? 2 * RB : RB);
     bulk_g2s(sa, in + (long long)ia * g.ld, RB, mbar);
     if (hb) bulk_g2s(sb, in + (long long)(ia + 1) * g.ld, RB, mbar);
+  };
+  // stage1: after the row-a pass, fetch row b into the same staging row
+  auto issue_b = [&](int ia) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(mbar, RB);
+      bulk_g2s(sa, in + (long long)(ia + 1) * g.ld, RB, mbar);
+    }
+    mbar_wait(mbar, 1);
   };
   const int s = blockIdx.x;
   if (threadIdx.x == 0 && s < S) issue(s);
@@ -97,7 +118,39 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
     mbar_wait(mbar, 0);
     const int ia = 2 * s;
     const bool hasb = ia + 1 < g.n;
-    if constexpr (!INV) {
+    if (one) {
+      if constexpr (!INV) {
+        for (int j0 = 4 * threadIdx.x; j0 < n; j0 += 4 * blockDim.x) {
+          const int je = min(j0 + 4, n);
+          for (int j = j0; j < je; ++j) buf[spad(mperm(j, n))] = mk<T>(sa[j], (T)0);
+        }
+        if (hasb) {
+          issue_b(ia);
+          for (int j0 = 4 * threadIdx.x; j0 < n; j0 += 4 * blockDim.x) {
+            const int je = min(j0 + 4, n);
+            for (int j = j0; j < je; ++j) buf[spad(mperm(j, n))].y = sa[j];
+          }
+        }
+      } else {
+        for (int k = threadIdx.x; k < half; k += blockDim.x) {
+          const int nk = k == 0 ? 0 : n - k;
+          cplx<T> ck, cnk;
+          dct3_pre<T>(sa[k], sa[nk], (T)0, (T)0, k, nk, pl, ck, cnk);
+          buf[spad(k)] = ck;
+          if (nk != k) buf[spad(nk)] = cnk;
+        }
+        if (hasb) {
+          issue_b(ia);
+          for (int k = threadIdx.x; k < half; k += blockDim.x) {
+            const int nk = k == 0 ? 0 : n - k;
+            cplx<T> ck, cnk;
+            dct3_pre<T>((T)0, (T)0, sa[k], sa[nk], k, nk, pl, ck, cnk);
+            buf[spad(k)] = cadd<T>(buf[spad(k)], ck);
+            if (nk != k) buf[spad(nk)] = cadd<T>(buf[spad(nk)], cnk);
+          }
+        }
+      }
+    } else if constexpr (!INV) {
       // Makhoul permutation + (a + i b) packing
       for (int j0 = 4 * threadIdx.x; j0 < n; j0 += 4 * blockDim.x) {
         if (j0 + 4 <= n) {
@@ -120,7 +173,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
     }
     __syncthreads();
     const bool axpy = INV && pold != nullptr && !first;
-    if (axpy && threadIdx.x == 0) {
+    if (axpy && !one && threadIdx.x == 0) {
       // staging is free now: fetch the old search direction rows behind the FFT
       fence_proxy_async();
       mbar_expect_tx(mbar, hasb ? 2 * RB : RB);
@@ -143,7 +196,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
     } else {
       const int cpr = (n + 3) >> 2;
       const T beta = axpy ? (T)ctrl->beta : (T)0;
-      if (axpy) mbar_wait(mbar, 1);
+      if (axpy && !one) mbar_wait(mbar, 1);
       for (int e = threadIdx.x; e < 2 * cpr; e += blockDim.x) {
         const int rr = e >= cpr, j0 = (e - rr * cpr) * 4;
         if (rr && !hasb) continue;
@@ -160,7 +213,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
         }
         const long long oo = (rr ? ob : oa) + j0;
         if (axpy) {
-          const Q4<T> pp = ld4((rr ? sb : sa) + j0);
+          const Q4<T> pp = one ? ldg4(pold + oo) : ld4((rr ? sb : sa) + j0);
 #pragma unroll
           for (int k = 0; k < 4; ++k) o.a[k] = (j0 + k < n) ? add_rn(mul_rn(beta, pp.a[k]), o.a[k]) : (T)0;
         }

@@ -89,6 +89,25 @@ def test_sylvester_vs_dct_oracle(rng, shape):
     assert rel(got32, want) <= 5e-5
 
 
+@pytest.mark.parametrize("shape,dtypes", [((4, 16384), ("fp32",)), ((16384, 4), ("fp32",)),
+                                          ((3, 8192), ("fp64", "fp32")), ((8192, 3), ("fp64", "fp32")),
+                                          ((5, 12000), ("fp32",))])
+def test_sylvester_long_rows(rng, shape, dtypes):
+    """Rows too long for two staged rows beside the FFT buffer (single-row
+    staging) and the one-sequence static column panel (L / EMAX = 1024)."""
+    n, m = shape
+    r = rng.standard_normal((n, m))
+    want = port.DctPoisson(n, m)(r, 1e-2)
+    for dt in dtypes:
+        got = pu.sylvester_solve(r, 1e-2, dtype=dt)
+        assert rel(got, want) <= (1e-11 if dt == "fp64" else 5e-5), dt
+
+
+def test_fp64_row_limit():
+    with pytest.raises(NotImplementedError):
+        pu.sylvester_solve(np.zeros((2, 16384)), 1e-2, dtype="fp64")
+
+
 def test_apply_preconditioner(rng):
     n, m = 40, 33
     r = sysvec(rng.standard_normal((n, m)), rng.standard_normal((n - 1, m)), rng.standard_normal((n, m - 1)))
