@@ -185,6 +185,73 @@ int pu_pcg_solve(pu_handle* h, const void* b, const void* x0, void* x, const voi
 int pu_timing_enable(pu_handle* h, int on);
 int pu_timing_read(pu_handle* h, int* kinds, int* its, float* ms, int cap);
 
+/* ------------------------------------------------------------------------
+ * Row-sharded grids (BASELINE config C4: one image across the GPUs of a box;
+ * SURVEY.md §8(e)).  The reference has no distributed mode; these entry
+ * points split its pcg_solve iteration (pcg.py:81-108) at the points where a
+ * sharded run exchanges data, so the host (paper_2401_09961_b200/band.py)
+ * can put the collectives between them:
+ *   - halo: every plane of a band handle has ghost rows -1 and `rows`
+ *     (plane = (rows + 2) * pitch elements; pass pointers to row 0), which
+ *     mirror the neighbouring bands' edge rows;
+ *   - all-reduce: in band mode every reduction leaves its band totals in the
+ *     `totals` buffer (row `site`, PU_MAX_SUMS doubles) instead of
+ *     finalising; after summing them over ranks, pu_finalize runs the
+ *     finalisers of the listed sites;
+ *   - all-to-all: the row DCT-II writes the spectrum in the packed layout
+ *     chunk q = columns [q mb, (q+1) mb) x rows, row pitch mb; after the
+ *     transpose each rank runs the column transform on its N x cols block
+ *     (pitch mb); the reverse transpose returns the same packed layout to the
+ *     row DCT-III.
+ * The same calls on a whole-grid handle reproduce pu_pcg_solve.
+ * ------------------------------------------------------------------------ */
+typedef struct pu_band {
+  int32_t n_glob;      /* N of the whole grid */
+  int32_t row0, rows;  /* this rank's rows [row0, row0 + rows) */
+  int32_t nq;          /* ranks = column chunks of the transpose */
+  int32_t mb;          /* columns per chunk: multiple of 8, nq * mb >= M */
+  int32_t col0, cols;  /* this rank's column block: col0 = rank * mb, cols = min(mb, M - col0) >= 1 */
+} pu_band;
+
+enum pu_site { PU_SITE_WH = 1, PU_SITE_HPAIR = 3, PU_SITE_ACC = 4, PU_SITE_START = 6, PU_SITE_K1 = 7,
+               PU_SITE_K2 = 8, PU_SITE_K3 = 9, PU_SITE_UPD = 10, PU_NSITES = 12 };
+#define PU_MAX_SUMS_ABI 12
+
+int pu_create_band(pu_handle** out, int m, const pu_band* band, int dtype, double tau, double delta);
+/* Device fp64 [PU_NSITES * PU_MAX_SUMS_ABI] that receives band totals; NULL
+ * restores single-grid finalisation. */
+int pu_set_band_totals(pu_handle* h, double* totals);
+/* Run the finalisers of the sites in `mask` (bit = pu_site) on `totals` (the
+ * all-reduced buffer), in PCG order, skipping PCG sites once ctrl->done.
+ * mode: 1 = PCG set-up (z0, rho0), 2 = iteration `it`.  out: the scalar
+ * block of the outer-iteration sites (WH, HPAIR, ACC). */
+int pu_finalize(pu_handle* h, unsigned mask, int mode, int it, void* ctrl, double* res_norms, double* out,
+                double rel_tol, int max_iters, void* stream);
+/* pcg.py:59-75 (+ the candidate step objective.py:118-125 when cand != NULL,
+ * as in pu_irls_step).  x may alias x0. */
+int pu_pcg_begin(pu_handle* h, const void* b, const void* x0, void* x, const void* dv, const void* dh, void* r,
+                 void* ctrl, double* res_norms, int max_iters, double rel_tol, const void* gv, const void* gh,
+                 const void* cv, const void* ch, const void* wv, const void* wh, double lipschitz, void* cand,
+                 void* stream);
+/* K2a + K2b: it < 0 = set-up (rho_s of r0); else x += alpha p, r -= alpha A p
+ * (submean: after pu_pcg_update_sum, r_u -= mean instead), ||r||, rho_s;
+ * then the row DCT-II of r_u into spec_out (packed in band mode). */
+int pu_pcg_residual_rows(pu_handle* h, const void* p, const void* dv, const void* dh, void* x, void* r, void* ctrl,
+                         double* res_norms, void* spec_out, int it, int submean, void* stream);
+/* pcg.py:90-93 on every 50th iteration: update and sum(r_u). */
+int pu_pcg_update_sum(pu_handle* h, const void* p, const void* dv, const void* dh, void* x, void* r, void* ctrl,
+                      int it, void* stream);
+/* K3: column DCT-II, spectral division, rho_u, column DCT-III, in place
+ * (it < 0: set-up). */
+int pu_pcg_columns(pu_handle* h, void* spec, void* ctrl, int it, void* stream);
+/* K4: pnew_u = beta pold_u + row DCT-III(spec_in) (first: no axpy). */
+int pu_pcg_rows_inv(pu_handle* h, const void* spec_in, void* pnew, const void* pold, int first, void* ctrl, int it,
+                    void* stream);
+/* K1: slack blocks of the new direction (+ the ghost row in band mode), A p,
+ * p'Ap. */
+int pu_pcg_direction(pu_handle* h, const void* r, const void* pold, void* pnew, const void* dv, const void* dh,
+                     void* ctrl, int it, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

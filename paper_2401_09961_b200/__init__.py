@@ -7,6 +7,8 @@ operation executed by hand-written sm_100a CUDA kernels in
 fallback; calling into the solver without the library or a GPU raises.
 """
 
+from . import band
+from .band import unwrap_rows
 from .irls import unwrap, unwrap_device
 from .objective import (IrlsWeights, arc_count, candidate_step, eval_f, eval_h_delta,
                         update_weights)

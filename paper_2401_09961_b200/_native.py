@@ -52,7 +52,28 @@ SIGNATURES = {
     "pu_set_graphs": (_i, [_vp, _i]),
     "pu_timing_enable": (_i, [_vp, _i]),
     "pu_timing_read": (_i, [_vp, _vp, _vp, _vp, _i]),
+    # row-sharded grids (band.py)
+    "pu_create_band": (_i, [ctypes.POINTER(_vp), _i, _vp, _i, _d, _d]),
+    "pu_set_band_totals": (_i, [_vp, _vp]),
+    "pu_finalize": (_i, [_vp, ctypes.c_uint, _i, _i, _vp, _vp, _vp, _d, _i, _vp]),
+    "pu_pcg_begin": (_i, [_vp] + [_vp] * 8 + [_i, _d] + [_vp] * 6 + [_d, _vp, _vp]),
+    "pu_pcg_residual_rows": (_i, [_vp] + [_vp] * 8 + [_i, _i, _vp]),
+    "pu_pcg_update_sum": (_i, [_vp] + [_vp] * 6 + [_i, _vp]),
+    "pu_pcg_columns": (_i, [_vp, _vp, _vp, _i, _vp]),
+    "pu_pcg_rows_inv": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _vp]),
+    "pu_pcg_direction": (_i, [_vp] + [_vp] * 6 + [_i, _vp]),
 }
+
+
+class PuBand(ctypes.Structure):
+    """struct pu_band (include/pu_unwrap.h)."""
+    _fields_ = [("n_glob", ctypes.c_int32), ("row0", ctypes.c_int32), ("rows", ctypes.c_int32),
+                ("nq", ctypes.c_int32), ("mb", ctypes.c_int32), ("col0", ctypes.c_int32), ("cols", ctypes.c_int32)]
+
+
+# reduction sites (enum pu_site) and the totals row length
+SITE_WH, SITE_HPAIR, SITE_ACC, SITE_START, SITE_K1, SITE_K2, SITE_K3, SITE_UPD = 1, 3, 4, 6, 7, 8, 9, 10
+NSITES, MAX_SUMS = 12, 12
 
 _lib = None
 

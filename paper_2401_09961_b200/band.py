@@ -1,0 +1,567 @@
+"""One image row-sharded across GPUs (BASELINE config C4).
+
+The reference unwraps one grid in one process (irls.py:132-224); this module
+runs the same outer loop and the same PCG iteration (pcg.py:47-116) on a grid
+split into contiguous row bands, one band per rank:
+
+  halo       every plane of a band carries ghost rows -1 and `rows` that mirror
+             the neighbours' edge rows; the stencils (A x, the candidate
+             gradient, the penalty terms) read them.  Exchanged: the state
+             (u both ways, vv down) after each acceptance, the proposal and the
+             candidate u before the H pair, the u block of the search direction
+             and the vv block of the residual after every PCG iteration, gv and
+             dv when they change.  The vv block of the new direction in the
+             ghost row is recomputed locally (k_ghost_pslack).
+  all-reduce every reduction leaves the band's fp64 totals in a small buffer;
+             the ranks sum them and every rank runs the same finaliser
+             (pu_finalize), so all ranks hold identical PCG/IRLS scalars and
+             take identical control-flow decisions.  Two per PCG iteration:
+             p'Ap, then {||r||^2, rho_s, rho_u}.
+  transpose  the 2-D DCT preconditioner (preconditioner.py:86-100) runs its
+             row transforms on the row bands and its column transforms on
+             column blocks: the row DCT-II writes the spectrum packed by
+             destination, an all-to-all moves it, the column kernel works on
+             the N x cols block, and the reverse all-to-all feeds the row
+             DCT-III.  Two all-to-alls per PCG iteration.
+
+Communicators: `LoopbackComm` holds every band in this process on one device
+and implements the collectives as device copies (used to test the band
+decomposition on a single GPU); `DistComm` has one band per process and uses
+torch.distributed (NCCL over NVLink on a B200 box, gloo in the CPU tests of
+the exchange plumbing).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as nat
+from .device import _DTYPES, _ptr
+from .params import IrlsParams, IrlsTrace, ModelParams, UnwrapResult, cg_budget_update, relative_improvement
+from .phase import WeightField
+
+
+def _torch():
+    import torch
+    return torch
+
+
+# ---------------------------------------------------------------------------
+# partition
+# ---------------------------------------------------------------------------
+class BandLayout:
+    """Row bands (near-equal, contiguous) and the column blocks of the transpose."""
+
+    def __init__(self, n: int, m: int, world: int):
+        if world < 1:
+            raise ValueError(f"world size must be >= 1, got {world}")
+        if n < 2 or m < 1:
+            raise ValueError(f"grid {n}x{m} too small to shard")
+        if n < world:
+            raise ValueError(f"{n} rows cannot be split into {world} bands")
+        self.n, self.m, self.world = int(n), int(m), int(world)
+        base, extra = divmod(self.n, world)
+        self.rows = [base + (1 if r < extra else 0) for r in range(world)]
+        self.row0 = [int(v) for v in np.concatenate([[0], np.cumsum(self.rows)[:-1]])]
+        per = -(-self.m // world)
+        self.mb = max(8, -(-per // 8) * 8)
+        self.col0 = [r * self.mb for r in range(world)]
+        self.cols = [min(self.mb, self.m - c) for c in self.col0]
+        if min(self.cols) < 1:
+            raise ValueError(f"{m} columns cannot be split into {world} column blocks of {self.mb}")
+
+    def band(self, r: int) -> nat.PuBand:
+        return nat.PuBand(self.n, self.row0[r], self.rows[r], self.world, self.mb, self.col0[r], self.cols[r])
+
+
+# ---------------------------------------------------------------------------
+# per-band device state
+# ---------------------------------------------------------------------------
+class BandState:
+    """Handle + HBM buffers of one band (planes stored as (k, rows + 2, ld):
+    storage row 0 is the ghost row -1, rows 1..rows the band, rows + 1 the
+    ghost row `rows`)."""
+
+    NSCAL = 16
+    (S_HOLD, S_HNEW, S_HPROP, S_HCAND, S_MEAN, S_TAKE, S_HACC, S_HNEXT) = range(8)
+
+    def __init__(self, layout: BandLayout, rank: int, dtype: str, tau: float, delta: float, device):
+        torch = _torch()
+        self.lib = nat.ensure()
+        if dtype not in _DTYPES:
+            raise ValueError(f"dtype must be 'fp32' or 'fp64', got {dtype!r}")
+        self.layout, self.rank = layout, rank
+        self.rows, self.row0 = layout.rows[rank], layout.row0[rank]
+        self.n, self.m, self.mb, self.nq = layout.n, layout.m, layout.mb, layout.world
+        self.code = _DTYPES[dtype]
+        self.tdtype = torch.float32 if self.code == nat.PU_F32 else torch.float64
+        self.device = device
+        band = layout.band(rank)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            nat.check(self.lib.pu_create_band(ctypes.byref(h), self.m, ctypes.byref(band), self.code, float(tau),
+                                              float(delta)))
+        self.h = h
+        self.ld = int(self.lib.pu_pitch(h))
+        z = lambda k: torch.zeros((k, self.rows + 2, self.ld), dtype=self.tdtype, device=device)  # noqa: E731
+        self.S = [z(3), z(3)]
+        self.C, self.B, self.G, self.D, self.R = z(3), z(3), z(2), z(2), z(3)
+        self.Wt = [z(2), z(2)]
+        self.P = [z(3), z(3)]
+        self.W = None
+        self.spec_send = torch.zeros(self.nq * self.rows * self.mb, dtype=self.tdtype, device=device)
+        self.spec_col = torch.zeros(self.n * self.mb, dtype=self.tdtype, device=device)
+        self.totals = torch.zeros(nat.NSITES * nat.MAX_SUMS, dtype=torch.float64, device=device)
+        ctrl_bytes = int(self.lib.pu_pcg_ctrl_bytes())
+        self.block = torch.zeros(self.NSCAL * 8 + ctrl_bytes, dtype=torch.uint8, device=device)
+        self.scal = self.block[: self.NSCAL * 8].view(torch.float64)
+        self.ctrl = self.block[self.NSCAL * 8:]
+        self.norms = torch.zeros(1, dtype=torch.float64, device=device)
+        nat.check(self.lib.pu_set_band_totals(self.h, _ptr(self.totals)))
+        self._ctrl_dtype = _ctrl_dtype()
+        self.cur = 0
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) is not None and self.h.value:
+                self.lib.pu_destroy(self.h)
+        except Exception:
+            pass
+
+    # pointers -------------------------------------------------------------
+    @staticmethod
+    def p(t, plane=0):
+        """Device pointer to row 0 of plane `plane` of a band tensor."""
+        return ctypes.c_void_p(t[plane, 1].data_ptr())
+
+    def sp(self, slot):
+        return ctypes.c_void_p(self.scal.data_ptr() + 8 * slot)
+
+    def stream(self):
+        return ctypes.c_void_p(_torch().cuda.current_stream(self.device).cuda_stream)
+
+    def call(self, name, *args):
+        nat.check(getattr(self.lib, name)(self.h, *args))
+
+    def ensure_norms(self, k):
+        if self.norms.numel() < k + 1:
+            self.norms = _torch().zeros(k + 1, dtype=_torch().float64, device=self.device)
+        return self.norms
+
+    def read_block(self):
+        host = self.block.cpu().numpy()
+        scal = host[: self.NSCAL * 8].view(np.float64).copy()
+        ctrl = host[self.NSCAL * 8:].view(self._ctrl_dtype)[0]
+        return scal, ctrl
+
+    def pack_rows(self, arr, dst, plane, r0, nrows):
+        """Host/device fp64 rows [r0, r0 + nrows) of a compact array -> band rows of dst[plane]."""
+        torch = _torch()
+        src = torch.as_tensor(np.ascontiguousarray(arr[r0:r0 + nrows], dtype=np.float64)) \
+            if isinstance(arr, np.ndarray) else arr[r0:r0 + nrows]
+        src = src.to(device=self.device, dtype=torch.float64).contiguous()
+        rows, cols = (int(src.shape[0]), int(src.shape[1])) if src.numel() else (0, 0)
+        self.call("pu_pack", _ptr(src) if src.numel() else ctypes.c_void_p(0), max(cols, 1), rows, cols,
+                  self.p(dst, plane), self.stream())
+        return src
+
+
+def _ctrl_dtype():
+    return np.dtype([("rho", "<f8"), ("alpha", "<f8"), ("beta", "<f8"), ("thr", "<f8"), ("bnorm", "<f8"),
+                     ("pap", "<f8"), ("rn", "<f8"), ("mean_ru", "<f8"), ("rho_s", "<f8"), ("done", "<i4"),
+                     ("converged", "<i4"), ("breakdown", "<i4"), ("bkind", "<i4"), ("iterations", "<i4"),
+                     ("max_iters", "<i4"), ("pad", "<i4", 2)])
+
+
+# ---------------------------------------------------------------------------
+# communicators
+# ---------------------------------------------------------------------------
+def _site_slice(lo, hi):
+    return slice(lo * nat.MAX_SUMS, (hi + 1) * nat.MAX_SUMS)
+
+
+class LoopbackComm:
+    """Every band in this process; collectives are device copies in rank order."""
+
+    def __init__(self, world: int):
+        self.world = world
+
+    def allreduce(self, bands, lo, hi):
+        sl = _site_slice(lo, hi)
+        tot = bands[0].totals[sl].clone()
+        for b in bands[1:]:
+            tot += b.totals[sl]
+        for b in bands:
+            b.totals[sl].copy_(tot)
+
+    def transpose(self, bands):
+        for b in bands:
+            src = b.spec_send.view(b.nq, b.rows, b.mb)
+            for q, d in enumerate(bands):
+                d.spec_col.view(d.n, d.mb)[b.row0:b.row0 + b.rows].copy_(src[q])
+
+    def transpose_back(self, bands):
+        for b in bands:
+            dst = b.spec_send.view(b.nq, b.rows, b.mb)
+            for q, s in enumerate(bands):
+                dst[q].copy_(s.spec_col.view(s.n, s.mb)[b.row0:b.row0 + b.rows])
+
+    def halo(self, bands, items):
+        """items: (getter(band) -> (k, rows + 2, ld) tensor, plane, 'down'|'up'|'both')."""
+        for get, plane, way in items:
+            for r, b in enumerate(bands):
+                t = get(b)
+                if way in ("down", "both") and r + 1 < len(bands):
+                    get(bands[r + 1])[plane, 0].copy_(t[plane, b.rows])
+                if way in ("up", "both") and r > 0:
+                    a = bands[r - 1]
+                    get(a)[plane, a.rows + 1].copy_(t[plane, 1])
+
+
+class DistComm:
+    """One band per process over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def _peer(self, r):
+        return r if self.group is None else self.dist.get_global_rank(self.group, r)
+
+    def allreduce(self, bands, lo, hi):
+        (b,) = bands
+        self.dist.all_reduce(b.totals[_site_slice(lo, hi)], group=self.group)
+
+    def _splits(self, b):
+        lay = b.layout
+        mine = [b.rows * b.mb] * self.world
+        theirs = [lay.rows[p] * b.mb for p in range(self.world)]
+        return mine, theirs
+
+    def transpose(self, bands):
+        (b,) = bands
+        mine, theirs = self._splits(b)
+        self.dist.all_to_all_single(b.spec_col, b.spec_send, output_split_sizes=theirs, input_split_sizes=mine,
+                                    group=self.group)
+
+    def transpose_back(self, bands):
+        (b,) = bands
+        mine, theirs = self._splits(b)
+        self.dist.all_to_all_single(b.spec_send, b.spec_col, output_split_sizes=mine, input_split_sizes=theirs,
+                                    group=self.group)
+
+    def halo(self, bands, items):
+        torch = _torch()
+        (b,) = bands
+        r, world = self.rank, self.world
+        down = [(get, pl) for get, pl, way in items if way in ("down", "both")]
+        up = [(get, pl) for get, pl, way in items if way in ("up", "both")]
+        ops, recv_above, recv_below = [], None, None
+        P2P = self.dist.P2POp
+        if down and r + 1 < world:
+            send = torch.stack([get(b)[pl, b.rows] for get, pl in down])
+            ops.append(P2P(self.dist.isend, send, self._peer(r + 1), self.group))
+        if up and r > 0:
+            send_up = torch.stack([get(b)[pl, 1] for get, pl in up])
+            ops.append(P2P(self.dist.isend, send_up, self._peer(r - 1), self.group))
+        if down and r > 0:
+            recv_above = torch.empty((len(down), b.ld), dtype=b.tdtype, device=b.spec_col.device)
+            ops.append(P2P(self.dist.irecv, recv_above, self._peer(r - 1), self.group))
+        if up and r + 1 < world:
+            recv_below = torch.empty((len(up), b.ld), dtype=b.tdtype, device=b.spec_col.device)
+            ops.append(P2P(self.dist.irecv, recv_below, self._peer(r + 1), self.group))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+        if recv_above is not None:
+            for k, (get, pl) in enumerate(down):
+                get(b)[pl, 0].copy_(recv_above[k])
+        if recv_below is not None:
+            for k, (get, pl) in enumerate(up):
+                get(b)[pl, b.rows + 1].copy_(recv_below[k])
+
+
+# ---------------------------------------------------------------------------
+# the sharded unwrap
+# ---------------------------------------------------------------------------
+def _mask(*sites):
+    m = 0
+    for s in sites:
+        m |= 1 << s
+    return ctypes.c_uint(m)
+
+
+class BandUnwrap:
+    """irls.py:132-224 on row bands.  `bands`: the bands this process drives
+    (all of them with LoopbackComm, its own with DistComm)."""
+
+    def __init__(self, bands, comm):
+        self.bands, self.comm = bands, comm
+
+    # ---- helpers ------------------------------------------------------------
+    def _each(self, name, fn):
+        for b in self.bands:
+            b.call(name, *fn(b))
+
+    def _reduce(self, lo, hi, mask, mode, it, out_slot=None, rel_tol=0.0, max_iters=0):
+        self.comm.allreduce(self.bands, lo, hi)
+        for b in self.bands:
+            b.call("pu_finalize", mask, mode, it, _ptr(b.ctrl), _ptr(b.norms),
+                   b.sp(out_slot) if out_slot is not None else ctypes.c_void_p(0), float(rel_tol), int(max_iters),
+                   b.stream())
+
+    @staticmethod
+    def _c(b):
+        return (None, None) if b.W is None else (BandState.p(b.W, 0), BandState.p(b.W, 1))
+
+    def _state_halo(self, idx_fn, with_dv=False):
+        items = [(lambda b, f=idx_fn: f(b), 0, "both"), (lambda b, f=idx_fn: f(b), 1, "down")]
+        if with_dv:
+            items.append((lambda b: b.D, 0, "down"))
+        self.comm.halo(self.bands, items)
+
+    # ---- set-up ---------------------------------------------------------------
+    def load(self, x_rows, c: WeightField | None, lo):
+        """x_rows[i]: fp64 device grid rows [row0, row0 + rows (+1 if not last)) of band i."""
+        P = BandState.p
+        self._keep = []
+        for b, xr in zip(self.bands, x_rows):
+            if c is not None:
+                b.W = _torch().zeros((2, b.rows + 2, b.ld), dtype=b.tdtype, device=b.device)
+                nv = max(0, min(b.rows, b.n - 1 - b.row0))
+                self._keep += [b.pack_rows(c.cv, b.W, 0, b.row0, nv), b.pack_rows(c.ch, b.W, 1, b.row0, b.rows)]
+            self._keep.append(xr)
+            b.call("pu_wrapped_gradients", _ptr(xr), int(xr.shape[1]), P(b.G, 0), P(b.G, 1), float(lo), b.stream())
+        self.comm.halo(self.bands, [(lambda b: b.G, 0, "down")])  # gv[-1]: rhs and candidate stencils
+        for b in self.bands:
+            b.call("pu_build_rhs", P(b.G, 0), P(b.G, 1), P(b.B), b.stream())
+            b.call("pu_init_state", P(b.G, 0), P(b.G, 1), P(b.S[0]), b.stream())
+            b.cur = 0
+        self._state_halo(lambda b: b.S[0])
+        for b in self.bands:
+            cv, ch = self._c(b)
+            b.call("pu_weights_hpair", P(b.S[0]), cv, ch, P(b.G, 0), P(b.G, 1), None, None, P(b.Wt[0], 0),
+                   P(b.Wt[0], 1), P(b.D, 0), P(b.D, 1), b.sp(b.S_HOLD), b.stream())
+        self._reduce(nat.SITE_WH, nat.SITE_WH, _mask(nat.SITE_WH), 0, -1, out_slot=BandState.S_HOLD)
+        self.comm.halo(self.bands, [(lambda b: b.D, 0, "down")])
+
+    # ---- one outer iteration ------------------------------------------------------
+    def step(self, k, m_cg, params: IrlsParams, lip, poll=16):
+        P = BandState.p
+        tol = float(params.cg_rel_tol)
+        for b in self.bands:
+            b.ensure_norms(m_cg)
+        cur = lambda b: b.S[b.cur]  # noqa: E731
+        nxt = lambda b: b.S[1 - b.cur]  # noqa: E731
+        for b in self.bands:
+            cv, ch = self._c(b)
+            w = b.Wt[k & 1]
+            b.call("pu_pcg_begin", P(b.B), P(cur(b)), P(cur(b)), P(b.D, 0), P(b.D, 1), P(b.R), _ptr(b.ctrl),
+                   _ptr(b.norms), int(m_cg), tol, P(b.G, 0), P(b.G, 1), cv, ch, P(w, 0), P(w, 1), float(lip),
+                   P(b.C), b.stream())
+        self._reduce(nat.SITE_START, nat.SITE_START, _mask(nat.SITE_START), 1, -1, rel_tol=tol, max_iters=m_cg)
+        # z0 = M r0, rho0; p0 = z0 (pcg.py:77-79)
+        for b in self.bands:
+            b.call("pu_pcg_residual_rows", None, P(b.D, 0), P(b.D, 1), P(cur(b)), P(b.R), _ptr(b.ctrl),
+                   _ptr(b.norms), _ptr(b.spec_send), -1, 0, b.stream())
+        self._precond_tail(-1, mode=1)
+        for b in self.bands:
+            b.call("pu_pcg_rows_inv", _ptr(b.spec_send), P(b.P[0]), P(b.P[1]), 1, _ptr(b.ctrl), -1, b.stream())
+        self._dir_halo(0)
+        for it in range(m_cg):
+            if it > 0 and it % poll == 0 and self._done():
+                break
+            for b in self.bands:
+                pn, po = b.P[it & 1], b.P[(it + 1) & 1]
+                b.call("pu_pcg_direction", P(b.R), P(po), P(pn), P(b.D, 0), P(b.D, 1), _ptr(b.ctrl), it,
+                       b.stream())
+            self._reduce(nat.SITE_K1, nat.SITE_K1, _mask(nat.SITE_K1), 2, it)
+            submean = (it + 1) % 50 == 0
+            if submean:  # pcg.py:92-93
+                for b in self.bands:
+                    b.call("pu_pcg_update_sum", P(b.P[it & 1]), P(b.D, 0), P(b.D, 1), P(cur(b)), P(b.R),
+                           _ptr(b.ctrl), it, b.stream())
+                self._reduce(nat.SITE_UPD, nat.SITE_UPD, _mask(nat.SITE_UPD), 2, it)
+            for b in self.bands:
+                b.call("pu_pcg_residual_rows", P(b.P[it & 1]), P(b.D, 0), P(b.D, 1), P(cur(b)), P(b.R),
+                       _ptr(b.ctrl), _ptr(b.norms), _ptr(b.spec_send), it, 1 if submean else 0, b.stream())
+            self._precond_tail(it, mode=2)
+            for b in self.bands:
+                b.call("pu_pcg_rows_inv", _ptr(b.spec_send), P(b.P[(it + 1) & 1]), P(b.P[it & 1]), 0,
+                       _ptr(b.ctrl), it, b.stream())
+            self._dir_halo((it + 1) & 1)
+        # H pair (irls.py:202-205) on the proposal (= state, solved in place) and the candidate
+        self.comm.halo(self.bands, [(cur, 0, "up"), (lambda b: b.C, 0, "up")])
+        for b in self.bands:
+            cv, ch = self._c(b)
+            w = b.Wt[k & 1]
+            b.call("pu_hpair_states", P(cur(b)), P(b.C), P(w, 0), P(w, 1), P(b.G, 0), P(b.G, 1), cv, ch,
+                   b.sp(b.S_HPROP), b.stream())
+        self._reduce(nat.SITE_HPAIR, nat.SITE_HPAIR, _mask(nat.SITE_HPAIR), 0, -1, out_slot=BandState.S_HPROP)
+        for b in self.bands:
+            cv, ch = self._c(b)
+            w, wn = b.Wt[k & 1], b.Wt[(k + 1) & 1]
+            b.call("pu_accept_weights", P(cur(b)), P(b.C), b.sp(b.S_MEAN), P(nxt(b)), P(b.G, 0), P(b.G, 1), cv,
+                   ch, P(w, 0), P(w, 1), P(wn, 0), P(wn, 1), P(b.D, 0), P(b.D, 1), b.sp(b.S_HACC), b.stream())
+        self._reduce(nat.SITE_ACC, nat.SITE_ACC, _mask(nat.SITE_ACC), 0, -1, out_slot=BandState.S_HACC)
+        for b in self.bands:
+            b.cur = 1 - b.cur
+        self._state_halo(lambda b: b.S[b.cur], with_dv=True)
+
+    def _precond_tail(self, it, mode):
+        self.comm.transpose(self.bands)
+        for b in self.bands:
+            b.call("pu_pcg_columns", _ptr(b.spec_col), _ptr(b.ctrl), it, b.stream())
+        self.comm.transpose_back(self.bands)
+        self._reduce(nat.SITE_K2, nat.SITE_K3, _mask(nat.SITE_K2, nat.SITE_K3), mode, it)
+
+    def _dir_halo(self, idx):
+        self.comm.halo(self.bands, [(lambda b, i=idx: b.P[i], 0, "both"), (lambda b: b.R, 1, "down")])
+
+    def _done(self):
+        return bool(self.bands[0].read_block()[1]["done"])
+
+    # ---- results ---------------------------------------------------------------
+    def band_arrays(self, b):
+        """(u, vv, vh) fp64 device tensors of band b's own rows (vv without the global pad row)."""
+        torch = _torch()
+        s = b.S[b.cur]
+        nv = max(0, min(b.rows, b.n - 1 - b.row0))
+        u = s[0, 1:b.rows + 1, :b.m].to(torch.float64)
+        vv = s[1, 1:nv + 1, :b.m].to(torch.float64)
+        vh = s[2, 1:b.rows + 1, :b.m - 1].to(torch.float64)
+        return u, vv, vh
+
+
+def run_loop(driver: BandUnwrap, c, model: ModelParams, params: IrlsParams):
+    """The host loop of irls.py:172-222 (same as irls._unwrap_loop) over the band driver."""
+    from .irls import _record
+    cmax = 1.0 if c is None else c.max_weight
+    lip = 12.0 / model.tau + cmax ** 2 / model.delta
+    trace = IrlsTrace()
+    m_history = [params.max_iter_cg_start]
+    pending = None
+    b0 = driver.bands[0]
+    for k in range(params.max_outer_iters):
+        delta_rel = None
+        if k >= 1:
+            scal, ctrl = b0.read_block()
+            trace.append(_record(*pending, scal, ctrl, b0))
+            pending = None
+            h_old, h_new = float(scal[b0.S_HACC]), float(scal[b0.S_HNEXT])
+            delta_rel = 0.0 if h_old == 0 else relative_improvement(h_old, h_new)
+            m_prev = m_history[k - 1]
+            m_prev2 = m_history[k - 2] if k >= 2 else m_prev
+            decision = cg_budget_update(delta_rel, m_prev, m_prev2, params)
+            if decision.action == "stop":
+                break
+            m_cg = decision.m_cg
+            m_history.append(m_cg)
+        else:
+            m_cg = m_history[0]
+        driver.step(k, m_cg, params, lip)
+        pending = (k, m_cg, delta_rel)
+    if pending is not None:
+        scal, ctrl = b0.read_block()
+        trace.append(_record(*pending, scal, ctrl, b0))
+    return trace
+
+
+def _check_inputs(x, c, n, m, gradient_lo):
+    if c is not None and (c.cv.shape != (n - 1, m) or c.ch.shape != (n, m - 1)):
+        raise ValueError(f"weight shapes {c.cv.shape}/{c.ch.shape} do not match grid {(n, m)}")
+    if gradient_lo not in (0.0, 0, -np.pi):
+        raise ValueError(f"lo must be 0 or -pi, got {gradient_lo!r}")
+
+
+def _validate_device(x_dev):
+    torch = _torch()
+    chk = torch.stack([x_dev.min(), x_dev.max(), torch.isfinite(x_dev).all().to(torch.float64)]).cpu()
+    if chk[2] != 1.0:
+        raise ValueError("phase grid contains non-finite values")
+    if float(chk[0]) < 0.0 or float(chk[1]) >= 2.0 * np.pi:
+        raise ValueError("wrapped phase values must lie in [0, 2*pi)")
+
+
+def unwrap_rows(x, c: WeightField | None = None, model: ModelParams | None = None, params: IrlsParams | None = None,
+                gradient_lo=-np.pi, *, dtype="fp64", bands=None, group=None, gather=True, device=None):
+    """irls.py:132-224 on a row-sharded grid.
+
+    Inside a torch.distributed job (and `bands` None) every rank passes the same
+    full grid `x` and solves its own row band, exchanging halos, reduction
+    totals and the DCT transpose with the others (`group`, default world).
+    Otherwise `bands` = B > 1 runs all B bands in this process on one device
+    (loopback collectives) — the same decomposition, for testing.
+    Returns an UnwrapResult with the full grid on every rank when `gather`,
+    else the rank's band arrays (u, vv, vh rows of its band) and the trace.
+    """
+    nat.ensure()
+    torch = _torch()
+    model = model or ModelParams()
+    params = params or IrlsParams()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    arr = np.asarray(x, dtype=np.float64) if not isinstance(x, torch.Tensor) else x
+    if arr.ndim != 2 or arr.shape[0] < 1 or arr.shape[1] < 1:
+        raise ValueError(f"phase grid must be 2-D and non-empty, got shape {tuple(arr.shape)}")
+    n, m = int(arr.shape[0]), int(arr.shape[1])
+    _check_inputs(arr, c, n, m, gradient_lo)
+    import torch.distributed as dist
+    distributed = bands is None and dist.is_available() and dist.is_initialized()
+    world = dist.get_world_size(group) if distributed else int(bands or 1)
+    lay = BandLayout(n, m, world)
+    if distributed:
+        rank = dist.get_rank(group)
+        comm, ranks = DistComm(group), [rank]
+    else:
+        comm, ranks = LoopbackComm(world), list(range(world))
+    with torch.cuda.device(dev):
+        xs = []
+        for r in ranks:  # only the rows a band needs travel to the device
+            r0, rows = lay.row0[r], lay.rows[r]
+            hi = min(n, r0 + rows + 1)
+            sl = torch.as_tensor(np.ascontiguousarray(arr[r0:hi])) if isinstance(arr, np.ndarray) else arr[r0:hi]
+            xs.append(sl.to(device=dev, dtype=torch.float64).contiguous())
+        for xr in xs:
+            _validate_device(xr)
+        band_states = [BandState(lay, r, dtype, model.tau, model.delta, dev) for r in ranks]
+        driver = BandUnwrap(band_states, comm)
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            driver.load(xs, c, gradient_lo)
+            trace = run_loop(driver, c, model, params)
+            parts = [driver.band_arrays(b) for b in band_states]
+        torch.cuda.current_stream(dev).wait_stream(s)
+        if distributed and gather:
+            parts = _gather_bands(parts[0], lay, group)
+        if gather or not distributed:
+            u = torch.cat([p[0] for p in parts]).cpu().numpy()
+            vv = torch.cat([p[1] for p in parts]).cpu().numpy()
+            vh = torch.cat([p[2] for p in parts]).cpu().numpy()
+        else:
+            u, vv, vh = (t.cpu().numpy() for t in parts[0])
+    return UnwrapResult(u=u, vv=vv, vh=vh, trace=trace)
+
+
+def _gather_bands(part, lay, group):
+    """all-gather of every rank's (u, vv, vh) band rows (padded to the largest band)."""
+    import torch.distributed as dist
+    torch = _torch()
+    out = []
+    rmax = max(lay.rows)
+    for idx, t in enumerate(part):
+        pad = torch.zeros((rmax, t.shape[1]), dtype=t.dtype, device=t.device)
+        pad[:t.shape[0]] = t
+        bufs = [torch.empty_like(pad) for _ in range(lay.world)]
+        dist.all_gather(bufs, pad, group=group)
+        rows = []
+        for r in range(lay.world):
+            nr = lay.rows[r] if idx != 1 else max(0, min(lay.rows[r], lay.n - 1 - lay.row0[r]))
+            rows.append(bufs[r][:nr])
+        out.append(rows)
+    return [(out[0][r], out[1][r], out[2][r]) for r in range(lay.world)]
+

@@ -46,7 +46,6 @@ static std::atomic<long long> g_launches{0};
     PU_CUDA(call);                                         \
   } while (0)
 
-enum Site { S_DOT = 0, S_WH, S_EVH, S_HPAIR, S_ACC, S_EVF, S_START, S_K1, S_K2, S_K3, S_UPD, S_K2B, S_NSITES };
 
 typedef long double ld_t;
 static const ld_t kPi = 3.141592653589793238462643383279502884L;
@@ -343,6 +342,10 @@ struct Impl : HandleBase {
   Timer tm;
   GraphCache graphs;
   bool use_graphs = true;
+  bool band = false;   // row band of a sharded grid (init with pu_band)
+  Grid gc{};           // grid of the column transform (band: the column block, else g)
+  Pack pk{};           // packed transpose layout of the band's spectrum (nq = 0: plain)
+  int col0 = 0;        // first global column of the band's column block
 
   ~Impl() override {
     prow.release();
@@ -352,17 +355,33 @@ struct Impl : HandleBase {
     if (pinned_done) cudaFreeHost(pinned_done);
   }
 
-  int init(int n, int m, double tau, double delta) {
+  // b == nullptr: the whole N x M grid.  Otherwise one row band of a
+  // row-sharded grid (pu_create_band): planes carry ghost rows -1 and n, the
+  // column transform runs on the band's column block of the transposed
+  // spectrum, and reductions leave band totals for the cross-rank all-reduce.
+  int init(int n, int m, double tau, double delta, const pu_band* b = nullptr) {
+    const int n_glob = b ? b->n_glob : n;
+    if (b) n = b->rows;
+    band = b != nullptr;
     g.n = n; g.m = m;
     g.ld = ((long long)m + 7) / 8 * 8;
-    g.plane = (long long)n * g.ld;
+    g.plane = (long long)(n + (band ? 2 : 0)) * g.ld;
     g.tau = tau; g.inv_tau = 1.0 / tau; g.delta = delta;
+    g.n_glob = n_glob;
+    g.top = band && b->row0 > 0;
+    g.bot = band && b->row0 + b->rows < n_glob;
+    gc = g;
+    if (band) {
+      gc.n = n_glob; gc.m = b->cols; gc.ld = b->mb; gc.plane = (long long)n_glob * b->mb;
+      gc.top = gc.bot = 0;
+      pk = Pack{b->nq, b->mb, (long long)n * b->mb};
+      col0 = b->col0;
+    }
     int rc;
-    if ((rc = prow.build(m)) || (rc = pcol.build(n))) return rc;
+    if ((rc = prow.build(m)) || (rc = pcol.build(n_glob))) return rc;
     // row kernels (k_rows_pipe): one row pair per CTA, whole sequence in one group
-    if (rows_pipe_smem(prow.dev.n, sizeof(T), prow.dev.ldseq) > kSmemLimit) prow.dev.stage1 = 1;
-    if (prow.threads_for(1) > prow.max_threads() ||
-        rows_pipe_smem(prow.dev.n, sizeof(T), prow.dev.ldseq, prow.dev.stage1 ? 1 : 2) > kSmemLimit)
+    if (pipe_bytes(2) > kSmemLimit) prow.dev.stage1 = 1;
+    if (prow.threads_for(1) > prow.max_threads() || pipe_bytes(prow.dev.stage1 ? 1 : 2) > kSmemLimit)
       return fail(PU_ERR_UNSUPPORTED, "row length " + std::to_string(m) + " exceeds the shared-memory FFT limit");
     // column kernels (k_cols_spec): panel of W = 2 cc columns
     // 2 sequences (W = 4 columns) per CTA, all in one thread group (<= 512
@@ -379,7 +398,7 @@ struct Impl : HandleBase {
     int cc = col_static ? scc : PU_PANEL_COLS / 2;
     if (!col_static && pcol.smem_for(cc) > kSmemLimit) cc = 1;
     if (pcol.threads_for(cc) > pcol.max_threads() || pcol.smem_for(cc) > kSmemLimit)
-      return fail(PU_ERR_UNSUPPORTED, "column length " + std::to_string(n) + " exceeds the shared-memory FFT limit");
+      return fail(PU_ERR_UNSUPPORTED, "column length " + std::to_string(n_glob) + " exceeds the shared-memory FFT limit");
     col_is_static = col_static;
     cols_per_cta = 2 * cc;
     col_threads = pcol.threads_for(cc);
@@ -397,6 +416,13 @@ struct Impl : HandleBase {
 
   static constexpr int EM = sizeof(T) == 4 ? 16 : 8;
 
+  // dynamic shared memory of the row kernels with `staged` rows of staging
+  size_t pipe_bytes(int staged) const {
+    const size_t row = std::max<size_t>(stage_row_bytes(prow.dev.n, sizeof(T)),
+                                        (size_t)pk.nq * pk.mb * sizeof(T));  // packed band input
+    return 128 + staged * row + (size_t)prow.dev.ldseq * 2 * sizeof(T);
+  }
+
   int set_smem_attrs() {
     rops = ops_for<T>(prow.dev.bluestein ? 0 : prow.dev.L);
     cops = ops_for<T>(col_is_static ? pcol.dev.L : 0);
@@ -406,7 +432,7 @@ struct Impl : HandleBase {
     PU_CUDA(cops.set_attrs(kSmemLimit, kSmemLimit));
     // persistent pipelined row kernels: one row pair per iteration
     pipe_threads = prow.threads_for(1);
-    pipe_smem = rows_pipe_smem(prow.dev.n, sizeof(T), prow.dev.ldseq, prow.dev.stage1 ? 1 : 2);
+    pipe_smem = pipe_bytes(prow.dev.stage1 ? 1 : 2);
     if (pipe_smem > kSmemLimit)
       return fail(PU_ERR_UNSUPPORTED, "row length " + std::to_string(g.m) + " exceeds the row pipeline staging");
     int dev = 0, sms = 148;
@@ -421,13 +447,13 @@ struct Impl : HandleBase {
   XLaunch cl(cudaStream_t st) const { return XLaunch{col_grid(), col_threads, col_smem, st}; }
   XLaunch pl_(cudaStream_t st) const { return XLaunch{pipe_grid, pipe_threads, pipe_smem, st}; }
 
-  int col_grid() const { return (g.m + cols_per_cta - 1) / cols_per_cta; }
+  int col_grid() const { return (gc.m + cols_per_cta - 1) / cols_per_cta; }
 
   // ---- preconditioner passes ----
   int sylvester(const T* r, T* z, T* spec, cudaStream_t st) {
-    PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, nullptr, nullptr, 0));
-    PU_DCT(cops.cols(MODE_API, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, nullptr, rs, S_K3, 0));
-    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, z, nullptr, nullptr, 0));
+    PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, nullptr, nullptr, 0, Pack{}));
+    PU_DCT(cops.cols(MODE_API, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, nullptr, rs, S_K3, 0));
+    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, z, nullptr, nullptr, 0, Pack{}));
     return PU_OK;
   }
 
@@ -459,15 +485,15 @@ struct Impl : HandleBase {
     PU_LAUNCH_CHECK();
     tm.end(st, e, TK_K2, -1);
     e = tm.begin(st);
-    PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl, nullptr, 0));
+    PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl, nullptr, 0, Pack{}));
     tm.end(st, e, TK_K2B, -1);
     e = tm.begin(st);
-    PU_DCT(cops.cols(MODE_INIT, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, ctrl, rs, S_K3, -1));
+    PU_DCT(cops.cols(MODE_INIT, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, ctrl, rs, S_K3, -1));
     tm.end(st, e, TK_K3, -1);
     // p of iteration k lives in pbuf[k & 1]; K4 writes its u block (p = z at k = 0)
     T* pbuf[2] = {p0, p1};
     e = tm.begin(st);
-    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, pbuf[0], ctrl, pbuf[1], 1));
+    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, pbuf[0], ctrl, pbuf[1], 1, Pack{}));
     tm.end(st, e, TK_K4, -1);
     const int chunk = 64;
     for (int it = 0; it < max_iters; ++it) {
@@ -498,15 +524,94 @@ struct Impl : HandleBase {
         tm.end(st, e, TK_K2, it);
       }
       e = tm.begin(st);
-      PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl, nullptr, 0));
+      PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl, nullptr, 0, Pack{}));
       tm.end(st, e, TK_K2B, it);
       e = tm.begin(st);
-      PU_DCT(cops.cols(MODE_ITER, cl(st), g, pcol.dev, prow.dev.lam, cols_per_cta, spec, ctrl, rs, S_K3, it));
+      PU_DCT(cops.cols(MODE_ITER, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, ctrl, rs, S_K3, it));
       tm.end(st, e, TK_K3, it);
       e = tm.begin(st);  // u block of p for iteration it + 1: beta p_u + z_u
-      PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, pbuf[(it + 1) & 1], ctrl, pn, 0));
+      PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, pbuf[(it + 1) & 1], ctrl, pn, 0, Pack{}));
       tm.end(st, e, TK_K4, it);
     }
+    return PU_OK;
+  }
+
+  // ---- the same iteration as separate launches, for row-sharded grids (the
+  // host all-reduces the band totals and calls finalize() between them; see
+  // paper_2401_09961_b200/band.py).  On a whole grid they reproduce pcg(). ----
+  int pcg_begin(const T* b, const T* x0, T* x, const T* dv, const T* dh, T* r, PcgCtrl* ctrl, double* norms,
+                double rel_tol, int max_iters, const CandArgs<T>* cand, cudaStream_t st) {
+    const int vg = vec_grid();
+    cudaEvent_t e = tm.begin(st);
+    if (cand)
+      k_pcg_start_v<T, true><<<vg, 256, 0, st>>>(g, b, x0, x, r, dv, dh, ctrl, norms, rel_tol, max_iters, rs, S_START,
+                                                  *cand);
+    else
+      k_pcg_start_v<T, false><<<vg, 256, 0, st>>>(g, b, x0, x, r, dv, dh, ctrl, norms, rel_tol, max_iters, rs,
+                                                   S_START, CandArgs<T>{});
+    PU_LAUNCH_CHECK();
+    tm.end(st, e, TK_START, -1);
+    return PU_OK;
+  }
+
+  // K2a (it < 0: initial rho_s only; submean: the every-50 re-projection
+  // after pcg_update_sum) then K2b, the row DCT-II of r_u into spec_out
+  // (packed for the transpose in band mode)
+  int pcg_residual_rows(const T* p, const T* dv, const T* dh, T* x, T* r, PcgCtrl* ctrl, double* norms, T* spec_out,
+                        int it, int submean, cudaStream_t st) {
+    const int vg = vec_grid();
+    cudaEvent_t e = tm.begin(st);
+    if (it < 0)
+      k_pcg_r_v<T, false, false, MODE_INIT><<<vg, 256, 0, st>>>(g, nullptr, dv, dh, x, r, ctrl, norms, rs, S_K2, -1);
+    else if (submean)
+      k_pcg_r_v<T, false, true, MODE_ITER><<<vg, 256, 0, st>>>(g, p, dv, dh, x, r, ctrl, norms, rs, S_K2, it);
+    else
+      k_pcg_r_v<T, true, false, MODE_ITER><<<vg, 256, 0, st>>>(g, p, dv, dh, x, r, ctrl, norms, rs, S_K2, it);
+    PU_LAUNCH_CHECK();
+    tm.end(st, e, TK_K2, it);
+    e = tm.begin(st);
+    PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec_out, ctrl, nullptr, 0, pk));
+    tm.end(st, e, TK_K2B, it);
+    return PU_OK;
+  }
+
+  int pcg_update_sum(const T* p, const T* dv, const T* dh, T* x, T* r, PcgCtrl* ctrl, int it, cudaStream_t st) {
+    cudaEvent_t e = tm.begin(st);
+    k_pcg_upd_sum_v<T><<<vec_grid(), 256, 0, st>>>(g, p, dv, dh, x, r, ctrl, rs, S_UPD);
+    PU_LAUNCH_CHECK();
+    tm.end(st, e, TK_UPD, it);
+    return PU_OK;
+  }
+
+  // K3 on the (column block of the) spectrum, in place
+  int pcg_columns(T* spec, PcgCtrl* ctrl, int it, cudaStream_t st) {
+    cudaEvent_t e = tm.begin(st);
+    PU_DCT(cops.cols(it < 0 ? MODE_INIT : MODE_ITER, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec,
+                     ctrl, rs, S_K3, it));
+    tm.end(st, e, TK_K3, it);
+    return PU_OK;
+  }
+
+  // K4: u block of the next direction, pnew_u = beta pold_u + DCT-III rows (first: no axpy)
+  int pcg_rows_inv(const T* spec_in, T* pnew, const T* pold, int first, PcgCtrl* ctrl, int it, cudaStream_t st) {
+    cudaEvent_t e = tm.begin(st);
+    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec_in, pnew, ctrl, pold, first, pk));
+    tm.end(st, e, TK_K4, it);
+    return PU_OK;
+  }
+
+  // K1 (band mode: after the ghost-row slack of the new direction)
+  int pcg_direction(const T* r, const T* pold, T* pnew, const T* dv, const T* dh, PcgCtrl* ctrl, int it,
+                    cudaStream_t st) {
+    cudaEvent_t e = tm.begin(st);
+    if (g.top) {
+      const int thr = 256, blocks = std::max(1, std::min(148, (g.m / 4 + thr - 1) / thr));
+      k_ghost_pslack<T><<<blocks, thr, 0, st>>>(g, r, pold, pnew, dv, ctrl, it);
+      PU_LAUNCH_CHECK();
+    }
+    k_pcg_p_v<T><<<vec_grid(), 256, 0, st>>>(g, r, pold, pnew, dv, dh, ctrl, rs, S_K1, it);
+    PU_LAUNCH_CHECK();
+    tm.end(st, e, TK_K1, it);
     return PU_OK;
   }
 };
@@ -883,6 +988,106 @@ int pu_pcg_solve(pu_handle* h, const void* b, const void* x0, void* x, const voi
   PU_DISPATCH(h, {
     return I.pcg(CP(b), CP(x0), MP(x), CP(dv), CP(dh), MP(r), MP(z), MP(p0), MP(p1), MP(spec), max_iters, rel_tol,
                  reinterpret_cast<PcgCtrl*>(ctrl), res_norms, ST(stream));
+  });
+}
+
+int pu_create_band(pu_handle** out, int m, const pu_band* b, int dtype, double tau, double delta) {
+  if (!out || !b) return fail(PU_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (b->n_glob < 2 || m < 1 || b->rows < 1 || b->row0 < 0 || b->row0 + b->rows > b->n_glob)
+    return fail(PU_ERR_ARG, "invalid row band");
+  if (b->nq < 1 || b->mb < 8 || b->mb % 8 != 0 || (long long)b->nq * b->mb < m)
+    return fail(PU_ERR_ARG, "transpose chunks: mb must be a multiple of 8 with nq * mb >= M");
+  if (b->col0 < 0 || b->cols < 1 || b->cols > b->mb || b->col0 + b->cols > m || b->col0 % b->mb != 0)
+    return fail(PU_ERR_ARG, "invalid column block");
+  if (!(tau > 0) || !std::isfinite(tau)) return fail(PU_ERR_ARG, "tau must be positive and finite");
+  if (!(delta > 0) || !std::isfinite(delta)) return fail(PU_ERR_ARG, "delta must be positive and finite");
+  if (dtype != PU_F32 && dtype != PU_F64) return fail(PU_ERR_ARG, "dtype must be PU_F32 or PU_F64");
+  pu_handle* h = new pu_handle();
+  h->dtype = dtype;
+  int rc;
+  if (dtype == PU_F32) {
+    h->f = new Impl<float>();
+    rc = h->f->init(b->rows, m, tau, delta, b);
+  } else {
+    h->d = new Impl<double>();
+    rc = h->d->init(b->rows, m, tau, delta, b);
+  }
+  if (rc != PU_OK) {
+    std::string keep = g_last_error;
+    delete h->f;
+    delete h->d;
+    delete h;
+    g_last_error = keep;
+    return rc;
+  }
+  *out = h;
+  return PU_OK;
+}
+
+int pu_set_band_totals(pu_handle* h, double* totals) {
+  PU_DISPATCH(h, { I.rs.dist = totals; });
+  return PU_OK;
+}
+
+int pu_finalize(pu_handle* h, unsigned mask, int mode, int it, void* ctrl, double* res_norms, double* out,
+                double rel_tol, int max_iters, void* stream) {
+  PU_DISPATCH(h, {
+    if (!I.rs.dist) return fail(PU_ERR_ARG, "pu_finalize needs pu_set_band_totals");
+    const FinArgs a{reinterpret_cast<PcgCtrl*>(ctrl), res_norms, out, rel_tol, max_iters, it, mode};
+    k_finalize<<<1, 32, 0, ST(stream)>>>(I.g, I.rs.dist, mask, a);
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
+int pu_pcg_begin(pu_handle* h, const void* b, const void* x0, void* x, const void* dv, const void* dh, void* r,
+                 void* ctrl, double* res_norms, int max_iters, double rel_tol, const void* gv, const void* gh,
+                 const void* cv, const void* ch, const void* wv, const void* wh, double lipschitz, void* cand,
+                 void* stream) {
+  if (max_iters < 0) return fail(PU_ERR_ARG, "max_iters must be >= 0");
+  if (rel_tol < 0) return fail(PU_ERR_ARG, "rel_tol must be >= 0");
+  if (cand && !(lipschitz > 0)) return fail(PU_ERR_ARG, "lipschitz constant must be positive");
+  if ((cv == nullptr) != (ch == nullptr)) return fail(PU_ERR_ARG, "cv and ch must both be given or both NULL");
+  PU_DISPATCH(h, {
+    const CandArgs<T> ca{CP(gv), CP(gh), CP(cv), CP(ch), CP(wv), CP(wh), (T)(cand ? -1.0 / lipschitz : 0.0),
+                         MP(cand)};
+    return I.pcg_begin(CP(b), CP(x0), MP(x), CP(dv), CP(dh), MP(r), reinterpret_cast<PcgCtrl*>(ctrl), res_norms,
+                       rel_tol, max_iters, cand ? &ca : nullptr, ST(stream));
+  });
+}
+
+int pu_pcg_residual_rows(pu_handle* h, const void* p, const void* dv, const void* dh, void* x, void* r, void* ctrl,
+                         double* res_norms, void* spec_out, int it, int submean, void* stream) {
+  PU_DISPATCH(h, {
+    return I.pcg_residual_rows(CP(p), CP(dv), CP(dh), MP(x), MP(r), reinterpret_cast<PcgCtrl*>(ctrl), res_norms,
+                               MP(spec_out), it, submean, ST(stream));
+  });
+}
+
+int pu_pcg_update_sum(pu_handle* h, const void* p, const void* dv, const void* dh, void* x, void* r, void* ctrl,
+                      int it, void* stream) {
+  PU_DISPATCH(h, {
+    return I.pcg_update_sum(CP(p), CP(dv), CP(dh), MP(x), MP(r), reinterpret_cast<PcgCtrl*>(ctrl), it, ST(stream));
+  });
+}
+
+int pu_pcg_columns(pu_handle* h, void* spec, void* ctrl, int it, void* stream) {
+  PU_DISPATCH(h, { return I.pcg_columns(MP(spec), reinterpret_cast<PcgCtrl*>(ctrl), it, ST(stream)); });
+}
+
+int pu_pcg_rows_inv(pu_handle* h, const void* spec_in, void* pnew, const void* pold, int first, void* ctrl, int it,
+                    void* stream) {
+  PU_DISPATCH(h, {
+    return I.pcg_rows_inv(CP(spec_in), MP(pnew), CP(pold), first, reinterpret_cast<PcgCtrl*>(ctrl), it, ST(stream));
+  });
+}
+
+int pu_pcg_direction(pu_handle* h, const void* r, const void* pold, void* pnew, const void* dv, const void* dh,
+                     void* ctrl, int it, void* stream) {
+  PU_DISPATCH(h, {
+    return I.pcg_direction(CP(r), CP(pold), MP(pnew), CP(dv), CP(dh), reinterpret_cast<PcgCtrl*>(ctrl), it,
+                           ST(stream));
   });
 }
 

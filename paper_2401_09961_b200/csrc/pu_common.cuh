@@ -22,7 +22,17 @@ struct Grid {
   double tau;
   double inv_tau;
   double delta;
+  // row band of a row-sharded grid (pu_create_band): rows [row0, row0 + n) of
+  // n_glob; `top`/`bot` = a neighbour band's row is mirrored in the ghost row
+  // -1 / n of every plane.  Single-GPU grids: n_glob = n, top = bot = 0.
+  int n_glob;
+  int top;
+  int bot;
 };
+
+// vertical neighbours of row i within the global grid (ghost rows count)
+__host__ __device__ __forceinline__ bool dn_ok(const Grid& g, int i) { return i < g.n - 1 || g.bot; }
+__host__ __device__ __forceinline__ bool up_ok(const Grid& g, int i) { return i > 0 || g.top; }
 
 template <typename T> struct Vec2;
 template <> struct Vec2<float> { using type = float2; };
@@ -53,6 +63,7 @@ struct RedScratch {
   double* partials;       // [PU_MAX_SUMS][stride]
   unsigned int* ticket;   // one counter per reduction site
   int stride;             // >= max gridDim.x of any reducing kernel
+  double* dist;           // band mode: [S_NSITES][PU_MAX_SUMS] band totals (pu_fin.cuh), else null
 };
 
 #define PU_MAX_SUMS 12

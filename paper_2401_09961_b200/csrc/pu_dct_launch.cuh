@@ -24,7 +24,7 @@ struct DctLaunch {
 
   // pipelined persistent row transforms (pu_pipe.cuh); grid from occupancy
   static cudaError_t rows_pipe(bool inv, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const T* in, T* out,
-                               const PcgCtrl* ctrl, const T* pold, int first);
+                               const PcgCtrl* ctrl, const T* pold, int first, Pack pk);
   static int rows_pipe_blocks_per_sm(int threads, size_t smem);
   static cudaError_t cols(int mode, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const T* lam_cols,
                           int cpc, T* data, PcgCtrl* ctrl, RedScratch rs, int site, int it);
@@ -47,11 +47,11 @@ cudaError_t DctLaunch<T, LS>::set_attrs(size_t row_smem, size_t col_smem) {
 
 template <typename T, int LS>
 cudaError_t DctLaunch<T, LS>::rows_pipe(bool inv, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const T* in,
-                                        T* out, const PcgCtrl* ctrl, const T* pold, int first) {
+                                        T* out, const PcgCtrl* ctrl, const T* pold, int first, Pack pk) {
   if (inv)
-    k_rows_pipe<T, EM, LS, true><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, in, out, ctrl, pold, first);
+    k_rows_pipe<T, EM, LS, true><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, in, out, ctrl, pold, first, pk);
   else
-    k_rows_pipe<T, EM, LS, false><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, in, out, ctrl, nullptr, 0);
+    k_rows_pipe<T, EM, LS, false><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, in, out, ctrl, nullptr, 0, pk);
   return cudaGetLastError();
 }
 

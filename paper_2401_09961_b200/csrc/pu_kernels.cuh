@@ -15,6 +15,7 @@
 
 #include "pu_common.cuh"
 #include "pu_fft.cuh"
+#include "pu_fin.cuh"
 
 namespace pu {
 
@@ -28,7 +29,6 @@ __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, 
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 
 #define PU_TWO_PI 6.283185307179586
-#define PU_TINY_CURVATURE 1e-300
 
 // Element loop over the valid N x M cells: thread-strided columns, block-strided rows.
 #define PU_FOR_CELLS(g, i, j)                                                        \
@@ -71,9 +71,9 @@ __device__ __forceinline__ void sys_at(const Grid& g, const Src& s, const T* __r
   xv = s.V(o);
   xh = s.H(o);
   T su = 0, rv = 0, rvm = 0, ut = 0, rh = 0, rhm = 0;
-  const bool hasv = i < g.n - 1, hash = j < g.m - 1;
+  const bool hasv = dn_ok(g, i), hash = j < g.m - 1;
   if (hasv) { su = s.U(o + g.ld) - xu; rv = su - xv; }
-  if (i > 0) { rvm = (xu - s.U(o - g.ld)) - s.V(o - g.ld); }
+  if (up_ok(g, i)) { rvm = (xu - s.U(o - g.ld)) - s.V(o - g.ld); }
   if (hash) { ut = s.U(o + 1) - xu; rh = ut - xh; }
   if (j > 0) { rhm = (xu - s.U(o - 1)) - s.H(o - 1); }
   au = inv * ((rvm - rv) + (rhm - rh));
@@ -99,7 +99,7 @@ __global__ void k_grad(Grid g, const double* __restrict__ x, long long ldx, T* g
   PU_FOR_CELLS(g, i, j) {
     const long long o = (long long)i * g.ld + j;
     const double xij = x[(long long)i * ldx + j];
-    gv[o] = (i < g.n - 1) ? (T)wrap_lo(__dsub_rn(x[(long long)(i + 1) * ldx + j], xij), lo) : (T)0;
+    gv[o] = dn_ok(g, i) ? (T)wrap_lo(__dsub_rn(x[(long long)(i + 1) * ldx + j], xij), lo) : (T)0;
     gh[o] = (j < g.m - 1) ? (T)wrap_lo(__dsub_rn(x[(long long)i * ldx + j + 1], xij), lo) : (T)0;
   }
 }
@@ -110,7 +110,7 @@ __global__ void k_init_state(Grid g, const T* __restrict__ gv, const T* __restri
   PU_FOR_CELLS(g, i, j) {
     const long long o = (long long)i * g.ld + j;
     x[o] = (T)0;
-    x[o + g.plane] = (i < g.n - 1) ? -gv[o] : (T)0;
+    x[o + g.plane] = dn_ok(g, i) ? -gv[o] : (T)0;
     x[o + 2 * g.plane] = (j < g.m - 1) ? -gh[o] : (T)0;
   }
 }
@@ -120,7 +120,7 @@ __global__ void k_rhs(Grid g, const T* __restrict__ gv, const T* __restrict__ gh
   const T inv = (T)g.inv_tau;
   PU_FOR_CELLS(g, i, j) {
     const long long o = (long long)i * g.ld + j;
-    const T gvo = (i < g.n - 1) ? gv[o] : (T)0, gvm = (i > 0) ? gv[o - g.ld] : (T)0;
+    const T gvo = dn_ok(g, i) ? gv[o] : (T)0, gvm = up_ok(g, i) ? gv[o - g.ld] : (T)0;
     const T gho = (j < g.m - 1) ? gh[o] : (T)0, ghm = (j > 0) ? gh[o - 1] : (T)0;
     b[o] = inv * ((gvm - gvo) + (ghm - gho));
     b[o + g.plane] = -inv * gvo;
@@ -207,7 +207,7 @@ __device__ __forceinline__ void pen_at(const Grid& g, const T* u, const T* vv, c
   const long long o = (long long)i * g.ld + j;
   rv = 0.0; rh = 0.0;
   const double uo = (double)u[o] - ushift;
-  if (i < g.n - 1) rv = (((double)u[o + g.ld] - ushift) - uo) - (double)gv[o] - (double)vv[o];
+  if (dn_ok(g, i)) rv = (((double)u[o + g.ld] - ushift) - uo) - (double)gv[o] - (double)vv[o];
   if (j < g.m - 1) rh = (((double)u[o + 1] - ushift) - uo) - (double)gh[o] - (double)vh[o];
 }
 
@@ -225,7 +225,7 @@ __global__ void k_weights_hpair(Grid g, const T* __restrict__ x, const T* __rest
   double acc[6] = {0, 0, 0, 0, 0, 0};
   PU_FOR_CELLS(g, i, j) {
     const long long o = (long long)i * g.ld + j;
-    if (i < g.n - 1) {
+    if (dn_ok(g, i)) {
       const T c = cv[o], v = vv[o];
       const T cvt = c * v;
       const T w = sqrt(cvt * cvt + (T)d2);
@@ -270,7 +270,7 @@ __global__ void k_eval_h(Grid g, const T* __restrict__ x, const T* __restrict__ 
   double acc[4] = {0, 0, 0, 0};
   PU_FOR_CELLS(g, i, j) {
     const long long o = (long long)i * g.ld + j;
-    if (i < g.n - 1) acc[0] += slack_term((double)cv[o], (double)vv[o], (double)wv[o], d2);
+    if (dn_ok(g, i)) acc[0] += slack_term((double)cv[o], (double)vv[o], (double)wv[o], d2);
     if (j < g.m - 1) acc[1] += slack_term((double)ch[o], (double)vh[o], (double)wh[o], d2);
     double rv, rh;
     pen_at<T>(g, u, vv, vh, gv, gh, i, j, 0.0, rv, rh);
@@ -298,7 +298,7 @@ __global__ void k_hpair_states(Grid g, const T* __restrict__ xa, const T* __rest
     for (int s = 0; s < 2; ++s) {
       const T* x = s ? xb : xa;
       const T* u = x; const T* vv = x + g.plane; const T* vh = x + 2 * g.plane;
-      if (i < g.n - 1) acc[5 * s + 0] += slack_term((double)cv[o], (double)vv[o], (double)wv[o], d2);
+      if (dn_ok(g, i)) acc[5 * s + 0] += slack_term((double)cv[o], (double)vv[o], (double)wv[o], d2);
       if (j < g.m - 1) acc[5 * s + 1] += slack_term((double)ch[o], (double)vh[o], (double)wh[o], d2);
       double rv, rh;
       pen_at<T>(g, u, vv, vh, gv, gh, i, j, 0.0, rv, rh);
@@ -314,7 +314,7 @@ __global__ void k_hpair_states(Grid g, const T* __restrict__ xa, const T* __rest
     const bool take_a = ha <= hb;
     out[0] = ha;
     out[1] = hb;
-    out[2] = (take_a ? tot[4] : tot[9]) / ((double)g.n * (double)g.m);
+    out[2] = (take_a ? tot[4] : tot[9]) / ((double)g.n_glob * (double)g.m);
     out[3] = take_a ? 1.0 : 0.0;
   }
 }
@@ -328,11 +328,11 @@ __global__ void k_candidate(Grid g, const T* __restrict__ x, const T* __restrict
   const T* u = x; const T* vv = x + g.plane; const T* vh = x + 2 * g.plane;
   PU_FOR_CELLS(g, i, j) {
     const long long o = (long long)i * g.ld + j;
-    const bool hasv = i < g.n - 1, hash = j < g.m - 1;
+    const bool hasv = dn_ok(g, i), hash = j < g.m - 1;
     const T uo = u[o];
     T rv = 0, rvm = 0, rh = 0, rhm = 0;
     if (hasv) rv = ((u[o + g.ld] - uo) - gv[o]) - vv[o];
-    if (i > 0) rvm = ((uo - u[o - g.ld]) - gv[o - g.ld]) - vv[o - g.ld];
+    if (up_ok(g, i)) rvm = ((uo - u[o - g.ld]) - gv[o - g.ld]) - vv[o - g.ld];
     if (hash) rh = ((u[o + 1] - uo) - gh[o]) - vh[o];
     if (j > 0) rhm = ((uo - u[o - 1]) - gh[o - 1]) - vh[o - 1];
     const T gu = inv * ((rvm - rv) + (rhm - rh));
@@ -371,7 +371,7 @@ __global__ void k_accept(Grid g, const T* __restrict__ xa, const T* __restrict__
     const long long o = (long long)i * g.ld + j;
     const T uo = u[o] - tmean;
     double rv = 0.0, rh = 0.0;
-    if (i < g.n - 1) {
+    if (dn_ok(g, i)) {
       const T un = u[o + g.ld] - tmean;
       rv = ((double)un - (double)uo) - (double)gv[o] - (double)vv[o];
       acc[0] += slack_term((double)cv[o], (double)vv[o], (double)wv[o], d2);
@@ -400,7 +400,7 @@ __global__ void k_eval_f(Grid g, const T* __restrict__ x, const T* __restrict__ 
   double acc[4] = {0, 0, 0, 0};
   PU_FOR_CELLS(g, i, j) {
     const long long o = (long long)i * g.ld + j;
-    if (i < g.n - 1) acc[0] += fabs((double)cv[o] * (double)vv[o]);
+    if (dn_ok(g, i)) acc[0] += fabs((double)cv[o] * (double)vv[o]);
     if (j < g.m - 1) acc[1] += fabs((double)ch[o] * (double)vh[o]);
     double rv, rh;
     pen_at<T>(g, u, vv, vh, gv, gh, i, j, 0.0, rv, rh);

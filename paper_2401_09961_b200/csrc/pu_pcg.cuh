@@ -20,7 +20,6 @@
 
 namespace pu {
 
-enum { MODE_API = 0, MODE_INIT = 1, MODE_ITER = 2 };
 
 // ---------------------------------------------------------------------------
 // Column-panel staging for K3.  A panel is W = 2 * nseq columns x n rows;
@@ -166,19 +165,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   if (MODE != MODE_API) {
     double acc[1] = {(double)accT};
     double tot[1];
-    if (grid_reduce<1>(acc, rs, site, tot) && threadIdx.x == 0) {
-      const double rho_next = ctrl->rho_s + tot[0];
-      if (MODE == MODE_INIT) {
-        ctrl->rho = rho_next;
-      } else {
-        if (!isfinite(rho_next)) {
-          ctrl->breakdown = it + 1; ctrl->bkind = 3; ctrl->done = 1;
-        } else {
-          ctrl->beta = rho_next / ctrl->rho;
-          ctrl->rho = rho_next;
-        }
-      }
-    }
+    if (red_final<1>(acc, rs, site, tot) && threadIdx.x == 0) fin_k3(ctrl, tot, it, MODE);
   }
 }
 
@@ -189,7 +176,7 @@ __global__ void k_precond_slack(Grid g, const T* __restrict__ r, const T* __rest
   const T inv = (T)g.inv_tau;
   PU_FOR_CELLS(g, i, j) {
     const long long o = (long long)i * g.ld + j;
-    z[o + g.plane] = (i < g.n - 1) ? r[o + g.plane] / (dv[o] + inv) : (T)0;
+    z[o + g.plane] = dn_ok(g, i) ? r[o + g.plane] / (dv[o] + inv) : (T)0;
     z[o + 2 * g.plane] = (j < g.m - 1) ? r[o + 2 * g.plane] / (dh[o] + inv) : (T)0;
   }
 }

@@ -61,6 +61,17 @@ __host__ __device__ constexpr size_t rows_pipe_smem(int n, int tsize, int ldseq,
   return 128 + (size_t)rows_staged * stage_row_bytes(n, tsize) + (size_t)ldseq * 2 * tsize;
 }
 
+// Row-sharded grids (pu_create_band): the spectrum travels between the row
+// bands and the column bands of the all-to-all transpose in a packed layout,
+// chunk q = columns [q mb, (q + 1) mb) of the band's rows, row pitch mb:
+// element (i, k) at (k / mb) * chunk + i * mb + k % mb.  The forward kernel
+// writes it, the inverse one reads its rows as nq bulk copies.  nq = 0: plain.
+struct Pack {
+  int nq;
+  int mb;
+  long long chunk;
+};
+
 // pl.stage1 (rows too long for two staged rows next to the FFT buffer, e.g.
 // 16384 fp32): one staging row; row b is fetched after row a has been packed
 // (its half of the packing is linear, so the sum is bitwise the same), and
@@ -72,12 +83,14 @@ __host__ __device__ constexpr size_t rows_pipe_smem(int n, int tsize, int ldseq,
 template <typename T, int EMAX, int LS, bool INV>
 __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, EMAX))
     k_rows_pipe(Grid g, FftPlan<T> pl, const T* __restrict__ in, T* __restrict__ out, const PcgCtrl* ctrl,
-                const T* __restrict__ pold, int first) {
+                const T* __restrict__ pold, int first, Pack pk) {
   extern __shared__ __align__(128) unsigned char smraw[];
   if (ctrl && ctrl->done) return;
   const int n = LS > 0 ? LS : g.m;  // static plans only when n == L
   const int S = (g.n + 1) >> 1;     // row pairs
-  const unsigned RB = stage_row_bytes(n, sizeof(T));
+  const unsigned RBrow = stage_row_bytes(n, sizeof(T));  // one plain row
+  const bool pin = INV && pk.nq > 0, pout = !INV && pk.nq > 0;
+  const unsigned RB = pin ? (unsigned)(pk.nq * pk.mb * sizeof(T)) : RBrow;  // one staged input row
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw);
   T* sa = reinterpret_cast<T*>(smraw + 128);
   const bool one = pl.stage1 != 0;
@@ -88,17 +101,25 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
     fence_mbar_init();
   }
   __syncthreads();
+  auto fetch = [&](T* dst, int row) {  // one thread; RB bytes
+    if (pin) {
+      for (int q = 0; q < pk.nq; ++q)
+        bulk_g2s(dst + q * pk.mb, in + q * pk.chunk + (long long)row * pk.mb, pk.mb * (unsigned)sizeof(T), mbar);
+    } else {
+      bulk_g2s(dst, in + (long long)row * g.ld, RB, mbar);
+    }
+  };
   auto issue = [&](int seq) {  // one thread
     const int ia = 2 * seq;
     const bool hb = ia + 1 < g.n;
     if (one) {
       mbar_expect_tx(mbar, RB);
-      bulk_g2s(sa, in + (long long)ia * g.ld, RB, mbar);
+      fetch(sa, ia);
       return;
     }
     mbar_expect_tx(mbar, hb ? 2 * RB : RB);
-    bulk_g2s(sa, in + (long long)ia * g.ld, RB, mbar);
-    if (hb) bulk_g2s(sb, in + (long long)(ia + 1) * g.ld, RB, mbar);
+    fetch(sa, ia);
+    if (hb) fetch(sb, ia + 1);
   };
   // stage1: after the row-a pass, fetch row b into the same staging row
   auto issue_b = [&](int ia) {
@@ -106,7 +127,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
     if (threadIdx.x == 0) {
       fence_proxy_async();
       mbar_expect_tx(mbar, RB);
-      bulk_g2s(sa, in + (long long)(ia + 1) * g.ld, RB, mbar);
+      fetch(sa, ia + 1);
     }
     mbar_wait(mbar, 1);
   };
@@ -176,21 +197,41 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
     if (axpy && !one && threadIdx.x == 0) {
       // staging is free now: fetch the old search direction rows behind the FFT
       fence_proxy_async();
-      mbar_expect_tx(mbar, hasb ? 2 * RB : RB);
-      bulk_g2s(sa, pold + (long long)ia * g.ld, RB, mbar);
-      if (hasb) bulk_g2s(sb, pold + (long long)(ia + 1) * g.ld, RB, mbar);
+      mbar_expect_tx(mbar, hasb ? 2 * RBrow : RBrow);
+      bulk_g2s(sa, pold + (long long)ia * g.ld, RBrow, mbar);
+      if (hasb) bulk_g2s(sb, pold + (long long)(ia + 1) * g.ld, RBrow, mbar);
     }
     fft_n<T, EMAX, LS>(buf, 1, pl);
     const long long oa = (long long)ia * g.ld, ob = oa + g.ld;
     if constexpr (!INV) {
-      for (int k = threadIdx.x; k < half; k += blockDim.x) {
-        const int nk = k == 0 ? 0 : n - k;
-        const PairOut<T> q = dct2_post<T>(buf[spad(k)], buf[spad(nk)], k, nk, pl);
-        out[oa + k] = q.a_k;
-        if (hasb) out[ob + k] = q.b_k;
-        if (nk != k) {
-          out[oa + nk] = q.a_nk;
-          if (hasb) out[ob + nk] = q.b_nk;
+      if (pout) {
+        // packed: column k of rows ia, ia + 1 -> chunk k / mb
+        auto at = [&](int k) -> long long {
+          const int q = k / pk.mb;
+          return q * pk.chunk + (long long)ia * pk.mb + (k - q * pk.mb);
+        };
+        for (int k = threadIdx.x; k < half; k += blockDim.x) {
+          const int nk = k == 0 ? 0 : n - k;
+          const PairOut<T> q = dct2_post<T>(buf[spad(k)], buf[spad(nk)], k, nk, pl);
+          const long long ok_ = at(k);
+          out[ok_] = q.a_k;
+          if (hasb) out[ok_ + pk.mb] = q.b_k;
+          if (nk != k) {
+            const long long onk = at(nk);
+            out[onk] = q.a_nk;
+            if (hasb) out[onk + pk.mb] = q.b_nk;
+          }
+        }
+      } else {
+        for (int k = threadIdx.x; k < half; k += blockDim.x) {
+          const int nk = k == 0 ? 0 : n - k;
+          const PairOut<T> q = dct2_post<T>(buf[spad(k)], buf[spad(nk)], k, nk, pl);
+          out[oa + k] = q.a_k;
+          if (hasb) out[ob + k] = q.b_k;
+          if (nk != k) {
+            out[oa + nk] = q.a_nk;
+            if (hasb) out[ob + nk] = q.b_nk;
+          }
         }
       }
     } else {

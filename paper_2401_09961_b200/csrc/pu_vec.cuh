@@ -40,7 +40,7 @@ template <typename T>
 __device__ __forceinline__ void apply4(const Grid& g, int i, int j0, const Stencil4<T>& s, const Q4<T>& dv,
                                        const Q4<T>& dh, Q4<T>& au, Q4<T>& av, Q4<T>& ah) {
   const T inv = (T)g.inv_tau;
-  const bool hasv = i < g.n - 1, hasa = i > 0;
+  const bool hasv = dn_ok(g, i), hasa = up_ok(g, i);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int j = j0 + k;
@@ -71,6 +71,43 @@ __device__ __forceinline__ double slack_div(double a, double b) { return a / b; 
 template <typename T>
 __device__ __forceinline__ T ldg_or0(const T* p, bool ok) { return ok ? __ldg(p) : (T)0; }
 
+// slack block of the new search direction at 4 cells of row i (plane offset
+// po, diagonal d), masked to valid arcs: beta p_old + r / (d + 1/tau)
+template <typename T>
+__device__ __forceinline__ Q4<T> pslack4(const Grid& g, const T* __restrict__ r, const T* __restrict__ pold,
+                                         const T* __restrict__ d, long long o, long long po, int i, int j0,
+                                         bool vert, T beta, bool first) {
+  const T inv = (T)g.inv_tau;
+  const Q4<T> rr = ldg4(r + o + po), dd = ldg4(d + o);
+  Q4<T> out;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int j = j0 + k;
+    const bool ok = vert ? (dn_ok(g, i) && j < g.m) : (j < g.m - 1);
+    out.a[k] = ok ? slack_div(rr.a[k], dd.a[k] + inv) : (T)0;
+  }
+  if (!first) {
+    const Q4<T> pp = ldg4(pold + o + po);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) out.a[k] = add_rn(mul_rn(beta, pp.a[k]), out.a[k]);
+  }
+  return out;
+}
+
+// Band mode, before K1: the vv slack of the new direction in the ghost row -1
+// (the band above owns it; recomputed here from the mirrored r_vv, p_vv, dv
+// rows with K1's arithmetic, so K2a's stencil sees the same value)
+template <typename T>
+__global__ void k_ghost_pslack(Grid g, const T* __restrict__ r, const T* __restrict__ pold, T* __restrict__ pnew,
+                               const T* __restrict__ dv, const PcgCtrl* ctrl, int it) {
+  if (ctrl->done || !g.top) return;
+  const T beta = (T)ctrl->beta;
+  for (int j0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x); j0 < g.m; j0 += 4 * gridDim.x * blockDim.x) {
+    const long long o = -g.ld + j0;
+    st4(pnew + o + g.plane, pslack4<T>(g, r, pold, dv, o, g.plane, -1, j0, true, beta, it == 0));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K1.  The u block of the new search direction, p_u = beta p_u_old + z_u, was
 // already written by the row DCT-III kernel (K4) of the previous iteration;
@@ -88,35 +125,21 @@ __global__ void __launch_bounds__(256, 4) k_pcg_p_v(Grid g, const T* __restrict_
   const T beta = (T)ctrl->beta;
   const T inv = (T)g.inv_tau;
   const long long P = g.plane, ld = g.ld;
-  // slack p at 4 cells of row i (plane offset po, diagonal d), masked to valid arcs
   auto ps4 = [&](long long o, long long po, const T* d, int i, int j0, bool vert) -> Q4<T> {
-    const Q4<T> rr = ldg4(r + o + po), dd = ldg4(d + o);
-    Q4<T> out;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int j = j0 + k;
-      const bool ok = vert ? (i < g.n - 1 && j < g.m) : (j < g.m - 1);
-      out.a[k] = ok ? slack_div(rr.a[k], dd.a[k] + inv) : (T)0;
-    }
-    if (!first) {
-      const Q4<T> pp = ldg4(pold + o + po);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) out.a[k] = add_rn(mul_rn(beta, pp.a[k]), out.a[k]);
-    }
-    return out;
+    return pslack4<T>(g, r, pold, d, o, po, i, j0, vert, beta, first);
   };
   double acc[1] = {0.0};
   PU_FOR_CHUNKS(g, i, j0) {
     const long long o = (long long)i * ld + j0;
     Stencil4<T> s;
     s.u = ldg4(pnew + o);
-    s.ua = i > 0 ? ldg4(pnew + o - ld) : zero4<T>();
-    s.ub = i < g.n - 1 ? ldg4(pnew + o + ld) : zero4<T>();
+    s.ua = up_ok(g, i) ? ldg4(pnew + o - ld) : zero4<T>();
+    s.ub = dn_ok(g, i) ? ldg4(pnew + o + ld) : zero4<T>();
     s.ul = ldg_or0(pnew + o - 1, j0 > 0);
     s.ur = ldg_or0(pnew + o + 4, j0 + 4 < g.m);
     s.v = ps4(o, P, dv, i, j0, true);
     s.h = ps4(o, 2 * P, dh, i, j0, false);
-    s.va = i > 0 ? ps4(o - ld, P, dv, i - 1, j0, true) : zero4<T>();
+    s.va = up_ok(g, i) ? ps4(o - ld, P, dv, i - 1, j0, true) : zero4<T>();
     if (j0 > 0) {  // p_h at (i, j0 - 1)
       const T zr = (j0 - 1 < g.m - 1) ? slack_div(__ldg(r + o - 1 + 2 * P), __ldg(dh + o - 1) + inv) : (T)0;
       s.hl = first ? zr : add_rn(mul_rn(beta, __ldg(pold + o - 1 + 2 * P)), zr);
@@ -134,17 +157,7 @@ __global__ void __launch_bounds__(256, 4) k_pcg_p_v(Grid g, const T* __restrict_
     acc[0] += (double)part;
   }
   double tot[1];
-  if (grid_reduce<1>(acc, rs, site, tot) && threadIdx.x == 0) {
-    const double pap = tot[0];
-    ctrl->pap = pap;
-    if (!isfinite(pap)) {
-      ctrl->breakdown = it; ctrl->bkind = 1; ctrl->done = 1;
-    } else if (pap <= PU_TINY_CURVATURE) {
-      ctrl->converged = ctrl->rn <= ctrl->thr; ctrl->done = 1;
-    } else {
-      ctrl->alpha = ctrl->rho / pap;
-    }
-  }
+  if (red_final<1>(acc, rs, site, tot) && threadIdx.x == 0) fin_k1(ctrl, tot, it);
 }
 
 // ---------------------------------------------------------------------------
@@ -171,9 +184,9 @@ __global__ void __launch_bounds__(256, 3) k_pcg_r_v(Grid g, const T* __restrict_
       s.u = ldg4(p + o);
       s.v = ldg4(p + o + P);
       s.h = ldg4(p + o + 2 * P);
-      s.ua = i > 0 ? ldg4(p + o - ld) : zero4<T>();
-      s.va = i > 0 ? ldg4(p + o - ld + P) : zero4<T>();
-      s.ub = i < g.n - 1 ? ldg4(p + o + ld) : zero4<T>();
+      s.ua = up_ok(g, i) ? ldg4(p + o - ld) : zero4<T>();
+      s.va = up_ok(g, i) ? ldg4(p + o - ld + P) : zero4<T>();
+      s.ub = dn_ok(g, i) ? ldg4(p + o + ld) : zero4<T>();
       s.ul = ldg_or0(p + o - 1, j0 > 0);
       s.hl = ldg_or0(p + o - 1 + 2 * P, j0 > 0);
       s.ur = ldg_or0(p + o + 4, j0 + 4 < g.m);
@@ -205,7 +218,7 @@ __global__ void __launch_bounds__(256, 3) k_pcg_r_v(Grid g, const T* __restrict_
 #pragma unroll
     for (int k = 0; k < 4; ++k) {  // z_s = r_s / (d + 1/tau) (preconditioner.py:115), recomputed by K1
       const int j = j0 + k;
-      const T zv = (i < g.n - 1 && j < g.m) ? slack_div(rv.a[k], d1.a[k] + inv) : (T)0;
+      const T zv = (dn_ok(g, i) && j < g.m) ? slack_div(rv.a[k], d1.a[k] + inv) : (T)0;
       const T zh = (j < g.m - 1) ? slack_div(rh.a[k], d2.a[k] + inv) : (T)0;
       prr += ru.a[k] * ru.a[k] + rv.a[k] * rv.a[k] + rh.a[k] * rh.a[k];
       prz += rv.a[k] * zv + rh.a[k] * zh;
@@ -214,20 +227,7 @@ __global__ void __launch_bounds__(256, 3) k_pcg_r_v(Grid g, const T* __restrict_
     acc[1] += (double)prz;
   }
   double tot[2];
-  if (grid_reduce<2>(acc, rs, site, tot) && threadIdx.x == 0) {
-    ctrl->rho_s = tot[1];
-    if (MODE == 2 /* MODE_ITER */) {
-      const double rn = sqrt(tot[0]);
-      ctrl->rn = rn;
-      if (!isfinite(rn)) {
-        ctrl->breakdown = it + 1; ctrl->bkind = 2; ctrl->done = 1;
-      } else {
-        res_norms[it + 1] = rn;
-        ctrl->iterations = it + 1;
-        if (rn <= ctrl->thr) { ctrl->converged = 1; ctrl->done = 1; }
-      }
-    }
-  }
+  if (red_final<2>(acc, rs, site, tot) && threadIdx.x == 0) fin_k2(ctrl, res_norms, tot, it, MODE);
 }
 
 // update + sum(r_u) for the every-50 re-projection (the mean is subtracted by
@@ -247,9 +247,9 @@ __global__ void __launch_bounds__(256) k_pcg_upd_sum_v(Grid g, const T* __restri
     s.u = ldg4(p + o);
     s.v = ldg4(p + o + P);
     s.h = ldg4(p + o + 2 * P);
-    s.ua = i > 0 ? ldg4(p + o - ld) : zero4<T>();
-    s.va = i > 0 ? ldg4(p + o - ld + P) : zero4<T>();
-    s.ub = i < g.n - 1 ? ldg4(p + o + ld) : zero4<T>();
+    s.ua = up_ok(g, i) ? ldg4(p + o - ld) : zero4<T>();
+    s.va = up_ok(g, i) ? ldg4(p + o - ld + P) : zero4<T>();
+    s.ub = dn_ok(g, i) ? ldg4(p + o + ld) : zero4<T>();
     s.ul = ldg_or0(p + o - 1, j0 > 0);
     s.hl = ldg_or0(p + o - 1 + 2 * P, j0 > 0);
     s.ur = ldg_or0(p + o + 4, j0 + 4 < g.m);
@@ -271,8 +271,7 @@ __global__ void __launch_bounds__(256) k_pcg_upd_sum_v(Grid g, const T* __restri
     st4(r + o, ru); st4(r + o + P, rv); st4(r + o + 2 * P, rh);
   }
   double tot[1];
-  if (grid_reduce<1>(acc, rs, site, tot) && threadIdx.x == 0)
-    ctrl->mean_ru = tot[0] / ((double)g.n * (double)g.m);
+  if (red_final<1>(acc, rs, site, tot) && threadIdx.x == 0) fin_upd(g, ctrl, tot);
 }
 
 // setup: x = x0 (skipped when x aliases x0), r = b - A x0, ||b||, ||r0||
@@ -301,9 +300,9 @@ __global__ void __launch_bounds__(256, 3) k_pcg_start_v(Grid g, const T* __restr
     s.u = ldg4(x0 + o);
     s.v = ldg4(x0 + o + P);
     s.h = ldg4(x0 + o + 2 * P);
-    s.ua = i > 0 ? ldg4(x0 + o - ld) : zero4<T>();
-    s.va = i > 0 ? ldg4(x0 + o - ld + P) : zero4<T>();
-    s.ub = i < g.n - 1 ? ldg4(x0 + o + ld) : zero4<T>();
+    s.ua = up_ok(g, i) ? ldg4(x0 + o - ld) : zero4<T>();
+    s.va = up_ok(g, i) ? ldg4(x0 + o - ld + P) : zero4<T>();
+    s.ub = dn_ok(g, i) ? ldg4(x0 + o + ld) : zero4<T>();
     s.ul = ldg_or0(x0 + o - 1, j0 > 0);
     s.hl = ldg_or0(x0 + o - 1 + 2 * P, j0 > 0);
     s.ur = ldg_or0(x0 + o + 4, j0 + 4 < g.m);
@@ -326,12 +325,12 @@ __global__ void __launch_bounds__(256, 3) k_pcg_start_v(Grid g, const T* __restr
     st4(r + o, ru); st4(r + o + P, rv); st4(r + o + 2 * P, rh);
     if constexpr (CAND) {
       const Q4<T> g1 = ldg4(ca.gv + o), g2 = ldg4(ca.gh + o);
-      const Q4<T> ga = i > 0 ? ldg4(ca.gv + o - ld) : zero4<T>();
+      const Q4<T> ga = up_ok(g, i) ? ldg4(ca.gv + o - ld) : zero4<T>();
       const T gl = ldg_or0(ca.gh + o - 1, j0 > 0);
       const Q4<T> w1 = ldg4(ca.wv + o), w2 = ldg4(ca.wh + o);
       Q4<T> c1, c2;
       if (ca.cv) { c1 = ldg4(ca.cv + o); c2 = ldg4(ca.ch + o); }
-      const bool hasb = i < g.n - 1, hasa = i > 0;
+      const bool hasb = dn_ok(g, i), hasa = up_ok(g, i);
       Q4<T> ou, ov, oh;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -359,22 +358,7 @@ __global__ void __launch_bounds__(256, 3) k_pcg_start_v(Grid g, const T* __restr
     }
   }
   double tot[2];
-  if (grid_reduce<2>(acc, rs, site, tot) && threadIdx.x == 0) {
-    const double bn = sqrt(tot[0]);
-    const double rn = sqrt(tot[1]);
-    ctrl->bnorm = bn;
-    ctrl->thr = rel_tol * bn;
-    ctrl->rn = rn;
-    ctrl->max_iters = max_iters;
-    ctrl->breakdown = -1; ctrl->bkind = -1; ctrl->converged = 0; ctrl->done = 0;
-    ctrl->iterations = 0; ctrl->alpha = 0; ctrl->beta = 0; ctrl->rho = 0; ctrl->pap = 0;
-    res_norms[0] = rn;
-    if (!isfinite(rn)) {
-      ctrl->breakdown = 0; ctrl->bkind = 0; ctrl->done = 1;
-    } else if (rn <= ctrl->thr || max_iters == 0) {
-      ctrl->converged = rn <= ctrl->thr; ctrl->done = 1;
-    }
-  }
+  if (red_final<2>(acc, rs, site, tot) && threadIdx.x == 0) fin_start(ctrl, res_norms, tot, rel_tol, max_iters);
 }
 
 }  // namespace pu
@@ -399,7 +383,7 @@ __device__ __forceinline__ void pen4(const Grid& g, int i, int j0, const Q4<T>& 
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int j = j0 + k;
-    if (i < g.n - 1 && j < g.m) {
+    if (dn_ok(g, i) && j < g.m) {
       const T rv = ((ub.a[k] - u.a[k]) - gv.a[k]) - vv.a[k];
       pv += rv * rv;
     }
@@ -435,7 +419,7 @@ __global__ void __launch_bounds__(256, 3) k_weights_hpair_v(Grid g, const T* __r
   PU_FOR_CHUNKS(g, i, j0) {
     const long long o = (long long)i * ld + j0;
     const Q4<T> u = ldg4(x + o), vv = ldg4(x + o + P), vh = ldg4(x + o + 2 * P);
-    const Q4<T> ub = i < g.n - 1 ? ldg4(x + o + ld) : zero4<T>();
+    const Q4<T> ub = dn_ok(g, i) ? ldg4(x + o + ld) : zero4<T>();
     const T ur = ldg_or0(x + o + 4, j0 + 4 < g.m);
     const Q4<T> g1 = ldg4(gv + o), g2 = ldg4(gh + o);
     Q4<T> c1 = ones4<T>(), c2 = ones4<T>();
@@ -447,7 +431,7 @@ __global__ void __launch_bounds__(256, 3) k_weights_hpair_v(Grid g, const T* __r
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int j = j0 + k;
-      const bool okv = i < g.n - 1 && j < g.m, okh = j < g.m - 1;
+      const bool okv = dn_ok(g, i) && j < g.m, okh = j < g.m - 1;
       const T a = c1.a[k] * vv.a[k], b = c2.a[k] * vh.a[k];
       const T wa = sqrt(a * a + d2), wb = sqrt(b * b + d2);
       w1.a[k] = okv ? wa : (T)1;
@@ -469,11 +453,7 @@ __global__ void __launch_bounds__(256, 3) k_weights_hpair_v(Grid g, const T* __r
     pen4<T>(g, i, j0, u, ub, ur, vv, vh, g1, g2, acc[4], acc[5]);
   }
   double tot[6];
-  if (grid_reduce<6>(acc, rs, site, tot) && threadIdx.x == 0) {
-    const double pen = (tot[4] + tot[5]) / (2.0 * g.tau);
-    out[0] = (0.5 * tot[0] + 0.5 * tot[1]) + pen;
-    out[1] = (0.5 * tot[2] + 0.5 * tot[3]) + pen;
-  }
+  if (red_final<6>(acc, rs, site, tot) && threadIdx.x == 0) fin_hpair6(g, tot, out);
 }
 
 // H(xa, w), H(xb, w), mean u of the accepted one, acceptance flag
@@ -496,13 +476,13 @@ __global__ void __launch_bounds__(256, 3) k_hpair_states_v(Grid g, const T* __re
     for (int s = 0; s < 2; ++s) {
       const T* x = s ? xb : xa;
       const Q4<T> u = ldg4(x + o), vv = ldg4(x + o + P), vh = ldg4(x + o + 2 * P);
-      const Q4<T> ub = i < g.n - 1 ? ldg4(x + o + ld) : zero4<T>();
+      const Q4<T> ub = dn_ok(g, i) ? ldg4(x + o + ld) : zero4<T>();
       const T ur = ldg_or0(x + o + 4, j0 + 4 < g.m);
       T pv = (T)0, ph = (T)0, pu = (T)0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int j = j0 + k;
-        if (i < g.n - 1 && j < g.m) pv += slack4(c1.a[k], vv.a[k], w1.a[k], d2);
+        if (dn_ok(g, i) && j < g.m) pv += slack4(c1.a[k], vv.a[k], w1.a[k], d2);
         if (j < g.m - 1) ph += slack4(c2.a[k], vh.a[k], w2.a[k], d2);
         if (j < g.m) pu += u.a[k];
       }
@@ -513,15 +493,7 @@ __global__ void __launch_bounds__(256, 3) k_hpair_states_v(Grid g, const T* __re
     }
   }
   double tot[10];
-  if (grid_reduce<10>(acc, rs, site, tot) && threadIdx.x == 0) {
-    const double ha = (0.5 * tot[0] + 0.5 * tot[1]) + (tot[2] + tot[3]) / (2.0 * g.tau);
-    const double hb = (0.5 * tot[5] + 0.5 * tot[6]) + (tot[7] + tot[8]) / (2.0 * g.tau);
-    const bool take_a = ha <= hb;
-    out[0] = ha;
-    out[1] = hb;
-    out[2] = (take_a ? tot[4] : tot[9]) / ((double)g.n * (double)g.m);
-    out[3] = take_a ? 1.0 : 0.0;
-  }
+  if (red_final<10>(acc, rs, site, tot) && threadIdx.x == 0) fin_hpair_states(g, tot, out);
 }
 
 // cand = x - (1/L) grad H(x, w)   (objective.py:108-125)
@@ -536,7 +508,7 @@ __global__ void __launch_bounds__(256, 3) k_candidate_v(Grid g, const T* __restr
     const long long o = (long long)i * ld + j0;
     const Q4<T> u = ldg4(x + o), vv = ldg4(x + o + P), vh = ldg4(x + o + 2 * P);
     const Q4<T> g1 = ldg4(gv + o), g2 = ldg4(gh + o);
-    const bool hasb = i < g.n - 1, hasa = i > 0;
+    const bool hasb = dn_ok(g, i), hasa = up_ok(g, i);
     const Q4<T> ub = hasb ? ldg4(x + o + ld) : zero4<T>();
     const Q4<T> ua = hasa ? ldg4(x + o - ld) : zero4<T>();
     const Q4<T> va = hasa ? ldg4(x + o - ld + P) : zero4<T>();
@@ -588,7 +560,7 @@ __global__ void __launch_bounds__(256, 3) k_accept_v(Grid g, const T* __restrict
     const long long o = (long long)i * ld + j0;
     Q4<T> u = ldg4(x + o);
     const Q4<T> vv = ldg4(x + o + P), vh = ldg4(x + o + 2 * P);
-    Q4<T> ub = i < g.n - 1 ? ldg4(x + o + ld) : zero4<T>();
+    Q4<T> ub = dn_ok(g, i) ? ldg4(x + o + ld) : zero4<T>();
     T ur = ldg_or0(x + o + 4, j0 + 4 < g.m);
     const Q4<T> c1 = ldg4(cv + o), c2 = ldg4(ch + o), g1 = ldg4(gv + o), g2 = ldg4(gh + o);
     const Q4<T> w1 = ldg4(wv + o), w2 = ldg4(wh + o);
@@ -598,7 +570,7 @@ __global__ void __launch_bounds__(256, 3) k_accept_v(Grid g, const T* __restrict
       const int j = j0 + k;
       u.a[k] = (j < g.m) ? u.a[k] - mean : (T)0;
       ub.a[k] = ub.a[k] - mean;
-      if (i < g.n - 1 && j < g.m) pv += slack4(c1.a[k], vv.a[k], w1.a[k], d2);
+      if (dn_ok(g, i) && j < g.m) pv += slack4(c1.a[k], vv.a[k], w1.a[k], d2);
       if (j < g.m - 1) ph += slack4(c2.a[k], vh.a[k], w2.a[k], d2);
     }
     acc[0] += (double)pv;
@@ -635,7 +607,7 @@ __global__ void __launch_bounds__(256, 3) k_accept_weights_v(Grid g, const T* __
     const long long o = (long long)i * ld + j0;
     Q4<T> u = ldg4(x + o);
     const Q4<T> vv = ldg4(x + o + P), vh = ldg4(x + o + 2 * P);
-    Q4<T> ub = i < g.n - 1 ? ldg4(x + o + ld) : zero4<T>();
+    Q4<T> ub = dn_ok(g, i) ? ldg4(x + o + ld) : zero4<T>();
     T ur = ldg_or0(x + o + 4, j0 + 4 < g.m);
     const Q4<T> g1 = ldg4(gv + o), g2 = ldg4(gh + o);
     Q4<T> c1 = ones4<T>(), c2 = ones4<T>();
@@ -646,7 +618,7 @@ __global__ void __launch_bounds__(256, 3) k_accept_weights_v(Grid g, const T* __
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int j = j0 + k;
-      const bool okv = i < g.n - 1 && j < g.m, okh = j < g.m - 1;
+      const bool okv = dn_ok(g, i) && j < g.m, okh = j < g.m - 1;
       u.a[k] = (j < g.m) ? u.a[k] - mean : (T)0;
       ub.a[k] = ub.a[k] - mean;
       const T a = c1.a[k] * vv.a[k], bb = c2.a[k] * vh.a[k];
@@ -672,11 +644,7 @@ __global__ void __launch_bounds__(256, 3) k_accept_weights_v(Grid g, const T* __
     st4(wnv + o, w1); st4(wnh + o, w2); st4(dv + o, e1); st4(dh + o, e2);
   }
   double tot[6];
-  if (grid_reduce<6>(acc, rs, site, tot) && threadIdx.x == 0) {
-    const double pen = (tot[4] + tot[5]) / (2.0 * g.tau);
-    out[0] = (0.5 * tot[0] + 0.5 * tot[1]) + pen;
-    out[1] = (0.5 * tot[2] + 0.5 * tot[3]) + pen;
-  }
+  if (red_final<6>(acc, rs, site, tot) && threadIdx.x == 0) fin_hpair6(g, tot, out);
 }
 
 }  // namespace pu

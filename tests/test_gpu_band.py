@@ -1,0 +1,84 @@
+"""Row-sharded unwrap (band.py) on one GPU through the loopback communicator:
+the band decomposition (ghost rows, cross-band reductions + finalisers, the
+packed DCT transpose) must reproduce the single-grid solve and the reference.
+The multi-process collective plumbing is covered by test_band_comm_gloo.py."""
+
+import numpy as np
+import pytest
+
+from oracle import phaseirls_port as port
+from cases import GOLDEN_UNWRAP_CASES, case_inputs, golden_trace, rel
+
+pytestmark = pytest.mark.gpu
+
+pu = pytest.importorskip("paper_2401_09961_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _scene(n, m, noise=0.7, seed=5):
+    spec = pu.SceneSpec("gaussian-bumps", n, m, 12.0, 6.0, seed)
+    return pu.add_phase_noise(pu.wrap_scene(pu.generate_scene(spec)), noise, 100 + seed)
+
+
+@pytest.mark.parametrize("shape,bands", [((64, 48), 2), ((50, 45), 3), ((37, 64), 4), ((96, 80), 5),
+                                         ((40, 33), 1)])
+def test_bands_match_single_grid_fp64(shape, bands):
+    x = _scene(*shape)
+    single = pu.unwrap(x, dtype="fp64")
+    res = pu.unwrap_rows(x, dtype="fp64", bands=bands)
+    assert [r.cg_iters for r in res.trace.records] == [r.cg_iters for r in single.trace.records]
+    assert [r.m_cg for r in res.trace.records] == [r.m_cg for r in single.trace.records]
+    np.testing.assert_allclose([r.h_delta for r in res.trace.records], [r.h_delta for r in single.trace.records],
+                               rtol=1e-9)
+    assert res.u.shape == single.u.shape and res.vv.shape == single.vv.shape and res.vh.shape == single.vh.shape
+    assert rel(res.u, single.u) <= 1e-9
+    assert rel(res.vv, single.vv) <= 1e-8
+
+
+@pytest.mark.parametrize("name", ["noisy64", "noisy96x80", "weighted40x36", "lo0_noisy48"])
+def test_bands_match_reference(golden_unwrap, golden_meta, name):
+    """north_star fp64 bar on the sharded path: u within 1e-8 of the reference's."""
+    if name not in GOLDEN_UNWRAP_CASES:
+        pytest.skip(f"{name} not in the golden set")
+    x, cv, ch, tau, delta, prm, lo = case_inputs(golden_unwrap, golden_meta, name)
+    c = None if cv is None else pu.WeightField(cv, ch)
+    res = pu.unwrap_rows(x, c, pu.ModelParams(tau, delta), pu.IrlsParams(**prm.__dict__), lo, dtype="fp64",
+                         bands=3)
+    want = golden_trace(golden_unwrap, name)
+    assert [r.cg_iters for r in res.trace.records] == want["cg_iters"].tolist()
+    u_ref = golden_unwrap[f"{name}/u"]
+    assert rel(res.u, u_ref) <= 1e-8 or np.max(np.abs(res.u - u_ref)) <= 1e-12
+
+
+def test_bands_fp32_objective():
+    x = _scene(128, 96, noise=0.9, seed=7)
+    ref_state, _, (gv, gh) = port.unwrap(x, poisson="dct")
+    res = pu.unwrap_rows(x, dtype="fp32", bands=4)
+    ones = (np.ones_like(gv), np.ones_like(gh))
+    f_ref = port.f_l1(ref_state, gv, gh, *ones, 1e-2)
+    f32 = port.f_l1(port.Triple(res.u, res.vv, res.vh), gv, gh, *ones, 1e-2)
+    assert abs(f32 - f_ref) <= max(1e-3 * f_ref, 1e-6)
+
+
+def test_band_pcg_long_budget_reprojection():
+    """Budgets past 50 iterations exercise the all-reduced mean re-projection."""
+    x = _scene(72, 64, noise=1.0, seed=9)
+    prm = pu.IrlsParams(max_iter_cg_start=60, cg_rel_tol=1e-14, max_outer_iters=3)
+    single = pu.unwrap(x, params=prm, dtype="fp64")
+    res = pu.unwrap_rows(x, params=prm, dtype="fp64", bands=3)
+    assert [r.cg_iters for r in res.trace.records] == [r.cg_iters for r in single.trace.records]
+    assert max(r.cg_iters for r in res.trace.records) > 50
+    assert rel(res.u, single.u) <= 1e-9
+
+
+def test_band_layout_errors():
+    with pytest.raises(ValueError):
+        pu.band.BandLayout(3, 8, 4)
+    with pytest.raises(ValueError):
+        pu.band.BandLayout(64, 8, 4)  # 8 columns cannot give 4 blocks of >= 8
