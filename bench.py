@@ -265,6 +265,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="only run N unwraps (for ncu launch lists); prints no JSON")
+    ap.add_argument("--shard", choices=("auto", "images", "rows"), default="auto",
+                    help="N>1: independent images per rank, or one image row-sharded over the ranks "
+                         "(auto: rows for c4, images otherwise)")
     ap.add_argument("--warmup-ref", type=int, default=1)
     ap.add_argument("--steps-ref", type=int, default=2)
     args = ap.parse_args()
@@ -287,6 +290,14 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     lib = _native.ensure()
+    shard = args.shard if args.shard != "auto" else ("rows" if args.config == "c4" and world > 1 else "images")
+    if shard == "rows":
+        if args.config == "c5":
+            raise SystemExit("--shard rows needs a single-image config (c1-c4)")
+        rc = main_rows(args, rank, local_rank, world, dev, lib)
+        if world > 1:
+            dist.destroy_process_group()
+        return rc
 
     # this rank's images: one C1-C3 image per rank, or its shard of the 64 C5 images
     if args.config == "c5":
@@ -464,6 +475,129 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def kernel_stats(kinds, ms, names):
+    per_kind = {}
+    for kd in np.unique(kinds):
+        sel = ms[kinds == kd]
+        ran = sel[sel >= 0.25 * np.median(sel)] if sel.size else sel
+        name = names[kd] if kd < len(names) else str(kd)
+        per_kind[name] = {"launches": int(sel.size), "ran": int(ran.size), "total_ms": float(ran.sum()),
+                          "avg_ms": float(ran.mean()) if ran.size else 0.0}
+    return per_kind
+
+
+def main_rows(args, rank, local_rank, world, dev, lib):
+    """One image row-sharded over the ranks (band.py): halo exchange, all-reduced
+    PCG scalars and the all-to-all DCT transpose between the band kernels.
+    value = the image's pixels / the max-over-ranks unwrap time (strong scaling)."""
+    import torch
+    import paper_2401_09961_b200 as pu
+    from paper_2401_09961_b200.band import RowSharded
+    from paper_2401_09961_b200.batch import max_over_ranks
+    from paper_2401_09961_b200.device import Workspace
+
+    _, x = pu.config_scene(args.config)
+    n, m = x.shape
+    model, params = pu.ModelParams(), pu.IrlsParams()
+    solver = RowSharded.get(n, m, args.dtype, model, dev)
+    lay = solver.layout
+    xs = solver.upload(x)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        trace = solver.run(xs, None, params, -np.pi)
+    torch.cuda.synchronize()
+    launches0 = lib.pu_launch_count()
+    with ClockSampler(local_rank) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            trace = solver.run(xs, None, params, -np.pi)
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+    launches = lib.pu_launch_count() - launches0
+    step_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, device=dev)
+    value = n * m / (step_ms / 1e3) / 1e6
+
+    # instrumented pass on this rank's band (CUDA events around each launch)
+    b = solver.bands[0]
+    lib.pu_timing_enable(b.h, 1)
+    kinds = np.zeros(0, dtype=np.int32)
+    barrier()
+    for _ in range(args.steps):
+        solver.run(xs, None, params, -np.pi)
+    torch.cuda.synchronize()
+    import ctypes
+    cap = 1 << 18
+    kb, ib, mb_ = (ctypes.c_int * cap)(), (ctypes.c_int * cap)(), (ctypes.c_float * cap)()
+    cnt = int(lib.pu_timing_read(b.h, kb, ib, mb_, cap))
+    lib.pu_timing_enable(b.h, 0)
+    kinds = np.frombuffer(kb, dtype=np.int32, count=cnt).copy()
+    ms = np.frombuffer(mb_, dtype=np.float32, count=cnt).astype(np.float64)
+    barrier()
+    per_kind = kernel_stats(kinds, ms, Workspace.TIME_KINDS)
+    e = 4 if args.dtype == "fp32" else 8
+    rows = lay.rows[rank]
+    alg = algorithmic_bytes(rows, m, e)
+    hbm, peak_kind = peaks()
+    n_pcg = sum(r.cg_iters for r in trace.records)
+    iter_kinds = ("K1_p_Ap_pAp", "K2a_update_norms", "K2b_row_dct", "K3_coldct_spectral", "K4_row_idct",
+                  "reproject_update")
+    iter_ms = sum(per_kind[k]["total_ms"] for k in iter_kinds if k in per_kind) / max(1, args.steps * n_pcg)
+    dom = max((k for k in per_kind if k in alg), key=lambda k: per_kind[k]["total_ms"])
+    achieved = alg[dom] / (per_kind[dom]["avg_ms"] / 1e3) / 1e9 if per_kind[dom]["avg_ms"] > 0 else None
+    roofline = {
+        "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+        "frac": achieved / hbm if achieved else None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+        "bytes_per_launch": alg[dom], "avg_launch_ms": per_kind[dom]["avg_ms"], "traffic": None,
+        "scope": f"rank 0's band ({rows} x {m}); collectives excluded",
+        "pcg_iteration": {"bytes": alg["iteration"], "kernel_ms": iter_ms,
+                          "frac": (alg["iteration"] / (iter_ms / 1e3) / 1e9) / hbm if iter_ms else None,
+                          "ms_from_step": step_ms / max(1, n_pcg),
+                          "how": "kernel_ms: rank 0's band kernels only; ms_from_step: whole step / PCG iterations "
+                                 "(includes outer work and all exchanges)"},
+    }
+    # end to end through the public API: host grid in, this rank's band rows out
+    e2e_ms = []
+    for i in range(args.steps + 1):
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = pu.unwrap_rows(x, dtype=args.dtype, gather=False)
+        t1 = time.perf_counter()
+        if i > 0:
+            e2e_ms.append((t1 - t0) * 1e3)
+    e2e_step = max_over_ranks(statistics.mean(e2e_ms), device=dev)
+    h2d = (n + world - 1) * m * 8
+    d2h = (n * m + (n - 1) * m + n * (m - 1)) * 8
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {WORKLOAD[args.config]}", "n": n, "m": m,
+                       "sharding": f"one image row-sharded over {world} rank(s): bands {lay.rows}, "
+                                   f"transpose blocks of {lay.mb} columns",
+                       "l2": "inputs larger than L2", "plan": None},
+            "unwrap_s": step_ms / 1e3, "pcg_iters_per_step": n_pcg, "outer_iters_per_step": len(trace.records),
+            "pcg_iters_per_s": n_pcg / (step_ms / 1e3),
+            "roofline": roofline, "kernels": per_kind, "cpu_baseline": None,
+            "e2e": {"value": n * m / (e2e_step / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step},
+            "clocks": clocks.summary(), "gpu_launches": int(launches),
+        }
+        print(json.dumps(line), flush=True)
+    del res
     return 0
 
 

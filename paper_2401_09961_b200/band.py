@@ -487,17 +487,85 @@ def _validate_device(x_dev):
         raise ValueError("wrapped phase values must lie in [0, 2*pi)")
 
 
+class RowSharded:
+    """Band states, communicator and driver for one (N, M, dtype, tau, delta)
+    on this process's device; reused across unwraps (see `get`)."""
+
+    _cache: dict = {}
+
+    @classmethod
+    def get(cls, n, m, dtype, model: ModelParams, device, bands=None, group=None):
+        import torch.distributed as dist
+        distributed = bands is None and dist.is_available() and dist.is_initialized()
+        key = (n, m, dtype, float(model.tau), float(model.delta), str(device), bands, id(group) if distributed else None,
+               distributed)
+        obj = cls._cache.get(key)
+        if obj is None:
+            obj = cls(n, m, dtype, model, device, bands, group)
+            cls._cache[key] = obj
+        return obj
+
+    def __init__(self, n, m, dtype, model: ModelParams, device, bands=None, group=None):
+        import torch.distributed as dist
+        torch = _torch()
+        nat.ensure()
+        self.distributed = bands is None and dist.is_available() and dist.is_initialized()
+        self.group = group
+        world = dist.get_world_size(group) if self.distributed else int(bands or 1)
+        self.layout = BandLayout(n, m, world)
+        if self.distributed:
+            self.comm, self.ranks = DistComm(group), [dist.get_rank(group)]
+        else:
+            self.comm, self.ranks = LoopbackComm(world), list(range(world))
+        self.device = torch.device(device)
+        self.model = model
+        with torch.cuda.device(self.device):
+            self.bands = [BandState(self.layout, r, dtype, model.tau, model.delta, self.device) for r in self.ranks]
+            self.stream = torch.cuda.Stream(device=self.device)
+        self.driver = BandUnwrap(self.bands, self.comm)
+
+    def rows_of(self, r):
+        """Rows of x band r reads: its own and the first row of the band below."""
+        lay = self.layout
+        return lay.row0[r], min(lay.n, lay.row0[r] + lay.rows[r] + 1)
+
+    def upload(self, x):
+        """This process's rows of a full host (numpy / CPU tensor) or device grid -> device fp64 tensors."""
+        torch = _torch()
+        xs = []
+        for r in self.ranks:
+            lo, hi = self.rows_of(r)
+            sl = torch.as_tensor(np.ascontiguousarray(x[lo:hi])) if isinstance(x, np.ndarray) else x[lo:hi]
+            xs.append(sl.to(device=self.device, dtype=torch.float64, non_blocking=True).contiguous())
+        return xs
+
+    def run(self, xs, c, params: IrlsParams, gradient_lo):
+        """The full IRLS loop on the uploaded rows; returns the trace (results stay on the device)."""
+        torch = _torch()
+        s = self.stream
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.driver.load(xs, c, gradient_lo)
+            trace = run_loop(self.driver, c, self.model, params)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        return trace
+
+    def band_parts(self):
+        return [self.driver.band_arrays(b) for b in self.bands]
+
+
 def unwrap_rows(x, c: WeightField | None = None, model: ModelParams | None = None, params: IrlsParams | None = None,
                 gradient_lo=-np.pi, *, dtype="fp64", bands=None, group=None, gather=True, device=None):
     """irls.py:132-224 on a row-sharded grid.
 
     Inside a torch.distributed job (and `bands` None) every rank passes the same
-    full grid `x` and solves its own row band, exchanging halos, reduction
-    totals and the DCT transpose with the others (`group`, default world).
-    Otherwise `bands` = B > 1 runs all B bands in this process on one device
+    full grid `x` (host array, or a tensor) and solves its own row band; only
+    that band's rows (+1) are copied to its GPU.  The ranks exchange halos,
+    reduction totals and the DCT transpose over `group` (default: world).
+    Otherwise `bands` = B runs all B bands in this process on one device
     (loopback collectives) — the same decomposition, for testing.
     Returns an UnwrapResult with the full grid on every rank when `gather`,
-    else the rank's band arrays (u, vv, vh rows of its band) and the trace.
+    else the rank's own band rows (u, vv, vh) and the trace.
     """
     nat.ensure()
     torch = _torch()
@@ -509,36 +577,16 @@ def unwrap_rows(x, c: WeightField | None = None, model: ModelParams | None = Non
         raise ValueError(f"phase grid must be 2-D and non-empty, got shape {tuple(arr.shape)}")
     n, m = int(arr.shape[0]), int(arr.shape[1])
     _check_inputs(arr, c, n, m, gradient_lo)
-    import torch.distributed as dist
-    distributed = bands is None and dist.is_available() and dist.is_initialized()
-    world = dist.get_world_size(group) if distributed else int(bands or 1)
-    lay = BandLayout(n, m, world)
-    if distributed:
-        rank = dist.get_rank(group)
-        comm, ranks = DistComm(group), [rank]
-    else:
-        comm, ranks = LoopbackComm(world), list(range(world))
     with torch.cuda.device(dev):
-        xs = []
-        for r in ranks:  # only the rows a band needs travel to the device
-            r0, rows = lay.row0[r], lay.rows[r]
-            hi = min(n, r0 + rows + 1)
-            sl = torch.as_tensor(np.ascontiguousarray(arr[r0:hi])) if isinstance(arr, np.ndarray) else arr[r0:hi]
-            xs.append(sl.to(device=dev, dtype=torch.float64).contiguous())
+        solver = RowSharded.get(n, m, dtype, model, dev, bands, group)
+        xs = solver.upload(arr)
         for xr in xs:
             _validate_device(xr)
-        band_states = [BandState(lay, r, dtype, model.tau, model.delta, dev) for r in ranks]
-        driver = BandUnwrap(band_states, comm)
-        s = torch.cuda.Stream(device=dev)
-        s.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(s):
-            driver.load(xs, c, gradient_lo)
-            trace = run_loop(driver, c, model, params)
-            parts = [driver.band_arrays(b) for b in band_states]
-        torch.cuda.current_stream(dev).wait_stream(s)
-        if distributed and gather:
-            parts = _gather_bands(parts[0], lay, group)
-        if gather or not distributed:
+        trace = solver.run(xs, c, params, gradient_lo)
+        parts = solver.band_parts()
+        if solver.distributed and gather:
+            parts = _gather_bands(parts[0], solver.layout, group)
+        if gather or not solver.distributed:
             u = torch.cat([p[0] for p in parts]).cpu().numpy()
             vv = torch.cat([p[1] for p in parts]).cpu().numpy()
             vh = torch.cat([p[2] for p in parts]).cpu().numpy()
