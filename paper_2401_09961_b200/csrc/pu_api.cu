@@ -370,6 +370,17 @@ struct Impl : HandleBase {
     g.n_glob = n_glob;
     g.top = band && b->row0 > 0;
     g.bot = band && b->row0 + b->rows < n_glob;
+    {
+      // bound of fin_k2: rho_u <= tau ||r||^2 / lambda_min (orthonormal DCT) and
+      // the unnormalised transforms grow values by at most N M; keep 16x margin
+      auto lam1 = [](int len) { const double s = std::sin(3.141592653589793 / (2.0 * len)); return 4.0 * s * s; };
+      double lam_min = INFINITY;
+      if (n_glob > 1) lam_min = std::min(lam_min, lam1(n_glob));
+      if (m > 1) lam_min = std::min(lam_min, lam1(m));
+      const double tmax = sizeof(T) == 4 ? 3.4028234663852886e38 : 1.7976931348623157e308;
+      const double grow = 16.0 * (double)n_glob * (double)m * (std::isfinite(lam_min) ? tau / lam_min + 1.0 : 1.0);
+      g.tail_rn2_max = tmax / grow;
+    }
     gc = g;
     if (band) {
       gc.n = n_glob; gc.m = b->cols; gc.ld = b->mb; gc.plane = (long long)n_glob * b->mb;

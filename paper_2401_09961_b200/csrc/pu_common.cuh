@@ -28,6 +28,9 @@ struct Grid {
   int n_glob;
   int top;
   int bot;
+  // largest ||r||^2 for which the preconditioned product r.z of the PCG tail
+  // is provably finite in T (see fin_k2); set by the host
+  double tail_rn2_max;
 };
 
 // vertical neighbours of row i within the global grid (ghost rows count)

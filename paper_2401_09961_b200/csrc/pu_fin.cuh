@@ -62,8 +62,16 @@ __device__ __forceinline__ void fin_k1(PcgCtrl* ctrl, const double* tot, int it)
   }
 }
 
-// pcg.py:94-100 (+ rho_s of preconditioner.py:115): ||r|| exits
-__device__ __forceinline__ void fin_k2(PcgCtrl* ctrl, double* res_norms, const double* tot, int it, int mode) {
+// pcg.py:94-100 (+ rho_s of preconditioner.py:115): ||r|| exits.
+// On the last iteration of the budget the reference still forms z = M r and
+// rho (pcg.py:101-108) only to check rho for a NumericalBreakdown; z and p are
+// then discarded.  When rho_s is finite and ||r||^2 is below the bound for
+// which rho_u = <r_hat, tau r_hat / lambda> and every transform intermediate
+// provably stay finite in T (g.tail_rn2_max, set by the host), that check
+// cannot fire, so the loop ends here and the transforms of the tail are
+// skipped.  Otherwise they run and K3 performs the check.
+__device__ __forceinline__ void fin_k2(const Grid& g, PcgCtrl* ctrl, double* res_norms, const double* tot, int it,
+                                       int mode) {
   ctrl->rho_s = tot[1];
   if (mode == MODE_ITER) {
     const double rn = sqrt(tot[0]);
@@ -73,7 +81,11 @@ __device__ __forceinline__ void fin_k2(PcgCtrl* ctrl, double* res_norms, const d
     } else {
       res_norms[it + 1] = rn;
       ctrl->iterations = it + 1;
-      if (rn <= ctrl->thr) { ctrl->converged = 1; ctrl->done = 1; }
+      if (rn <= ctrl->thr) {
+        ctrl->converged = 1; ctrl->done = 1;
+      } else if (it + 1 == ctrl->max_iters && isfinite(tot[1]) && tot[0] <= g.tail_rn2_max) {
+        ctrl->done = 1;  // budget exhausted, rho provably finite: nothing left to compute
+      }
     }
   }
 }
@@ -141,7 +153,7 @@ static __global__ void k_finalize(Grid g, const double* __restrict__ tot, unsign
     if (mask & (1u << S_K1)) fin_k1(a.ctrl, T_(S_K1), a.it);
     if (a.ctrl->done) return;
     if (mask & (1u << S_UPD)) fin_upd(g, a.ctrl, T_(S_UPD));
-    if (mask & (1u << S_K2)) fin_k2(a.ctrl, a.res_norms, T_(S_K2), a.it, a.mode);
+    if (mask & (1u << S_K2)) fin_k2(g, a.ctrl, a.res_norms, T_(S_K2), a.it, a.mode);
     if (a.ctrl->done) return;
     if (mask & (1u << S_K3)) fin_k3(a.ctrl, T_(S_K3), a.it, a.mode);
   }

@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(256, 3) k_pcg_r_v(Grid g, const T* __restrict_
     acc[1] += (double)prz;
   }
   double tot[2];
-  if (red_final<2>(acc, rs, site, tot) && threadIdx.x == 0) fin_k2(ctrl, res_norms, tot, it, MODE);
+  if (red_final<2>(acc, rs, site, tot) && threadIdx.x == 0) fin_k2(g, ctrl, res_norms, tot, it, MODE);
 }
 
 // update + sum(r_u) for the every-50 re-projection (the mean is subtracted by
