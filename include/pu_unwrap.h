@@ -175,6 +175,20 @@ int pu_pcg_solve(pu_handle* h, const void* b, const void* x0, void* x, const voi
                  void* r, void* z, void* p0, void* p1, void* spec, int max_iters, double rel_tol,
                  void* ctrl, double* res_norms, void* stream);
 
+/* Harness metrics on the device (whole-grid handles), against compact or
+ * pitched fp64 device grids (row pitch ldx / ldr elements):
+ *  pu_shift_error    phase.py:152-175: out[0] alpha = mean(x_u - u),
+ *                    out[1] max |err|, out[2] rmse, out[3] congruent fraction
+ *                    (|err / 2pi - rint| <= 1e-3), err = x_u - (u + alpha);
+ *  pu_kmap_mismatch  SURVEY §8(d): mean(rint((u - x)/2pi) != rint((u_ref - x)/2pi));
+ *  pu_congruent_round phase.py:178-184: out (compact N x M fp64) =
+ *                    x + 2pi rint((u - x)/2pi).
+ * u is the u plane of a system vector (handle dtype). */
+int pu_shift_error(pu_handle* h, const void* u, const double* xu, int64_t ldx, double* out, void* stream);
+int pu_kmap_mismatch(pu_handle* h, const void* u, const double* uref, int64_t ldr, const double* x, int64_t ldx,
+                     double* out, void* stream);
+int pu_congruent_round(pu_handle* h, const void* u, const double* x, int64_t ldx, double* out, void* stream);
+
 /* Per-launch CUDA-event timing on the launching stream (off by default).
  * pu_timing_read synchronises on the recorded events and returns the number
  * of records (kind, iteration, milliseconds) written, up to cap; kinds:
@@ -214,7 +228,7 @@ typedef struct pu_band {
 } pu_band;
 
 enum pu_site { PU_SITE_WH = 1, PU_SITE_HPAIR = 3, PU_SITE_ACC = 4, PU_SITE_START = 6, PU_SITE_K1 = 7,
-               PU_SITE_K2 = 8, PU_SITE_K3 = 9, PU_SITE_UPD = 10, PU_NSITES = 12 };
+               PU_SITE_K2 = 8, PU_SITE_K3 = 9, PU_SITE_UPD = 10, PU_SITE_MET = 12, PU_NSITES = 13 };
 #define PU_MAX_SUMS_ABI 12
 
 int pu_create_band(pu_handle** out, int m, const pu_band* band, int dtype, double tau, double delta);

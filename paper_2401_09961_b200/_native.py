@@ -52,6 +52,9 @@ SIGNATURES = {
     "pu_set_graphs": (_i, [_vp, _i]),
     "pu_timing_enable": (_i, [_vp, _i]),
     "pu_timing_read": (_i, [_vp, _vp, _vp, _vp, _i]),
+    "pu_shift_error": (_i, [_vp, _vp, _vp, _i64, _vp, _vp]),
+    "pu_kmap_mismatch": (_i, [_vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp]),
+    "pu_congruent_round": (_i, [_vp, _vp, _vp, _i64, _vp, _vp]),
     # row-sharded grids (band.py)
     "pu_create_band": (_i, [ctypes.POINTER(_vp), _i, _vp, _i, _d, _d]),
     "pu_set_band_totals": (_i, [_vp, _vp]),
@@ -73,7 +76,7 @@ class PuBand(ctypes.Structure):
 
 # reduction sites (enum pu_site) and the totals row length
 SITE_WH, SITE_HPAIR, SITE_ACC, SITE_START, SITE_K1, SITE_K2, SITE_K3, SITE_UPD = 1, 3, 4, 6, 7, 8, 9, 10
-NSITES, MAX_SUMS = 12, 12
+NSITES, MAX_SUMS = 13, 12
 
 _lib = None
 

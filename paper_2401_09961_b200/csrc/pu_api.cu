@@ -855,6 +855,35 @@ int pu_eval_f(pu_handle* h, const void* x, const void* gv, const void* gh, const
   return PU_OK;
 }
 
+int pu_shift_error(pu_handle* h, const void* u, const double* xu, int64_t ldx, double* out, void* stream) {
+  PU_DISPATCH(h, {
+    if (I.band) return fail(PU_ERR_ARG, "metrics need a whole-grid handle");
+    k_shift_alpha<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(u), xu, ldx, I.rs, S_MET, out);
+    PU_LAUNCH_CHECK();
+    k_shift_stats<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(u), xu, ldx, I.rs, S_MET, out);
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
+int pu_kmap_mismatch(pu_handle* h, const void* u, const double* uref, int64_t ldr, const double* x, int64_t ldx,
+                     double* out, void* stream) {
+  PU_DISPATCH(h, {
+    if (I.band) return fail(PU_ERR_ARG, "metrics need a whole-grid handle");
+    k_kmap<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(u), uref, ldr, x, ldx, I.rs, S_MET, out);
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
+int pu_congruent_round(pu_handle* h, const void* u, const double* x, int64_t ldx, double* out, void* stream) {
+  PU_DISPATCH(h, {
+    k_congruent<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(u), x, ldx, out);
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
 int pu_candidate_step(pu_handle* h, const void* x, const void* wv, const void* wh, const void* gv, const void* gh,
                       const void* cv, const void* ch, double lipschitz, void* out, void* stream) {
   if (!(lipschitz > 0)) return fail(PU_ERR_ARG, "lipschitz constant must be positive");

@@ -392,6 +392,76 @@ __global__ void k_accept(Grid g, const T* __restrict__ xa, const T* __restrict__
     out[0] = (0.5 * tot[0] + 0.5 * tot[1]) + (tot[2] + tot[3]) / (2.0 * g.tau);
 }
 
+// ---------------------------------------------------------------------------
+// Harness metrics on the device (phase.py:152-184; SURVEY §8(d) parity
+// metrics), against fp64 grids with row pitch ldx, so large results need no
+// device-to-host copy.
+// ---------------------------------------------------------------------------
+// shift_error pass 1: alpha = mean(x_u - u); clears the max slot
+template <typename T>
+__global__ void k_shift_alpha(Grid g, const T* __restrict__ u, const double* __restrict__ xu, long long ldx,
+                              RedScratch rs, int site, double* out) {
+  double acc[1] = {0.0};
+  PU_FOR_CELLS(g, i, j) acc[0] += xu[(long long)i * ldx + j] - (double)u[(long long)i * g.ld + j];
+  double tot[1];
+  if (grid_reduce<1>(acc, rs, site, tot) && threadIdx.x == 0) {
+    out[0] = tot[0] / ((double)g.n * (double)g.m);
+    out[1] = 0.0;
+  }
+}
+
+// shift_error pass 2: err = x_u - (u + alpha); out[1] = max |err|, out[2] =
+// rmse, out[3] = fraction of cells within 1e-3 cycles of a multiple of 2 pi
+template <typename T>
+__global__ void k_shift_stats(Grid g, const T* __restrict__ u, const double* __restrict__ xu, long long ldx,
+                              RedScratch rs, int site, double* out) {
+  const double alpha = out[0];
+  double acc[2] = {0.0, 0.0};
+  double mx = 0.0;
+  PU_FOR_CELLS(g, i, j) {
+    const double err = xu[(long long)i * ldx + j] - ((double)u[(long long)i * g.ld + j] + alpha);
+    const double cyc = err / PU_TWO_PI;
+    acc[0] += err * err;
+    acc[1] += fabs(cyc - rint(cyc)) <= 1e-3 ? 1.0 : 0.0;
+    mx = fmax(mx, fabs(err));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  // non-negative doubles order like their bit patterns: an integer max is exact
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(out + 1), (unsigned long long)__double_as_longlong(mx));
+  double tot[2];
+  if (grid_reduce<2>(acc, rs, site, tot) && threadIdx.x == 0) {
+    const double cells = (double)g.n * (double)g.m;
+    out[2] = sqrt(tot[0] / cells);
+    out[3] = tot[1] / cells;
+  }
+}
+
+// K-map mismatch fraction: mean(rint((u - x)/2pi) != rint((u_ref - x)/2pi))
+template <typename T>
+__global__ void k_kmap(Grid g, const T* __restrict__ u, const double* __restrict__ uref, long long ldr,
+                       const double* __restrict__ x, long long ldx, RedScratch rs, int site, double* out) {
+  double acc[1] = {0.0};
+  PU_FOR_CELLS(g, i, j) {
+    const double xi = x[(long long)i * ldx + j];
+    const double ka = rint(((double)u[(long long)i * g.ld + j] - xi) / PU_TWO_PI);
+    const double kb = rint((uref[(long long)i * ldr + j] - xi) / PU_TWO_PI);
+    acc[0] += ka != kb ? 1.0 : 0.0;
+  }
+  double tot[1];
+  if (grid_reduce<1>(acc, rs, site, tot) && threadIdx.x == 0) out[0] = tot[0] / ((double)g.n * (double)g.m);
+}
+
+// congruent_round: out = x + 2pi rint((u - x)/2pi), compact fp64 (pitch m)
+template <typename T>
+__global__ void k_congruent(Grid g, const T* __restrict__ u, const double* __restrict__ x, long long ldx,
+                            double* __restrict__ out) {
+  PU_FOR_CELLS(g, i, j) {
+    const double xi = x[(long long)i * ldx + j];
+    out[(long long)i * g.m + j] = xi + PU_TWO_PI * rint(((double)u[(long long)i * g.ld + j] - xi) / PU_TWO_PI);
+  }
+}
+
 // F = sum |c v| + penalties (objective.py:63-66); out[1] = l1 part.
 template <typename T>
 __global__ void k_eval_f(Grid g, const T* __restrict__ x, const T* __restrict__ gv, const T* __restrict__ gh,
