@@ -157,7 +157,7 @@ def dist_env():
 # ---------------------------------------------------------------------------
 # reference CPU path (the oracle port of the reference algorithm)
 # ---------------------------------------------------------------------------
-def cpu_reference_sample(x, n_outer, n_pcg, pcg_reps=2):
+def cpu_reference_sample(x, n_outer, n_pcg, pcg_reps=2, poisson="dense"):
     """Time the reference algorithm (oracle/phaseirls_port.py, dense-eigenbasis
     preconditioner exactly as preconditioner.py:64-100) on the host cores:
     the once-per-unwrap setup, `pcg_reps` PCG iterations and one outer
@@ -168,7 +168,7 @@ def cpu_reference_sample(x, n_outer, n_pcg, pcg_reps=2):
     t0 = time.perf_counter()
     gv, gh = port.grad_wrapped(x)
     b = port.rhs(gv, gh, tau)
-    solver = port.make_poisson(n, m, "dense")                 # 2 x LAPACK eigh (preconditioner.py:77-83)
+    solver = port.make_poisson(n, m, poisson)                 # dense: 2 x LAPACK eigh (preconditioner.py:77-83)
     t_setup = time.perf_counter() - t0
     cv, ch = np.ones_like(gv), np.ones_like(gh)
     state = port.Triple(np.zeros((n, m)), -gv.copy(), -gh.copy())
@@ -198,8 +198,11 @@ def cpu_reference_sample(x, n_outer, n_pcg, pcg_reps=2):
         "seconds": total, "t_setup_s": t_setup, "t_outer_s": t_outer, "t_pcg_start_s": t_start,
         "t_pcg_iter_s": t_iter, "n_outer": n_outer, "n_pcg": n_pcg,
         "mpix_s": n * m / total / 1e6, "pcg_it_s": n_pcg / total,
-        "sample": (f"reference algorithm (oracle port, dense LAPACK eigenbasis preconditioner) on the full {n}x{m} "
-                   f"input: setup + {pcg_reps} PCG iterations + 1 outer iteration timed "
+        "sample": (f"reference algorithm (oracle port, "
+                   + ("dense LAPACK eigenbasis preconditioner" if poisson == "dense" else
+                      "preconditioner restated as scipy DCT-II/III with all host threads (the 'fast CPU restatement' "
+                      "of SURVEY §8(d), not the reference's own path)")
+                   + f") on the full {n}x{m} input: setup + {pcg_reps} PCG iterations + 1 outer iteration timed "
                    f"({t_setup + t_outer + t_k + t_start:.1f} s), scaled to {n_outer} outer / {n_pcg} PCG iterations"),
     }
 
@@ -404,6 +407,9 @@ def main():
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "bytes_per_launch": alg[dom],
         "avg_launch_ms": per_kind[dom]["avg_ms"], "share_of_kernel_time": per_kind[dom]["total_ms"] / timed_total,
         "traffic": ncu_traffic(dom, args.dtype, n),
+        "note": ("achieved = algorithmic bytes / event-timed launch time; frac > 1 means part of the algorithmic "
+                 "operands (the direction p just written by K1/K4) is served from the 126 MB L2 - traffic is the "
+                 "ncu DRAM bytes of the same kernel"),
         "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)",
         "pcg_iteration": {"bytes": alg["iteration"], "ms": iter_ms,
                           "how": "sum of the per-iteration kernels' event-timed durations",
@@ -446,6 +452,9 @@ def main():
         smp = cpu_reference_sample(x, n_outer, n_pcg)
         cpu_base = {"value": smp["mpix_s"], "unit": UNIT, "cores": cores, "kind": "port", "sample": smp["sample"],
                     "cpu": model_name, "pcg_iters_per_s": smp["pcg_it_s"], "seconds_per_unwrap": smp["seconds"]}
+        fast = cpu_reference_sample(x, n_outer, n_pcg, poisson="dct")
+        cpu_base["fast_cpu_restatement"] = {"value": fast["mpix_s"], "unit": UNIT, "cores": cores,
+                                            "seconds_per_unwrap": fast["seconds"], "sample": fast["sample"]}
 
     if rank == 0:
         line = {
