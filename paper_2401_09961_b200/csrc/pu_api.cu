@@ -490,11 +490,7 @@ struct Impl : HandleBase {
     }
     PU_LAUNCH_CHECK();
     tm.end(st, e, TK_START, -1);
-    // z = M r, rho = r.z (pcg.py:77-79)
-    e = tm.begin(st);
-    k_pcg_r_v<T, false, false, MODE_INIT><<<vg, 256, 0, st>>>(g, nullptr, dv, dh, x, r, ctrl, norms, rs, S_K2, -1);
-    PU_LAUNCH_CHECK();
-    tm.end(st, e, TK_K2, -1);
+    // z = M r, rho = r.z (pcg.py:77-79); rho_s came with the start-up sums
     e = tm.begin(st);
     PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl, nullptr, 0, Pack{}));
     tm.end(st, e, TK_K2B, -1);

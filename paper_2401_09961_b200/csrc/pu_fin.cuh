@@ -30,9 +30,10 @@ __device__ __forceinline__ bool red_final(double (&v)[NS], RedScratch rs, int si
   return true;
 }
 
-// pcg.py:59-75: ||b||, ||r0||, threshold, initial exits
+// pcg.py:59-79: ||b||, ||r0||, threshold, initial exits; rho_s of z0 = M r0
 __device__ __forceinline__ void fin_start(PcgCtrl* ctrl, double* res_norms, const double* tot, double rel_tol,
                                           int max_iters) {
+  ctrl->rho_s = tot[2];
   const double bn = sqrt(tot[0]);
   const double rn = sqrt(tot[1]);
   ctrl->bnorm = bn;

@@ -284,7 +284,7 @@ struct CandArgs {
 };
 
 template <typename T, bool CAND>
-__global__ void __launch_bounds__(256, 3) k_pcg_start_v(Grid g, const T* __restrict__ b, const T* x0, T* x,
+__global__ void __launch_bounds__(256, 2) k_pcg_start_v(Grid g, const T* __restrict__ b, const T* x0, T* x,
                                                         T* __restrict__ r, const T* __restrict__ dv,
                                                         const T* __restrict__ dh, PcgCtrl* ctrl, double* res_norms,
                                                         double rel_tol, int max_iters, RedScratch rs, int site,
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(256, 3) k_pcg_start_v(Grid g, const T* __restr
   const long long P = g.plane, ld = g.ld;
   const bool copy = x != x0;
   const T inv = (T)g.inv_tau;
-  double acc[2] = {0.0, 0.0};
+  double acc[3] = {0.0, 0.0, 0.0};
   PU_FOR_CHUNKS(g, i, j0) {
     const long long o = (long long)i * ld + j0;
     const Q4<T> d1 = ldg4(dv + o), d2 = ldg4(dh + o);
@@ -310,17 +310,23 @@ __global__ void __launch_bounds__(256, 3) k_pcg_start_v(Grid g, const T* __restr
     apply4<T>(g, i, j0, s, d1, d2, au, av, ah);
     const Q4<T> bu = ldg4(b + o), bv = ldg4(b + o + P), bh = ldg4(b + o + 2 * P);
     Q4<T> ru, rv, rh;
-    T pb = (T)0, pr = (T)0;
+    T pb = (T)0, pr = (T)0, prz = (T)0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
       ru.a[k] = add_rn(bu.a[k], -au.a[k]);
       rv.a[k] = add_rn(bv.a[k], -av.a[k]);
       rh.a[k] = add_rn(bh.a[k], -ah.a[k]);
       pb += bu.a[k] * bu.a[k] + bv.a[k] * bv.a[k] + bh.a[k] * bh.a[k];
       pr += ru.a[k] * ru.a[k] + rv.a[k] * rv.a[k] + rh.a[k] * rh.a[k];
+      // rho_s of r0 (pcg.py:77-79, slack part of preconditioner.py:115), as K2a forms it
+      const T zv = (dn_ok(g, i) && j < g.m) ? slack_div(rv.a[k], d1.a[k] + inv) : (T)0;
+      const T zh = (j < g.m - 1) ? slack_div(rh.a[k], d2.a[k] + inv) : (T)0;
+      prz += rv.a[k] * zv + rh.a[k] * zh;
     }
     acc[0] += (double)pb;  // chunk partials in T, grid sums in fp64
     acc[1] += (double)pr;
+    acc[2] += (double)prz;
     if (copy) { st4(x + o, s.u); st4(x + o + P, s.v); st4(x + o + 2 * P, s.h); }
     st4(r + o, ru); st4(r + o + P, rv); st4(r + o + 2 * P, rh);
     if constexpr (CAND) {
@@ -357,8 +363,8 @@ __global__ void __launch_bounds__(256, 3) k_pcg_start_v(Grid g, const T* __restr
       st4(ca.out + o, ou); st4(ca.out + o + P, ov); st4(ca.out + o + 2 * P, oh);
     }
   }
-  double tot[2];
-  if (red_final<2>(acc, rs, site, tot) && threadIdx.x == 0) fin_start(ctrl, res_norms, tot, rel_tol, max_iters);
+  double tot[3];
+  if (red_final<3>(acc, rs, site, tot) && threadIdx.x == 0) fin_start(ctrl, res_norms, tot, rel_tol, max_iters);
 }
 
 }  // namespace pu
