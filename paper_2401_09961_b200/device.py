@@ -168,19 +168,24 @@ class Workspace:
         torch = _torch()
         n, m = self.n, self.m
         shapes = ((n, m), (n - 1, m), (n, m - 1))
-        outs = []
+        outs, events = [], []
+        stream = torch.cuda.current_stream(self.device)
         for idx, (r, c) in enumerate(shapes):
             dev = torch.empty((max(r, 0), max(c, 0)), dtype=self.tdtype, device=self.device)
             if r > 0 and c > 0:
                 self.call("pu_unpack_native", _ptr(x[idx]), r, c, _ptr(dev), self.stream())
             pin = self.pinned(f"out{idx}", (max(r, 0), max(c, 0)), self.tdtype)
             pin.copy_(dev, non_blocking=True)
-            outs.append(pin)
-        torch.cuda.current_stream(self.device).synchronize()
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            outs.append((pin, dev))
+            events.append(ev)
         res = []
-        for p in outs:
+        for (p, _), ev in zip(outs, events):
+            # widen each block on the host while the next one is still in flight;
             # numpy's allocator madvises huge pages for large arrays (few page
             # faults); torch's multi-threaded copy widens fp32 -> fp64 into it
+            ev.synchronize()
             a = np.empty(tuple(p.shape), dtype=np.float64)
             if a.size:
                 torch.from_numpy(a).copy_(p)
