@@ -247,7 +247,8 @@ int pu_pcg_begin(pu_handle* h, const void* b, const void* x0, void* x, const voi
                  void* ctrl, double* res_norms, int max_iters, double rel_tol, const void* gv, const void* gh,
                  const void* cv, const void* ch, const void* wv, const void* wh, double lipschitz, void* cand,
                  void* stream);
-/* K2a + K2b: it < 0 = set-up (rho_s of r0); else x += alpha p, r -= alpha A p
+/* K2a + K2b: it < 0 = set-up (row DCT-II of r0 only; rho_s of r0 came with
+ * pu_pcg_begin); else x += alpha p, r -= alpha A p
  * (submean: after pu_pcg_update_sum, r_u -= mean instead), ||r||, rho_s;
  * then the row DCT-II of r_u into spec_out (packed in band mode). */
 int pu_pcg_residual_rows(pu_handle* h, const void* p, const void* dv, const void* dh, void* x, void* r, void* ctrl,

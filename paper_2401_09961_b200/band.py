@@ -417,7 +417,10 @@ class BandUnwrap:
         for b in self.bands:
             b.call("pu_pcg_columns", _ptr(b.spec_col), _ptr(b.ctrl), it, b.stream())
         self.comm.transpose_back(self.bands)
-        self._reduce(nat.SITE_K2, nat.SITE_K3, _mask(nat.SITE_K2, nat.SITE_K3), mode, it)
+        if it < 0:  # set-up: rho_s of r0 was finalised with the start-up sums
+            self._reduce(nat.SITE_K3, nat.SITE_K3, _mask(nat.SITE_K3), mode, it)
+        else:
+            self._reduce(nat.SITE_K2, nat.SITE_K3, _mask(nat.SITE_K2, nat.SITE_K3), mode, it)
 
     def _dir_halo(self, idx):
         self.comm.halo(self.bands, [(lambda b, i=idx: b.P[i], 0, "both"), (lambda b: b.R, 1, "down")])

@@ -568,9 +568,12 @@ struct Impl : HandleBase {
                         int it, int submean, cudaStream_t st) {
     const int vg = vec_grid();
     cudaEvent_t e = tm.begin(st);
-    if (it < 0)
-      k_pcg_r_v<T, false, false, MODE_INIT><<<vg, 256, 0, st>>>(g, nullptr, dv, dh, x, r, ctrl, norms, rs, S_K2, -1);
-    else if (submean)
+    if (it < 0) {  // set-up: rho_s of r0 came with pu_pcg_begin; only the row transform
+      PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec_out, ctrl, nullptr, 0, pk));
+      tm.end(st, e, TK_K2B, it);
+      return PU_OK;
+    }
+    if (submean)
       k_pcg_r_v<T, false, true, MODE_ITER><<<vg, 256, 0, st>>>(g, p, dv, dh, x, r, ctrl, norms, rs, S_K2, it);
     else
       k_pcg_r_v<T, true, false, MODE_ITER><<<vg, 256, 0, st>>>(g, p, dv, dh, x, r, ctrl, norms, rs, S_K2, it);

@@ -128,32 +128,32 @@ __global__ void __launch_bounds__(256, 4) k_pcg_p_v(Grid g, const T* __restrict_
   auto ps4 = [&](long long o, long long po, const T* d, int i, int j0, bool vert) -> Q4<T> {
     return pslack4<T>(g, r, pold, d, o, po, i, j0, vert, beta, first);
   };
+  // p'Ap as the quadratic form of A (operators.py:138-153): with
+  // rv = S p_u - p_vv and rh = p_u T - p_vh,
+  //   p'Ap = (||rv||^2 + ||rh||^2) / tau + sum dv p_vv^2 + sum dh p_vh^2,
+  // an identity of the reference's p.dot(apply_a(p)) that needs only the
+  // forward differences (row below, next column) and no recomputed neighbours
   double acc[1] = {0.0};
   PU_FOR_CHUNKS(g, i, j0) {
     const long long o = (long long)i * ld + j0;
-    Stencil4<T> s;
-    s.u = ldg4(pnew + o);
-    s.ua = up_ok(g, i) ? ldg4(pnew + o - ld) : zero4<T>();
-    s.ub = dn_ok(g, i) ? ldg4(pnew + o + ld) : zero4<T>();
-    s.ul = ldg_or0(pnew + o - 1, j0 > 0);
-    s.ur = ldg_or0(pnew + o + 4, j0 + 4 < g.m);
-    s.v = ps4(o, P, dv, i, j0, true);
-    s.h = ps4(o, 2 * P, dh, i, j0, false);
-    s.va = up_ok(g, i) ? ps4(o - ld, P, dv, i - 1, j0, true) : zero4<T>();
-    if (j0 > 0) {  // p_h at (i, j0 - 1)
-      const T zr = (j0 - 1 < g.m - 1) ? slack_div(__ldg(r + o - 1 + 2 * P), __ldg(dh + o - 1) + inv) : (T)0;
-      s.hl = first ? zr : add_rn(mul_rn(beta, __ldg(pold + o - 1 + 2 * P)), zr);
-    } else {
-      s.hl = (T)0;
-    }
+    const Q4<T> u = ldg4(pnew + o);
+    const bool hasv = dn_ok(g, i);
+    const Q4<T> ub = hasv ? ldg4(pnew + o + ld) : zero4<T>();
+    const T ur = ldg_or0(pnew + o + 4, j0 + 4 < g.m);
+    const Q4<T> v = ps4(o, P, dv, i, j0, true);
+    const Q4<T> h = ps4(o, 2 * P, dh, i, j0, false);
     const Q4<T> d1 = ldg4(dv + o), d2 = ldg4(dh + o);
-    Q4<T> au, av, ah;
-    apply4<T>(g, i, j0, s, d1, d2, au, av, ah);
-    st4(pnew + o + P, s.v);
-    st4(pnew + o + 2 * P, s.h);
+    st4(pnew + o + P, v);
+    st4(pnew + o + 2 * P, h);
     T part = (T)0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) part += s.u.a[k] * au.a[k] + s.v.a[k] * av.a[k] + s.h.a[k] * ah.a[k];
+    for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
+      const T right = (k == 3) ? ur : u.a[k + 1];
+      const T rv = (hasv && j < g.m) ? (ub.a[k] - u.a[k]) - v.a[k] : (T)0;
+      const T rh = (j < g.m - 1) ? (right - u.a[k]) - h.a[k] : (T)0;
+      part += inv * (rv * rv + rh * rh) + d1.a[k] * v.a[k] * v.a[k] + d2.a[k] * h.a[k] * h.a[k];
+    }
     acc[0] += (double)part;
   }
   double tot[1];
