@@ -271,6 +271,7 @@ def main():
     ap.add_argument("--shard", choices=("auto", "images", "rows"), default="auto",
                     help="N>1: independent images per rank, or one image row-sharded over the ranks "
                          "(auto: rows for c4, images otherwise)")
+    ap.add_argument("--concurrency", type=int, default=8, help="c5: images in flight per GPU")
     ap.add_argument("--warmup-ref", type=int, default=1)
     ap.add_argument("--steps-ref", type=int, default=2)
     args = ap.parse_args()
@@ -315,10 +316,18 @@ def main():
     ws = Workspace.get(n, m, args.dtype, model.tau, model.delta, dev)
     x_devs = [torch.from_numpy(xi).to(dev) for xi in xs]
 
-    def one_unwrap():
+    def one_unwrap_sequential():
         for x_dev in x_devs:
             run, trace = unwrap_device(x_dev, None, model, params, -np.pi, args.dtype, ws)
         return run, trace
+
+    def one_unwrap():
+        if n_img == 1:
+            return one_unwrap_sequential()
+        # C5: the rank's images in flight concurrently (one workspace + stream each)
+        res = pu.unwrap_many(x_devs, None, model, params, -np.pi, dtype=args.dtype, concurrency=args.concurrency,
+                             download=False)
+        return res[-1]
 
     if args.profile_steps:
         for _ in range(args.profile_steps):
@@ -363,7 +372,7 @@ def main():
     ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev2.record()
     for _ in range(args.steps):
-        one_unwrap()
+        one_unwrap_sequential()
     ev3.record()
     torch.cuda.synchronize()
     ws.timing(False)
@@ -437,8 +446,10 @@ def main():
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for x_pin in x_pins:
-            res = pu.unwrap(x_pin, dtype=args.dtype)
+        if n_img == 1:
+            res = pu.unwrap(x_pins[0], dtype=args.dtype)
+        else:
+            res = pu.unwrap_many(x_pins, dtype=args.dtype, concurrency=args.concurrency)[-1]
         t1 = time.perf_counter()
         if i > 0:
             e2e_ms.append((t1 - t0) * 1e3)

@@ -9,7 +9,7 @@ fallback; calling into the solver without the library or a GPU raises.
 
 from . import band
 from .band import unwrap_rows
-from .irls import unwrap, unwrap_device
+from .irls import unwrap, unwrap_device, unwrap_many
 from .objective import (IrlsWeights, arc_count, candidate_step, eval_f, eval_h_delta,
                         update_weights)
 from .operators import DiagonalWeights, SystemVector, apply_system, build_rhs

@@ -41,10 +41,12 @@ class Workspace:
     NSCAL = 16
 
     @classmethod
-    def get(cls, n, m, dtype="fp64", tau=1e-2, delta=1e-6, device=None):
+    def get(cls, n, m, dtype="fp64", tau=1e-2, delta=1e-6, device=None, slot=0):
+        """Cached workspace; `slot` > 0 gives independent buffer sets for
+        concurrent unwraps of the same size (irls.unwrap_many)."""
         torch = _torch()
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        key = (n, m, dtype, float(tau), float(delta), dev.index)
+        key = (n, m, dtype, float(tau), float(delta), dev.index, int(slot))
         with cls._lock:
             ws = cls._cache.get(key)
             if ws is None:

@@ -132,38 +132,133 @@ def unwrap_device(x_dev, c: WeightField | None, model: ModelParams, params: Irls
     return out
 
 
-def _unwrap_loop(ws, x_dev, c, model, params, gradient_lo):
-    run = DeviceUnwrap(ws)
-    run.load(x_dev, c, gradient_lo)
-    cmax = 1.0 if c is None else c.max_weight
-    lip = 12.0 / model.tau + cmax ** 2 / model.delta          # objective.py:103-105
-    trace = IrlsTrace()
-    m_history = [params.max_iter_cg_start]
-    pending = None  # (k, m_cg, delta_rel) of the enqueued iteration awaiting its scalars
-    for k in range(params.max_outer_iters):
-        delta_rel = None
-        if k >= 1:
-            scal, ctrl = ws.read_block()                     # the one sync of this iteration
-            trace.append(_record(*pending, scal, ctrl, ws))
-            pending = None
-            # H(state_k, w_{k-1}) is the accepted value of k-1; H(state_k, w_k) its refresh
-            h_old, h_new = float(scal[ws.S_HACC]), float(scal[ws.S_HNEXT])
-            delta_rel = 0.0 if h_old == 0 else relative_improvement(h_old, h_new)
-            m_prev = m_history[k - 1]
-            m_prev2 = m_history[k - 2] if k >= 2 else m_prev
-            decision = cg_budget_update(delta_rel, m_prev, m_prev2, params)
-            if decision.action == "stop":
-                break
-            m_cg = decision.m_cg
-            m_history.append(m_cg)
-        else:
-            m_cg = m_history[0]
-        run.step(k, m_cg, params, lip)
-        pending = (k, m_cg, delta_rel)
-    if pending is not None:
+class _LoopJob:
+    """The host loop of irls.py:172-222 as a resumable state machine: each
+    `advance()` reads the scalar block of the iteration in flight (the one
+    synchronisation per outer iteration), applies the budget rule and enqueues
+    the next iteration.  One job = one unwrap on its workspace's stream;
+    several jobs interleave on one GPU (unwrap_many)."""
+
+    def __init__(self, ws, x_dev, c, model, params, gradient_lo):
+        self.ws, self.params = ws, params
+        self.run = DeviceUnwrap(ws)
+        self.run.load(x_dev, c, gradient_lo)
+        cmax = 1.0 if c is None else c.max_weight
+        self.lip = 12.0 / model.tau + cmax ** 2 / model.delta          # objective.py:103-105
+        self.trace = IrlsTrace()
+        self.m_history = [params.max_iter_cg_start]
+        self.pending = None  # (k, m_cg, delta_rel) of the enqueued iteration awaiting its scalars
+        self.k = 0
+        if params.max_outer_iters > 0:
+            self.run.step(0, self.m_history[0], params, self.lip)
+            self.pending = (0, self.m_history[0], None)
+            self.k = 1
+
+    def advance(self):
+        """Returns True once the loop has finished (trace complete)."""
+        if self.pending is None:
+            return True
+        ws, params = self.ws, self.params
         scal, ctrl = ws.read_block()
-        trace.append(_record(*pending, scal, ctrl, ws))
-    return run, trace
+        self.trace.append(_record(*self.pending, scal, ctrl, ws))
+        self.pending = None
+        k = self.k
+        if k >= params.max_outer_iters:
+            return True
+        # H(state_k, w_{k-1}) is the accepted value of k-1; H(state_k, w_k) its refresh
+        h_old, h_new = float(scal[ws.S_HACC]), float(scal[ws.S_HNEXT])
+        delta_rel = 0.0 if h_old == 0 else relative_improvement(h_old, h_new)
+        m_prev = self.m_history[k - 1]
+        m_prev2 = self.m_history[k - 2] if k >= 2 else m_prev
+        decision = cg_budget_update(delta_rel, m_prev, m_prev2, params)
+        if decision.action == "stop":
+            return True
+        m_cg = decision.m_cg
+        self.m_history.append(m_cg)
+        self.run.step(k, m_cg, params, self.lip)
+        self.pending = (k, m_cg, delta_rel)
+        self.k = k + 1
+        return False
+
+
+def _unwrap_loop(ws, x_dev, c, model, params, gradient_lo):
+    job = _LoopJob(ws, x_dev, c, model, params, gradient_lo)
+    while not job.advance():
+        pass
+    return job.run, job.trace
+
+
+def unwrap_many(xs, c: WeightField | None = None, model: ModelParams | None = None, params: IrlsParams | None = None,
+                gradient_lo=-np.pi, *, dtype="fp64", concurrency=8, device=None, download=True):
+    """Unwrap independent grids of one size concurrently on one GPU (BASELINE
+    config C5): up to `concurrency` unwraps in flight, each on its own
+    workspace and stream; the host round-robins over them, so while it waits
+    for one iteration's scalars the others keep the GPU busy.  Results are
+    identical to calling `unwrap` on each grid.  Returns UnwrapResults (or
+    (DeviceUnwrap, trace) pairs when download=False)."""
+    from . import _native
+    _native.ensure()
+    torch = _torch()
+    model = model or ModelParams()
+    params = params or IrlsParams()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if not xs:
+        return []
+    n, m = int(xs[0].shape[0]), int(xs[0].shape[1])
+    slots = max(1, min(int(concurrency), len(xs)))
+    wss = [Workspace.get(n, m, dtype, model.tau, model.delta, dev, slot=s) for s in range(slots)]
+    caller = torch.cuda.current_stream(dev)
+    out = [None] * len(xs)
+    active = {}  # slot -> (index, job)
+    nxt = 0
+
+    def start(slot):
+        nonlocal nxt
+        i = nxt
+        nxt += 1
+        xi = xs[i]
+        if tuple(xi.shape) != (n, m):
+            raise ValueError(f"all grids must share one shape, got {tuple(xi.shape)} vs {(n, m)}")
+        ws = wss[slot]
+        s = ws.solve_stream()
+        s.wait_stream(caller)
+        with torch.cuda.stream(s):
+            x_dev = xi.to(device=dev, dtype=torch.float64) if isinstance(xi, torch.Tensor) else ws.upload_grid(xi)
+            _validate_device(x_dev)
+            active[slot] = (i, _LoopJob(ws, x_dev, c, model, params, gradient_lo))
+
+    for slot in range(slots):
+        start(slot)
+    while active:
+        for slot in list(active):
+            i, job = active[slot]
+            ws = wss[slot]
+            with torch.cuda.stream(ws.solve_stream()):
+                finished = job.advance()
+                if finished:
+                    if download:
+                        u, vv, vh = ws.download_system(job.run.state)
+                        out[i] = UnwrapResult(u=u, vv=vv, vh=vh, trace=job.trace)
+                    else:
+                        out[i] = (job.run, job.trace)
+            if finished:
+                del active[slot]
+                caller.wait_stream(ws.solve_stream())
+                if nxt < len(xs):
+                    start(slot)
+    return out
+
+
+def _validate_device(x_dev):
+    """phase.py:100-115 on a device grid (one small synchronising read)."""
+    torch = _torch()
+    if x_dev.dim() != 2 or x_dev.shape[0] < 1 or x_dev.shape[1] < 1:
+        raise ValueError(f"phase grid must be 2-D and non-empty, got shape {tuple(x_dev.shape)}")
+    chk = torch.stack([x_dev.min(), x_dev.max(), torch.isfinite(x_dev).all().to(torch.float64)]).cpu()
+    if chk[2] != 1.0:
+        raise ValueError("phase grid contains non-finite values")
+    if float(chk[0]) < 0.0 or float(chk[1]) >= 2.0 * np.pi:
+        raise ValueError("wrapped phase values must lie in [0, 2*pi)")
 
 
 def unwrap(x, c: WeightField | None = None, model: ModelParams | None = None, params: IrlsParams | None = None,
@@ -190,14 +285,7 @@ def unwrap(x, c: WeightField | None = None, model: ModelParams | None = None, pa
         ws_in = Workspace.get(int(arr.shape[0]), int(arr.shape[1]), dtype, (model or ModelParams()).tau,
                               (model or ModelParams()).delta, dev)
         x_dev = ws_in.upload_grid(arr if isinstance(arr, torch.Tensor) else arr)
-    if x_dev.dim() != 2 or x_dev.shape[0] < 1 or x_dev.shape[1] < 1:
-        raise ValueError(f"phase grid must be 2-D and non-empty, got shape {tuple(x_dev.shape)}")
-    # phase.py:100-115 on the device: finite, within [0, 2pi)
-    chk = torch.stack([x_dev.min(), x_dev.max(), torch.isfinite(x_dev).all().to(torch.float64)]).cpu()
-    if chk[2] != 1.0:
-        raise ValueError("phase grid contains non-finite values")
-    if float(chk[0]) < 0.0 or float(chk[1]) >= 2.0 * np.pi:
-        raise ValueError("wrapped phase values must lie in [0, 2*pi)")
+    _validate_device(x_dev)  # phase.py:100-115 on the device: finite, within [0, 2pi)
     n, m = int(x_dev.shape[0]), int(x_dev.shape[1])
     model = model or ModelParams()
     params = params or IrlsParams()

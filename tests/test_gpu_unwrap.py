@@ -120,3 +120,17 @@ def test_monotone_descent_and_safeguard():
         x = pu.add_phase_noise(pu.wrap_scene(pu.generate_scene(spec)), 0.3, seed + 1000)
         h = pu.unwrap(x).trace.h_values()
         assert all(b <= a * (1 + 1e-12) for a, b in zip(h, h[1:]))
+
+
+def test_unwrap_many_matches_sequential():
+    """Concurrent unwraps (one workspace + stream each, host round-robin) give
+    exactly the results of one-at-a-time unwraps."""
+    xs = [pu.add_phase_noise(pu.wrap_scene(pu.generate_scene(pu.SceneSpec("gaussian-bumps", 40, 36, 8.0, 5.0, s))),
+                             0.6, 50 + s) for s in range(5)]
+    for dtype in ("fp64", "fp32"):
+        seq = [pu.unwrap(x, dtype=dtype) for x in xs]
+        many = pu.unwrap_many(xs, dtype=dtype, concurrency=3)
+        for a, b in zip(seq, many):
+            assert [r.cg_iters for r in a.trace.records] == [r.cg_iters for r in b.trace.records]
+            np.testing.assert_array_equal(a.u, b.u)
+            np.testing.assert_array_equal(a.vh, b.vh)
