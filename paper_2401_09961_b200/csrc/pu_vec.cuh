@@ -17,6 +17,10 @@
 #include "pu_q4.cuh"
 #include "pu_fft.cuh"
 
+// resident CTAs per SM the element-wise kernels are compiled for: the fp32
+// budget in fp32; 2 (128 registers) in fp64, where the fp32 budgets spill
+#define PU_MINB(T, N) (sizeof(T) == 4 ? (N) : 2)
+
 namespace pu {
 
 // chunk loop: chunk q covers cells (i, 4c .. 4c+3), c < cpr = ceil(m / 4)
@@ -116,7 +120,7 @@ __global__ void k_ghost_pslack(Grid g, const T* __restrict__ r, const T* __restr
 // new p (neighbours recomputed the same way) and p'Ap.  (pcg.py:82-89, 102-108)
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(256, 4) k_pcg_p_v(Grid g, const T* __restrict__ r, const T* __restrict__ pold,
+__global__ void __launch_bounds__(256, PU_MINB(T, 4)) k_pcg_p_v(Grid g, const T* __restrict__ r, const T* __restrict__ pold,
                                                     T* __restrict__ pnew, const T* __restrict__ dv,
                                                     const T* __restrict__ dh, PcgCtrl* ctrl, RedScratch rs, int site,
                                                     int it) {
@@ -166,7 +170,7 @@ __global__ void __launch_bounds__(256, 4) k_pcg_p_v(Grid g, const T* __restrict_
 // MODE_ITER finaliser: ||r|| exits (pcg.py:94-100); MODE_INIT: rho_s only.
 // ---------------------------------------------------------------------------
 template <typename T, bool UPDATE, bool SUBMEAN, int MODE>
-__global__ void __launch_bounds__(256, 3) k_pcg_r_v(Grid g, const T* __restrict__ p, const T* __restrict__ dv,
+__global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_pcg_r_v(Grid g, const T* __restrict__ p, const T* __restrict__ dv,
                                                  const T* __restrict__ dh, T* __restrict__ x, T* __restrict__ r,
                                                  PcgCtrl* ctrl, double* res_norms, RedScratch rs, int site, int it) {
   if (ctrl->done) return;
@@ -412,7 +416,7 @@ __device__ __forceinline__ T slack4(T c, T v, T w, T d2) {
 
 // w = sqrt((c v)^2 + delta^2), d = c^2 / w; H(x, w_prev), H(x, w)
 template <typename T>
-__global__ void __launch_bounds__(256, 3) k_weights_hpair_v(Grid g, const T* __restrict__ x, const T* __restrict__ cv,
+__global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_weights_hpair_v(Grid g, const T* __restrict__ x, const T* __restrict__ cv,
                                                          const T* __restrict__ ch, const T* __restrict__ gv,
                                                          const T* __restrict__ gh, const T* __restrict__ wpv,
                                                          const T* __restrict__ wph, T* __restrict__ wv,
@@ -464,7 +468,7 @@ __global__ void __launch_bounds__(256, 3) k_weights_hpair_v(Grid g, const T* __r
 
 // H(xa, w), H(xb, w), mean u of the accepted one, acceptance flag
 template <typename T>
-__global__ void __launch_bounds__(256, 3) k_hpair_states_v(Grid g, const T* __restrict__ xa, const T* __restrict__ xb,
+__global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_hpair_states_v(Grid g, const T* __restrict__ xa, const T* __restrict__ xb,
                                                         const T* __restrict__ wv, const T* __restrict__ wh,
                                                         const T* __restrict__ gv, const T* __restrict__ gh,
                                                         const T* __restrict__ cv, const T* __restrict__ ch,
@@ -504,7 +508,7 @@ __global__ void __launch_bounds__(256, 3) k_hpair_states_v(Grid g, const T* __re
 
 // cand = x - (1/L) grad H(x, w)   (objective.py:108-125)
 template <typename T>
-__global__ void __launch_bounds__(256, 3) k_candidate_v(Grid g, const T* __restrict__ x, const T* __restrict__ wv,
+__global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_candidate_v(Grid g, const T* __restrict__ x, const T* __restrict__ wv,
                                                      const T* __restrict__ wh, const T* __restrict__ gv,
                                                      const T* __restrict__ gh, const T* __restrict__ cv,
                                                      const T* __restrict__ ch, T neg_inv_lip, T* __restrict__ out) {
@@ -552,7 +556,7 @@ __global__ void __launch_bounds__(256, 3) k_candidate_v(Grid g, const T* __restr
 
 // dst = (sel[1] ? xa : xb) with u -= sel[0]; H(dst, w)   (irls.py:206-215)
 template <typename T>
-__global__ void __launch_bounds__(256, 3) k_accept_v(Grid g, const T* __restrict__ xa, const T* __restrict__ xb,
+__global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_accept_v(Grid g, const T* __restrict__ xa, const T* __restrict__ xb,
                                                   const double* sel, T* __restrict__ dst, const T* __restrict__ wv,
                                                   const T* __restrict__ wh, const T* __restrict__ gv,
                                                   const T* __restrict__ gh, const T* __restrict__ cv,
@@ -596,7 +600,7 @@ __global__ void __launch_bounds__(256, 3) k_accept_v(Grid g, const T* __restrict
 // out[0] = H(dst, w_k) (the trace value and the next h_old), out[1] =
 // H(dst, w_next) (the next h_new).  cv/ch == nullptr: unit weights.
 template <typename T>
-__global__ void __launch_bounds__(256, 3) k_accept_weights_v(Grid g, const T* __restrict__ xa,
+__global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_accept_weights_v(Grid g, const T* __restrict__ xa,
                                                              const T* __restrict__ xb, const double* sel,
                                                              T* __restrict__ dst, const T* __restrict__ gv,
                                                              const T* __restrict__ gh, const T* __restrict__ cv,
