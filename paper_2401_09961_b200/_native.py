@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libpu_unwrap.so")
+# PU_LIB_PATH: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("PU_LIB_PATH") or os.path.join(_HERE, "_lib", "libpu_unwrap.so")
 
 PU_F32, PU_F64 = 0, 1
 PU_OK, PU_ERR_ARG, PU_ERR_CUDA, PU_ERR_UNSUPPORTED, PU_ERR_NOMEM = 0, 1, 2, 3, 4
