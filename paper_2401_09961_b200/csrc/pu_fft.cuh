@@ -21,7 +21,7 @@ namespace pu {
 // columns per CTA of a static column plan: 2 packed sequences while they fit
 // one 1024-thread group, else 1 (L / EMAX = 1024 threads, e.g. 16384 fp32)
 __host__ __device__ constexpr int static_panel_cols(int L, int emax) {
-  return 2 * L <= 1024 * emax ? PU_PANEL_COLS : PU_PANEL_COLS / 2;
+  return 4 * L <= 1024 * emax ? 2 * PU_PANEL_COLS : (2 * L <= 1024 * emax ? PU_PANEL_COLS : PU_PANEL_COLS / 2);
 }
 #define PU_FFT_MAX_THREADS 1024  // absolute per-CTA thread cap of the transform kernels
 
