@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_weights_hpair_v(Grid g, 
 
 // H(xa, w), H(xb, w), mean u of the accepted one, acceptance flag
 template <typename T>
-__global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_hpair_states_v(Grid g, const T* __restrict__ xa, const T* __restrict__ xb,
+__global__ void __launch_bounds__(256, PU_MINB(T, 2)) k_hpair_states_v(Grid g, const T* __restrict__ xa, const T* __restrict__ xb,
                                                         const T* __restrict__ wv, const T* __restrict__ wh,
                                                         const T* __restrict__ gv, const T* __restrict__ gh,
                                                         const T* __restrict__ cv, const T* __restrict__ ch,
@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_accept_v(Grid g, const T
 // out[0] = H(dst, w_k) (the trace value and the next h_old), out[1] =
 // H(dst, w_next) (the next h_new).  cv/ch == nullptr: unit weights.
 template <typename T>
-__global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_accept_weights_v(Grid g, const T* __restrict__ xa,
+__global__ void __launch_bounds__(256, PU_MINB(T, 2)) k_accept_weights_v(Grid g, const T* __restrict__ xa,
                                                              const T* __restrict__ xb, const double* sel,
                                                              T* __restrict__ dst, const T* __restrict__ gv,
                                                              const T* __restrict__ gh, const T* __restrict__ cv,
