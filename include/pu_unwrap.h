@@ -235,6 +235,20 @@ int pu_create_band(pu_handle** out, int m, const pu_band* band, int dtype, doubl
 /* Device fp64 [PU_NSITES * PU_MAX_SUMS_ABI] that receives band totals; NULL
  * restores single-grid finalisation. */
 int pu_set_band_totals(pu_handle* h, double* totals);
+/* Fused transpose: `table` (device, nq uint64) holds the address of every
+ * rank's column block (N x mb, pitch mb) -- on this GPU, or a peer's block
+ * mapped with pu_ipc_open over NVLink.  The row DCT-II then stores each
+ * chunk straight into its owner's block and the row DCT-III fetches its rows
+ * from them (spec_out / spec_in are ignored); the caller orders the kernels
+ * across ranks (the all-reduces between them do).  NULL: packed buffers. */
+int pu_set_band_peers(pu_handle* h, const uint64_t* table);
+/* CUDA IPC for the peer tables: a 64-byte handle of a pu_dev_alloc block,
+ * opened in another process on a peer GPU. */
+int pu_ipc_handle(const void* dev_ptr, void* handle);
+int pu_ipc_open(const void* handle, void** dev_ptr);
+int pu_ipc_close(void* dev_ptr);
+int pu_dev_alloc(int64_t bytes, void** dev_ptr);
+int pu_dev_free(void* dev_ptr);
 /* Run the finalisers of the sites in `mask` (bit = pu_site) on `totals` (the
  * all-reduced buffer), in PCG order, skipping PCG sites once ctrl->done.
  * mode: 1 = PCG set-up (z0, rho0), 2 = iteration `it`.  out: the scalar

@@ -59,6 +59,12 @@ SIGNATURES = {
     # row-sharded grids (band.py)
     "pu_create_band": (_i, [ctypes.POINTER(_vp), _i, _vp, _i, _d, _d]),
     "pu_set_band_totals": (_i, [_vp, _vp]),
+    "pu_set_band_peers": (_i, [_vp, _vp]),
+    "pu_ipc_handle": (_i, [_vp, _vp]),
+    "pu_ipc_open": (_i, [_vp, ctypes.POINTER(_vp)]),
+    "pu_ipc_close": (_i, [_vp]),
+    "pu_dev_alloc": (_i, [_i64, ctypes.POINTER(_vp)]),
+    "pu_dev_free": (_i, [_vp]),
     "pu_finalize": (_i, [_vp, ctypes.c_uint, _i, _i, _vp, _vp, _vp, _d, _i, _vp]),
     "pu_pcg_begin": (_i, [_vp] + [_vp] * 8 + [_i, _d] + [_vp] * 6 + [_d, _vp, _vp]),
     "pu_pcg_residual_rows": (_i, [_vp] + [_vp] * 8 + [_i, _i, _vp]),

@@ -87,7 +87,7 @@ class BandState:
     NSCAL = 16
     (S_HOLD, S_HNEW, S_HPROP, S_HCAND, S_MEAN, S_TAKE, S_HACC, S_HNEXT) = range(8)
 
-    def __init__(self, layout: BandLayout, rank: int, dtype: str, tau: float, delta: float, device):
+    def __init__(self, layout: BandLayout, rank: int, dtype: str, tau: float, delta: float, device, peer=False):
         torch = _torch()
         self.lib = nat.ensure()
         if dtype not in _DTYPES:
@@ -111,8 +111,20 @@ class BandState:
         self.Wt = [z(2), z(2)]
         self.P = [z(3), z(3)]
         self.W = None
-        self.spec_send = torch.zeros(self.nq * self.rows * self.mb, dtype=self.tdtype, device=device)
-        self.spec_col = torch.zeros(self.n * self.mb, dtype=self.tdtype, device=device)
+        self.peer = bool(peer)
+        self.col_ptr, self.peer_table, self._opened = None, None, []
+        if self.peer:
+            # fused transpose (pu_set_band_peers): the column block is a plain
+            # cudaMalloc block so other ranks can map it over NVLink (CUDA IPC)
+            ptr = ctypes.c_void_p()
+            with torch.cuda.device(device):
+                nat.check(self.lib.pu_dev_alloc(self.n * self.mb * (4 if self.code == nat.PU_F32 else 8),
+                                                ctypes.byref(ptr)))
+            self.col_ptr = ptr.value
+            self.spec_send = self.spec_col = None
+        else:
+            self.spec_send = torch.zeros(self.nq * self.rows * self.mb, dtype=self.tdtype, device=device)
+            self.spec_col = torch.zeros(self.n * self.mb, dtype=self.tdtype, device=device)
         self.totals = torch.zeros(nat.NSITES * nat.MAX_SUMS, dtype=torch.float64, device=device)
         ctrl_bytes = int(self.lib.pu_pcg_ctrl_bytes())
         self.block = torch.zeros(self.NSCAL * 8 + ctrl_bytes, dtype=torch.uint8, device=device)
@@ -127,8 +139,24 @@ class BandState:
         try:
             if getattr(self, "h", None) is not None and self.h.value:
                 self.lib.pu_destroy(self.h)
+            for q in getattr(self, "_opened", []):
+                self.lib.pu_ipc_close(ctypes.c_void_p(q))
+            if getattr(self, "col_ptr", None):
+                self.lib.pu_dev_free(ctypes.c_void_p(self.col_ptr))
         except Exception:
             pass
+
+    def set_peers(self, addresses):
+        """Column-block addresses of every rank (rank order) -> fused transpose."""
+        torch = _torch()
+        self.peer_table = torch.tensor([int(a) for a in addresses], dtype=torch.int64, device=self.device)
+        nat.check(self.lib.pu_set_band_peers(self.h, _ptr(self.peer_table)))
+
+    def col(self):
+        return ctypes.c_void_p(self.col_ptr) if self.peer else _ptr(self.spec_col)
+
+    def send(self):
+        return ctypes.c_void_p(0) if self.peer else _ptr(self.spec_send)
 
     # pointers -------------------------------------------------------------
     @staticmethod
@@ -269,10 +297,10 @@ class DistComm:
             send_up = torch.stack([get(b)[pl, 1] for get, pl in up])
             ops.append(P2P(self.dist.isend, send_up, self._peer(r - 1), self.group))
         if down and r > 0:
-            recv_above = torch.empty((len(down), b.ld), dtype=b.tdtype, device=b.spec_col.device)
+            recv_above = torch.empty((len(down), b.ld), dtype=b.tdtype, device=b.device)
             ops.append(P2P(self.dist.irecv, recv_above, self._peer(r - 1), self.group))
         if up and r + 1 < world:
-            recv_below = torch.empty((len(up), b.ld), dtype=b.tdtype, device=b.spec_col.device)
+            recv_below = torch.empty((len(up), b.ld), dtype=b.tdtype, device=b.device)
             ops.append(P2P(self.dist.irecv, recv_below, self._peer(r + 1), self.group))
         if ops:
             for req in self.dist.batch_isend_irecv(ops):
@@ -367,10 +395,10 @@ class BandUnwrap:
         # z0 = M r0, rho0; p0 = z0 (pcg.py:77-79)
         for b in self.bands:
             b.call("pu_pcg_residual_rows", None, P(b.D, 0), P(b.D, 1), P(cur(b)), P(b.R), _ptr(b.ctrl),
-                   _ptr(b.norms), _ptr(b.spec_send), -1, 0, b.stream())
+                   _ptr(b.norms), b.send(), -1, 0, b.stream())
         self._precond_tail(-1, mode=1)
         for b in self.bands:
-            b.call("pu_pcg_rows_inv", _ptr(b.spec_send), P(b.P[0]), P(b.P[1]), 1, _ptr(b.ctrl), -1, b.stream())
+            b.call("pu_pcg_rows_inv", b.send(), P(b.P[0]), P(b.P[1]), 1, _ptr(b.ctrl), -1, b.stream())
         self._dir_halo(0)
         for it in range(m_cg):
             if it > 0 and it % poll == 0 and self._done():
@@ -388,10 +416,10 @@ class BandUnwrap:
                 self._reduce(nat.SITE_UPD, nat.SITE_UPD, _mask(nat.SITE_UPD), 2, it)
             for b in self.bands:
                 b.call("pu_pcg_residual_rows", P(b.P[it & 1]), P(b.D, 0), P(b.D, 1), P(cur(b)), P(b.R),
-                       _ptr(b.ctrl), _ptr(b.norms), _ptr(b.spec_send), it, 1 if submean else 0, b.stream())
+                       _ptr(b.ctrl), _ptr(b.norms), b.send(), it, 1 if submean else 0, b.stream())
             self._precond_tail(it, mode=2)
             for b in self.bands:
-                b.call("pu_pcg_rows_inv", _ptr(b.spec_send), P(b.P[(it + 1) & 1]), P(b.P[it & 1]), 0,
+                b.call("pu_pcg_rows_inv", b.send(), P(b.P[(it + 1) & 1]), P(b.P[it & 1]), 0,
                        _ptr(b.ctrl), it, b.stream())
             self._dir_halo((it + 1) & 1)
         # H pair (irls.py:202-205) on the proposal (= state, solved in place) and the candidate
@@ -413,9 +441,22 @@ class BandUnwrap:
         self._state_halo(lambda b: b.S[b.cur], with_dv=True)
 
     def _precond_tail(self, it, mode):
+        if self.bands[0].peer:
+            # fused transpose: the row DCT-II stored straight into the column
+            # blocks; the all-reduces order the kernels across ranks (each
+            # completes only once every rank has reached it)
+            self.comm.allreduce(self.bands, nat.SITE_K2, nat.SITE_K2)
+            for b in self.bands:
+                b.call("pu_pcg_columns", b.col(), _ptr(b.ctrl), it, b.stream())
+            self.comm.allreduce(self.bands, nat.SITE_K3, nat.SITE_K3)
+            mask = _mask(nat.SITE_K3) if it < 0 else _mask(nat.SITE_K2, nat.SITE_K3)
+            for b in self.bands:
+                b.call("pu_finalize", mask, mode, it, _ptr(b.ctrl), _ptr(b.norms), ctypes.c_void_p(0), 0.0, 0,
+                       b.stream())
+            return
         self.comm.transpose(self.bands)
         for b in self.bands:
-            b.call("pu_pcg_columns", _ptr(b.spec_col), _ptr(b.ctrl), it, b.stream())
+            b.call("pu_pcg_columns", b.col(), _ptr(b.ctrl), it, b.stream())
         self.comm.transpose_back(self.bands)
         if it < 0:  # set-up: rho_s of r0 was finalised with the start-up sums
             self._reduce(nat.SITE_K3, nat.SITE_K3, _mask(nat.SITE_K3), mode, it)
@@ -497,18 +538,25 @@ class RowSharded:
     _cache: dict = {}
 
     @classmethod
-    def get(cls, n, m, dtype, model: ModelParams, device, bands=None, group=None):
+    def get(cls, n, m, dtype, model: ModelParams, device, bands=None, group=None, peer=None):
+        import os
         import torch.distributed as dist
         distributed = bands is None and dist.is_available() and dist.is_initialized()
+        if peer is None:
+            peer = os.environ.get("PU_BAND_P2P") == "1"
         key = (n, m, dtype, float(model.tau), float(model.delta), str(device), bands, id(group) if distributed else None,
-               distributed)
+               distributed, bool(peer))
         obj = cls._cache.get(key)
         if obj is None:
-            obj = cls(n, m, dtype, model, device, bands, group)
+            obj = cls(n, m, dtype, model, device, bands, group, peer)
             cls._cache[key] = obj
         return obj
 
-    def __init__(self, n, m, dtype, model: ModelParams, device, bands=None, group=None):
+    def __init__(self, n, m, dtype, model: ModelParams, device, bands=None, group=None, peer=False):
+        """peer: fuse the DCT transpose into the row kernels (stores into /
+        loads from every rank's column block: same GPU in loopback, peer GPUs
+        over NVLink via CUDA IPC under torch.distributed) instead of two
+        all-to-alls per PCG iteration."""
         import torch.distributed as dist
         torch = _torch()
         nat.ensure()
@@ -523,9 +571,36 @@ class RowSharded:
         self.device = torch.device(device)
         self.model = model
         with torch.cuda.device(self.device):
-            self.bands = [BandState(self.layout, r, dtype, model.tau, model.delta, self.device) for r in self.ranks]
+            self.bands = [BandState(self.layout, r, dtype, model.tau, model.delta, self.device, peer)
+                          for r in self.ranks]
+            if peer:
+                self._wire_peers()
             self.stream = torch.cuda.Stream(device=self.device)
         self.driver = BandUnwrap(self.bands, self.comm)
+
+    def _wire_peers(self):
+        """Every band learns the column-block address of every rank."""
+        if not self.distributed:
+            addrs = [b.col_ptr for b in self.bands]
+            for b in self.bands:
+                b.set_peers(addrs)
+            return
+        import torch.distributed as dist
+        (b,) = self.bands
+        handle = ctypes.create_string_buffer(64)
+        nat.check(b.lib.pu_ipc_handle(ctypes.c_void_p(b.col_ptr), handle))
+        handles = [None] * self.layout.world
+        dist.all_gather_object(handles, bytes(handle.raw), group=self.group)
+        addrs = []
+        for q, hq in enumerate(handles):
+            if q == b.rank:
+                addrs.append(b.col_ptr)
+                continue
+            ptr = ctypes.c_void_p()
+            nat.check(b.lib.pu_ipc_open(ctypes.create_string_buffer(hq, 64), ctypes.byref(ptr)))
+            b._opened.append(ptr.value)
+            addrs.append(ptr.value)
+        b.set_peers(addrs)
 
     def rows_of(self, r):
         """Rows of x band r reads: its own and the first row of the band below."""
@@ -558,7 +633,8 @@ class RowSharded:
 
 
 def unwrap_rows(x, c: WeightField | None = None, model: ModelParams | None = None, params: IrlsParams | None = None,
-                gradient_lo=-np.pi, *, dtype="fp64", bands=None, group=None, gather=True, device=None):
+                gradient_lo=-np.pi, *, dtype="fp64", bands=None, group=None, gather=True, device=None,
+                peer=None):
     """irls.py:132-224 on a row-sharded grid.
 
     Inside a torch.distributed job (and `bands` None) every rank passes the same
@@ -567,6 +643,9 @@ def unwrap_rows(x, c: WeightField | None = None, model: ModelParams | None = Non
     reduction totals and the DCT transpose over `group` (default: world).
     Otherwise `bands` = B runs all B bands in this process on one device
     (loopback collectives) — the same decomposition, for testing.
+    `peer` (default: PU_BAND_P2P=1) fuses the DCT transpose into the row
+    kernels (stores into / loads from the other ranks' column blocks,
+    pu_set_band_peers) instead of two all-to-alls per PCG iteration.
     Returns an UnwrapResult with the full grid on every rank when `gather`,
     else the rank's own band rows (u, vv, vh) and the trace.
     """
@@ -581,7 +660,7 @@ def unwrap_rows(x, c: WeightField | None = None, model: ModelParams | None = Non
     n, m = int(arr.shape[0]), int(arr.shape[1])
     _check_inputs(arr, c, n, m, gradient_lo)
     with torch.cuda.device(dev):
-        solver = RowSharded.get(n, m, dtype, model, dev, bands, group)
+        solver = RowSharded.get(n, m, dtype, model, dev, bands, group, peer)
         xs = solver.upload(arr)
         for xr in xs:
             _validate_device(xr)

@@ -385,7 +385,7 @@ struct Impl : HandleBase {
     if (band) {
       gc.n = n_glob; gc.m = b->cols; gc.ld = b->mb; gc.plane = (long long)n_glob * b->mb;
       gc.top = gc.bot = 0;
-      pk = Pack{b->nq, b->mb, (long long)n * b->mb};
+      pk = Pack{b->nq, b->mb, (long long)n * b->mb, nullptr, (long long)b->row0};
       col0 = b->col0;
     }
     int rc;
@@ -1061,6 +1061,47 @@ int pu_create_band(pu_handle** out, int m, const pu_band* b, int dtype, double t
     return rc;
   }
   *out = h;
+  return PU_OK;
+}
+
+int pu_set_band_peers(pu_handle* h, const uint64_t* table) {
+  PU_DISPATCH(h, {
+    if (!I.band) return fail(PU_ERR_ARG, "pu_set_band_peers needs a band handle");
+    I.pk.peers = reinterpret_cast<const unsigned long long*>(table);
+  });
+  return PU_OK;
+}
+
+int pu_ipc_handle(const void* dev_ptr, void* handle) {
+  if (!dev_ptr || !handle) return fail(PU_ERR_ARG, "null argument");
+  cudaIpcMemHandle_t hd;
+  PU_CUDA(cudaIpcGetMemHandle(&hd, const_cast<void*>(dev_ptr)));
+  std::memcpy(handle, &hd, sizeof(hd));
+  return PU_OK;
+}
+
+int pu_ipc_open(const void* handle, void** dev_ptr) {
+  if (!dev_ptr || !handle) return fail(PU_ERR_ARG, "null argument");
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle, sizeof(hd));
+  PU_CUDA(cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+  return PU_OK;
+}
+
+int pu_ipc_close(void* dev_ptr) {
+  PU_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return PU_OK;
+}
+
+int pu_dev_alloc(int64_t bytes, void** dev_ptr) {
+  if (!dev_ptr || bytes < 0) return fail(PU_ERR_ARG, "bad arguments");
+  PU_CUDA(cudaMalloc(dev_ptr, (size_t)std::max<int64_t>(bytes, 1)));
+  PU_CUDA(cudaMemset(*dev_ptr, 0, (size_t)std::max<int64_t>(bytes, 1)));
+  return PU_OK;
+}
+
+int pu_dev_free(void* dev_ptr) {
+  if (dev_ptr) PU_CUDA(cudaFree(dev_ptr));
   return PU_OK;
 }
 

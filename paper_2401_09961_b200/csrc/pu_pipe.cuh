@@ -66,10 +66,18 @@ __host__ __device__ constexpr size_t rows_pipe_smem(int n, int tsize, int ldseq,
 // chunk q = columns [q mb, (q + 1) mb) of the band's rows, row pitch mb:
 // element (i, k) at (k / mb) * chunk + i * mb + k % mb.  The forward kernel
 // writes it, the inverse one reads its rows as nq bulk copies.  nq = 0: plain.
+//
+// With `peers` set, the transpose is fused into the kernels instead: element
+// (band row i, column k) lives in rank q = k / mb's column block (N x mb,
+// pitch mb; peers[q] = its address, on this GPU or a peer mapped over NVLink)
+// at row row0 + i, so the forward kernel stores straight into the other
+// ranks' blocks and the inverse kernel fetches its rows from them.
 struct Pack {
   int nq;
   int mb;
   long long chunk;
+  const unsigned long long* peers;  // device array of nq block addresses, or null
+  long long row0;                   // this band's first global row
 };
 
 // pl.stage1 (rows too long for two staged rows next to the FFT buffer, e.g.
@@ -103,8 +111,11 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   __syncthreads();
   auto fetch = [&](T* dst, int row) {  // one thread; RB bytes
     if (pin) {
-      for (int q = 0; q < pk.nq; ++q)
-        bulk_g2s(dst + q * pk.mb, in + q * pk.chunk + (long long)row * pk.mb, pk.mb * (unsigned)sizeof(T), mbar);
+      for (int q = 0; q < pk.nq; ++q) {
+        const T* src = pk.peers ? reinterpret_cast<const T*>(pk.peers[q]) + (pk.row0 + row) * pk.mb
+                                : in + q * pk.chunk + (long long)row * pk.mb;
+        bulk_g2s(dst + q * pk.mb, src, pk.mb * (unsigned)sizeof(T), mbar);
+      }
     } else {
       bulk_g2s(dst, in + (long long)row * g.ld, RB, mbar);
     }
@@ -205,21 +216,24 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
     const long long oa = (long long)ia * g.ld, ob = oa + g.ld;
     if constexpr (!INV) {
       if (pout) {
-        // packed: column k of rows ia, ia + 1 -> chunk k / mb
-        auto at = [&](int k) -> long long {
+        // packed: column k of rows ia, ia + 1 -> chunk k / mb (local buffer,
+        // or the owning rank's column block)
+        auto at = [&](int k) -> T* {
           const int q = k / pk.mb;
-          return q * pk.chunk + (long long)ia * pk.mb + (k - q * pk.mb);
+          T* base = pk.peers ? reinterpret_cast<T*>(__ldg(pk.peers + q)) + (pk.row0 + ia) * pk.mb
+                             : out + q * pk.chunk + (long long)ia * pk.mb;
+          return base + (k - q * pk.mb);
         };
         for (int k = threadIdx.x; k < half; k += blockDim.x) {
           const int nk = k == 0 ? 0 : n - k;
           const PairOut<T> q = dct2_post<T>(buf[spad(k)], buf[spad(nk)], k, nk, pl);
-          const long long ok_ = at(k);
-          out[ok_] = q.a_k;
-          if (hasb) out[ok_ + pk.mb] = q.b_k;
+          T* ok_ = at(k);
+          ok_[0] = q.a_k;
+          if (hasb) ok_[pk.mb] = q.b_k;
           if (nk != k) {
-            const long long onk = at(nk);
-            out[onk] = q.a_nk;
-            if (hasb) out[onk + pk.mb] = q.b_nk;
+            T* onk = at(nk);
+            onk[0] = q.a_nk;
+            if (hasb) onk[pk.mb] = q.b_nk;
           }
         }
       } else {

@@ -29,7 +29,7 @@ def _fake_band(lay, r, seed):
     ld = (lay.m + 7) // 8 * 8
     rows = lay.rows[r]
     b = SimpleNamespace(layout=lay, rank=r, rows=rows, row0=lay.row0[r], n=lay.n, m=lay.m, mb=lay.mb, nq=lay.world,
-                        ld=ld, tdtype=torch.float64)
+                        ld=ld, tdtype=torch.float64, device=torch.device("cpu"))
     b.X = torch.randn((3, rows + 2, ld), generator=g, dtype=torch.float64)
     b.Y = torch.randn((3, rows + 2, ld), generator=g, dtype=torch.float64)
     b.spec_send = torch.randn(lay.world * rows * lay.mb, generator=g, dtype=torch.float64)

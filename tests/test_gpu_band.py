@@ -26,12 +26,15 @@ def _scene(n, m, noise=0.7, seed=5):
     return pu.add_phase_noise(pu.wrap_scene(pu.generate_scene(spec)), noise, 100 + seed)
 
 
+@pytest.mark.parametrize("peer", [False, True])
 @pytest.mark.parametrize("shape,bands", [((64, 48), 2), ((50, 45), 3), ((37, 64), 4), ((96, 80), 5),
                                          ((40, 33), 1)])
-def test_bands_match_single_grid_fp64(shape, bands):
+def test_bands_match_single_grid_fp64(shape, bands, peer):
+    """Packed all-to-all transposes (peer=False) and the transpose fused into
+    the row kernels through the column-block address table (peer=True)."""
     x = _scene(*shape)
     single = pu.unwrap(x, dtype="fp64")
-    res = pu.unwrap_rows(x, dtype="fp64", bands=bands)
+    res = pu.unwrap_rows(x, dtype="fp64", bands=bands, peer=peer)
     assert [r.cg_iters for r in res.trace.records] == [r.cg_iters for r in single.trace.records]
     assert [r.m_cg for r in res.trace.records] == [r.m_cg for r in single.trace.records]
     np.testing.assert_allclose([r.h_delta for r in res.trace.records], [r.h_delta for r in single.trace.records],
@@ -56,10 +59,11 @@ def test_bands_match_reference(golden_unwrap, golden_meta, name):
     assert rel(res.u, u_ref) <= 1e-8 or np.max(np.abs(res.u - u_ref)) <= 1e-12
 
 
-def test_bands_fp32_objective():
+@pytest.mark.parametrize("peer", [False, True])
+def test_bands_fp32_objective(peer):
     x = _scene(128, 96, noise=0.9, seed=7)
     ref_state, _, (gv, gh) = port.unwrap(x, poisson="dct")
-    res = pu.unwrap_rows(x, dtype="fp32", bands=4)
+    res = pu.unwrap_rows(x, dtype="fp32", bands=4, peer=peer)
     ones = (np.ones_like(gv), np.ones_like(gh))
     f_ref = port.f_l1(ref_state, gv, gh, *ones, 1e-2)
     f32 = port.f_l1(port.Triple(res.u, res.vv, res.vh), gv, gh, *ones, 1e-2)
@@ -71,7 +75,7 @@ def test_band_pcg_long_budget_reprojection():
     x = _scene(72, 64, noise=1.0, seed=9)
     prm = pu.IrlsParams(max_iter_cg_start=60, cg_rel_tol=1e-14, max_outer_iters=3)
     single = pu.unwrap(x, params=prm, dtype="fp64")
-    res = pu.unwrap_rows(x, params=prm, dtype="fp64", bands=3)
+    res = pu.unwrap_rows(x, params=prm, dtype="fp64", bands=3, peer=True)
     assert [r.cg_iters for r in res.trace.records] == [r.cg_iters for r in single.trace.records]
     assert max(r.cg_iters for r in res.trace.records) > 50
     assert rel(res.u, single.u) <= 1e-9
