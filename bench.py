@@ -304,6 +304,10 @@ def main():
                     help="N>1: independent images per rank, or one image row-sharded over the ranks "
                          "(auto: rows for c4, images otherwise)")
     ap.add_argument("--concurrency", type=int, default=8, help="c5: images in flight per GPU")
+    ap.add_argument("--peer", action="store_true",
+                    help="--shard rows: transpose fused into the row kernels over peer memory (default: all-to-all)")
+    ap.add_argument("--bands", type=int, default=None,
+                    help="--shard rows without torchrun: B bands in this process (loopback collectives)")
     ap.add_argument("--warmup-ref", type=int, default=1)
     ap.add_argument("--steps-ref", type=int, default=2)
     args = ap.parse_args()
@@ -554,7 +558,7 @@ def main_rows(args, rank, local_rank, world, dev, lib):
     _, x = pu.config_scene(args.config)
     n, m = x.shape
     model, params = pu.ModelParams(), pu.IrlsParams()
-    solver = RowSharded.get(n, m, args.dtype, model, dev)
+    solver = RowSharded.get(n, m, args.dtype, model, dev, bands=args.bands, peer=args.peer)
     lay = solver.layout
     xs = solver.upload(x)
     torch.cuda.synchronize()
@@ -625,7 +629,7 @@ def main_rows(args, rank, local_rank, world, dev, lib):
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = pu.unwrap_rows(x, dtype=args.dtype, gather=False)
+        res = pu.unwrap_rows(x, dtype=args.dtype, gather=False, bands=args.bands, peer=args.peer)
         t1 = time.perf_counter()
         if i > 0:
             e2e_ms.append((t1 - t0) * 1e3)
@@ -639,7 +643,10 @@ def main_rows(args, rank, local_rank, world, dev, lib):
             "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: {WORKLOAD[args.config]}", "n": n, "m": m,
                        "sharding": f"one image row-sharded over {world} rank(s): bands {lay.rows}, "
-                                   f"transpose blocks of {lay.mb} columns",
+                                   f"transpose blocks of {lay.mb} columns"
+                                   + (" (all bands in one process, loopback collectives)" if args.bands else "")
+                                   + (", transpose fused into the row kernels (peer stores/loads)" if args.peer
+                                      else ", NCCL all-to-all transposes"),
                        "l2": "inputs larger than L2", "plan": None},
             "unwrap_s": step_ms / 1e3, "pcg_iters_per_step": n_pcg, "outer_iters_per_step": len(trace.records),
             "pcg_iters_per_s": n_pcg / (step_ms / 1e3),
