@@ -134,3 +134,22 @@ def test_unwrap_many_matches_sequential():
             assert [r.cg_iters for r in a.trace.records] == [r.cg_iters for r in b.trace.records]
             np.testing.assert_array_equal(a.u, b.u)
             np.testing.assert_array_equal(a.vh, b.vh)
+
+
+@pytest.mark.parametrize("shape", [(257, 385), (1000, 3), (3, 1000), (513, 1023), (127, 2048)])
+def test_odd_sizes_vs_oracle(shape):
+    """Non-power-of-two and very skinny grids (runtime mixed-radix / Bluestein
+    transform plans) against the DCT restatement of the reference."""
+    n, m = shape
+    spec = pu.SceneSpec("gaussian-bumps", n, m, 9.0, max(2.0, min(n, m) / 6), 11)
+    x = pu.add_phase_noise(pu.wrap_scene(pu.generate_scene(spec)), 0.6, 77)
+    ref_state, ref_recs, (gv, gh) = port.unwrap(x, poisson="dct")
+    res = pu.unwrap(x, dtype="fp64")
+    ones = (np.ones_like(gv), np.ones_like(gh))
+    f_ref = port.f_l1(ref_state, gv, gh, *ones, 1e-2)
+    f64 = port.f_l1(port.Triple(res.u, res.vv, res.vh), gv, gh, *ones, 1e-2)
+    assert abs(f64 - f_ref) <= 1e-8 * max(f_ref, 1.0)
+    assert [r.cg_iters for r in res.trace.records] == [r.cg_iters for r in ref_recs]
+    res32 = pu.unwrap(x, dtype="fp32")
+    f32 = port.f_l1(port.Triple(res32.u, res32.vv, res32.vh), gv, gh, *ones, 1e-2)
+    assert abs(f32 - f_ref) <= max(1e-3 * f_ref, 1e-6)
