@@ -587,6 +587,8 @@ def main_rows(args, rank, local_rank, world, dev, lib):
 
     # instrumented pass on this rank's band (CUDA events around each launch)
     b = solver.bands[0]
+    graphs = solver.driver.graphs
+    solver.driver.graphs = False  # per-launch events need eager launches
     lib.pu_timing_enable(b.h, 1)
     kinds = np.zeros(0, dtype=np.int32)
     barrier()
@@ -598,6 +600,7 @@ def main_rows(args, rank, local_rank, world, dev, lib):
     kb, ib, mb_ = (ctypes.c_int * cap)(), (ctypes.c_int * cap)(), (ctypes.c_float * cap)()
     cnt = int(lib.pu_timing_read(b.h, kb, ib, mb_, cap))
     lib.pu_timing_enable(b.h, 0)
+    solver.driver.graphs = graphs
     kinds = np.frombuffer(kb, dtype=np.int32, count=cnt).copy()
     ms = np.frombuffer(mb_, dtype=np.float32, count=cnt).astype(np.float64)
     barrier()

@@ -110,7 +110,7 @@ class BandState:
         self.C, self.B, self.G, self.D, self.R = z(3), z(3), z(2), z(2), z(3)
         self.Wt = [z(2), z(2)]
         self.P = [z(3), z(3)]
-        self.W = None
+        self.W, self.use_w = None, False
         self.peer = bool(peer)
         self.col_ptr, self.peer_table, self._opened = None, None, []
         if self.peer:
@@ -327,8 +327,16 @@ class BandUnwrap:
     """irls.py:132-224 on row bands.  `bands`: the bands this process drives
     (all of them with LoopbackComm, its own with DistComm)."""
 
-    def __init__(self, bands, comm):
+    def __init__(self, bands, comm, graphs=None):
+        import os
         self.bands, self.comm = bands, comm
+        # one CUDA graph per (budget, buffer parity) replays a whole outer
+        # iteration -- kernels and loopback copies; NCCL collectives only on
+        # request (PU_BAND_GRAPHS=1) until graph capture has run on a multi-GPU box
+        if graphs is None:
+            graphs = isinstance(comm, LoopbackComm) or os.environ.get("PU_BAND_GRAPHS") == "1"
+        self.graphs = bool(graphs)
+        self._graphs = {}
 
     # ---- helpers ------------------------------------------------------------
     def _each(self, name, fn):
@@ -344,7 +352,7 @@ class BandUnwrap:
 
     @staticmethod
     def _c(b):
-        return (None, None) if b.W is None else (BandState.p(b.W, 0), BandState.p(b.W, 1))
+        return (None, None) if not b.use_w else (BandState.p(b.W, 0), BandState.p(b.W, 1))
 
     def _state_halo(self, idx_fn, with_dv=False):
         items = [(lambda b, f=idx_fn: f(b), 0, "both"), (lambda b, f=idx_fn: f(b), 1, "down")]
@@ -358,8 +366,10 @@ class BandUnwrap:
         P = BandState.p
         self._keep = []
         for b, xr in zip(self.bands, x_rows):
+            b.use_w = c is not None
             if c is not None:
-                b.W = _torch().zeros((2, b.rows + 2, b.ld), dtype=b.tdtype, device=b.device)
+                if b.W is None:  # kept across unwraps: captured graphs hold its address
+                    b.W = _torch().zeros((2, b.rows + 2, b.ld), dtype=b.tdtype, device=b.device)
                 nv = max(0, min(b.rows, b.n - 1 - b.row0))
                 self._keep += [b.pack_rows(c.cv, b.W, 0, b.row0, nv), b.pack_rows(c.ch, b.W, 1, b.row0, b.rows)]
             self._keep.append(xr)
@@ -379,6 +389,29 @@ class BandUnwrap:
 
     # ---- one outer iteration ------------------------------------------------------
     def step(self, k, m_cg, params: IrlsParams, lip, poll=16):
+        """irls.py:191-215 for iteration k (graph replay when enabled)."""
+        if not self.graphs or m_cg > 64:
+            return self._step(k, m_cg, params, lip, poll)
+        torch = _torch()
+        for b in self.bands:
+            b.ensure_norms(max(m_cg, 64))  # stable pointer across budgets
+        key = (m_cg, k & 1, self.bands[0].cur, float(lip), float(params.cg_rel_tol),
+               tuple(b.norms.data_ptr() for b in self.bands),
+               tuple(b.W.data_ptr() if b.use_w else 0 for b in self.bands))
+        g = self._graphs.get(key)
+        if g is None:
+            cur = [b.cur for b in self.bands]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=torch.cuda.Stream(device=self.bands[0].device)):
+                self._step(k, m_cg, params, lip, poll=None)
+            for b, c in zip(self.bands, cur):  # capture does not run the work
+                b.cur = c
+            self._graphs[key] = g
+        g.replay()
+        for b in self.bands:
+            b.cur = 1 - b.cur
+
+    def _step(self, k, m_cg, params: IrlsParams, lip, poll=16):
         P = BandState.p
         tol = float(params.cg_rel_tol)
         for b in self.bands:
@@ -401,7 +434,7 @@ class BandUnwrap:
             b.call("pu_pcg_rows_inv", b.send(), P(b.P[0]), P(b.P[1]), 1, _ptr(b.ctrl), -1, b.stream())
         self._dir_halo(0)
         for it in range(m_cg):
-            if it > 0 and it % poll == 0 and self._done():
+            if poll and it > 0 and it % poll == 0 and self._done():
                 break
             for b in self.bands:
                 pn, po = b.P[it & 1], b.P[(it + 1) & 1]
