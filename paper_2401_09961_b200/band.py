@@ -610,6 +610,7 @@ class RowSharded:
                 self._wire_peers()
             self.stream = torch.cuda.Stream(device=self.device)
         self.driver = BandUnwrap(self.bands, self.comm)
+        self._pins = {}
 
     def _wire_peers(self):
         """Every band learns the column-block address of every rank."""
@@ -647,8 +648,38 @@ class RowSharded:
         for r in self.ranks:
             lo, hi = self.rows_of(r)
             sl = torch.as_tensor(np.ascontiguousarray(x[lo:hi])) if isinstance(x, np.ndarray) else x[lo:hi]
+            if sl.device.type == "cpu" and not sl.is_pinned():
+                stage = self._pinned(("in", r), tuple(sl.shape), torch.float64)
+                stage.copy_(sl)  # multi-threaded host copy into page-locked staging
+                sl = stage
             xs.append(sl.to(device=self.device, dtype=torch.float64, non_blocking=True).contiguous())
         return xs
+
+    def _pinned(self, key, shape, dtype):
+        torch = _torch()
+        t = self._pins.get(key)
+        if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+            t = torch.empty(shape, dtype=dtype, pin_memory=True)
+            self._pins[key] = t
+        return t
+
+    def download(self, tensors):
+        """Device fp64 tensors -> fresh host numpy arrays through pinned staging."""
+        torch = _torch()
+        stream = torch.cuda.current_stream(self.device)
+        pins = []
+        for i, t in enumerate(tensors):
+            p = self._pinned(("out", i), tuple(t.shape), t.dtype)
+            p.copy_(t, non_blocking=True)
+            pins.append(p)
+        stream.synchronize()
+        out = []
+        for p in pins:
+            a = np.empty(tuple(p.shape), dtype=np.float64)
+            if a.size:
+                torch.from_numpy(a).copy_(p)
+            out.append(a)
+        return out
 
     def run(self, xs, c, params: IrlsParams, gradient_lo):
         """The full IRLS loop on the uploaded rows; returns the trace (results stay on the device)."""
@@ -702,11 +733,9 @@ def unwrap_rows(x, c: WeightField | None = None, model: ModelParams | None = Non
         if solver.distributed and gather:
             parts = _gather_bands(parts[0], solver.layout, group)
         if gather or not solver.distributed:
-            u = torch.cat([p[0] for p in parts]).cpu().numpy()
-            vv = torch.cat([p[1] for p in parts]).cpu().numpy()
-            vh = torch.cat([p[2] for p in parts]).cpu().numpy()
+            u, vv, vh = solver.download([torch.cat([p[i] for p in parts]) for i in range(3)])
         else:
-            u, vv, vh = (t.cpu().numpy() for t in parts[0])
+            u, vv, vh = solver.download([t.contiguous() for t in parts[0]])
     return UnwrapResult(u=u, vv=vv, vh=vh, trace=trace)
 
 
