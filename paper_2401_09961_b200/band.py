@@ -337,6 +337,7 @@ class BandUnwrap:
             graphs = isinstance(comm, LoopbackComm) or os.environ.get("PU_BAND_GRAPHS") == "1"
         self.graphs = bool(graphs)
         self._graphs = {}
+        self.replayed_kernels = 0  # library kernels run by graph replays (the capture counted the first)
 
     # ---- helpers ------------------------------------------------------------
     def _each(self, name, fn):
@@ -398,16 +399,20 @@ class BandUnwrap:
         key = (m_cg, k & 1, self.bands[0].cur, float(lip), float(params.cg_rel_tol),
                tuple(b.norms.data_ptr() for b in self.bands),
                tuple(b.W.data_ptr() if b.use_w else 0 for b in self.bands))
-        g = self._graphs.get(key)
-        if g is None:
+        entry = self._graphs.get(key)
+        if entry is None:
             cur = [b.cur for b in self.bands]
+            lib = self.bands[0].lib
+            n0 = lib.pu_launch_count()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=torch.cuda.Stream(device=self.bands[0].device)):
                 self._step(k, m_cg, params, lip, poll=None)
             for b, c in zip(self.bands, cur):  # capture does not run the work
                 b.cur = c
-            self._graphs[key] = g
-        g.replay()
+            entry = self._graphs[key] = (g, lib.pu_launch_count() - n0)
+        else:
+            self.replayed_kernels += entry[1]
+        entry[0].replay()
         for b in self.bands:
             b.cur = 1 - b.cur
 
