@@ -161,7 +161,7 @@ class Workspace:
             src = stage
         return src.to(self.device, non_blocking=True)
 
-    def download_system(self, x):
+    def download_system(self, x, out=None):
         """Device system vector -> fresh host fp64 numpy (u, vv, vh).
 
         The compact blocks move in the handle's dtype through persistent
@@ -183,12 +183,12 @@ class Workspace:
             outs.append((pin, dev))
             events.append(ev)
         res = []
-        for (p, _), ev in zip(outs, events):
+        for idx, ((p, _), ev) in enumerate(zip(outs, events)):
             # widen each block on the host while the next one is still in flight;
             # numpy's allocator madvises huge pages for large arrays (few page
             # faults); torch's multi-threaded copy widens fp32 -> fp64 into it
             ev.synchronize()
-            a = np.empty(tuple(p.shape), dtype=np.float64)
+            a = out[idx] if out is not None else np.empty(tuple(p.shape), dtype=np.float64)
             if a.size:
                 torch.from_numpy(a).copy_(p)
             res.append(a)

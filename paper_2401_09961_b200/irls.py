@@ -293,6 +293,22 @@ def unwrap(x, c: WeightField | None = None, model: ModelParams | None = None, pa
         raise ValueError(f"weight shapes {c.cv.shape}/{c.ch.shape} do not match grid {(n, m)}")
     if gradient_lo not in (0.0, 0, -np.pi):
         raise ValueError(f"lo must be 0 or -pi, got {gradient_lo!r}")
+    # the host is idle while the device loop runs: allocate and page in the
+    # result arrays meanwhile, so the final widening copy touches no new pages
+    import threading
+    outs = {}
+
+    def _prefault():
+        shapes = ((n, m), (n - 1, m), (n, m - 1))
+        arrs = [np.empty((max(r, 0), max(q, 0)), dtype=np.float64) for r, q in shapes]
+        for a in arrs:
+            if a.size:
+                torch.from_numpy(a).zero_()
+        outs["arrays"] = arrs
+
+    th = threading.Thread(target=_prefault, daemon=True)
+    th.start()
     run, trace = unwrap_device(x_dev, c, model, params, gradient_lo, dtype)
-    u, vv, vh = run.ws.download_system(run.state)
+    th.join()
+    u, vv, vh = run.ws.download_system(run.state, out=outs.get("arrays"))
     return UnwrapResult(u=u, vv=vv, vh=vh, trace=trace)
