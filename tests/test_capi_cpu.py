@@ -116,3 +116,33 @@ def test_weightfield_validation():
         WeightField(-np.ones((2, 3)), np.ones((3, 2)))
     with pytest.raises(ValueError):
         WeightField(np.zeros((2, 3)), np.zeros((3, 2)))
+
+
+def test_band_create_validates_before_cuda():
+    """pu_create_band rejects malformed bands with PU_ERR_ARG (no device needed)."""
+    import ctypes
+    lib = _native.load()
+    h = ctypes.c_void_p()
+
+    def band(**kw):
+        base = dict(n_glob=64, row0=0, rows=32, nq=2, mb=32, col0=0, cols=32)
+        base.update(kw)
+        return _native.PuBand(**base)
+
+    bad = [band(rows=0), band(row0=40), band(mb=12), band(nq=1, mb=32), band(col0=8), band(cols=40),
+           band(n_glob=1, rows=1)]
+    for b in bad:
+        assert lib.pu_create_band(ctypes.byref(h), 64, ctypes.byref(b), 0, 1e-2, 1e-6) == _native.PU_ERR_ARG
+    assert lib.pu_create_band(ctypes.byref(h), 64, ctypes.byref(band()), 0, -1.0, 1e-6) == _native.PU_ERR_ARG
+    assert lib.pu_create_band(ctypes.byref(h), 64, ctypes.byref(band()), 7, 1e-2, 1e-6) == _native.PU_ERR_ARG
+    assert lib.pu_create_band(ctypes.byref(h), 64, None, 0, 1e-2, 1e-6) == _native.PU_ERR_ARG
+
+
+def test_band_layout_partitions():
+    from paper_2401_09961_b200.band import BandLayout
+    for n, m, w in [(50, 45, 3), (16384, 16384, 8), (9, 100, 4), (4096, 4096, 5)]:
+        lay = BandLayout(n, m, w)
+        assert sum(lay.rows) == n and lay.row0[0] == 0
+        assert all(lay.row0[i] + lay.rows[i] == lay.row0[i + 1] for i in range(w - 1))
+        assert max(lay.rows) - min(lay.rows) <= 1
+        assert lay.mb % 8 == 0 and lay.mb * w >= m and sum(lay.cols) == m
