@@ -152,6 +152,20 @@ int pu_irls_step(pu_handle* h, void* state, const void* b, const void* gv, const
                  int max_iters, double rel_tol, void* cand, void* r, void* p0, void* p1, void* spec, void* ctrl,
                  double* res_norms, double* out, void* stream);
 
+/* pu_irls_step in two halves, so the host can run the first speculatively
+ * while it reads the previous iteration's scalars and applies the budget
+ * rule (irls.py:178-189): pu_irls_begin = candidate step + PCG start-up +
+ * z0 = M r0 (needs no budget; leaves the state untouched), pu_irls_iterate =
+ * the budget's iterations (in place on `state`) + the H pair.  Same
+ * arguments and outputs as pu_irls_step; each half is replayed as a graph. */
+int pu_irls_begin(pu_handle* h, void* state, const void* b, const void* gv, const void* gh, const void* cv,
+                  const void* ch, const void* wv, const void* wh, const void* dv, const void* dh, double lipschitz,
+                  double rel_tol, void* cand, void* r, void* p0, void* p1, void* spec, void* ctrl, double* res_norms,
+                  void* stream);
+int pu_irls_iterate(pu_handle* h, void* state, const void* gv, const void* gh, const void* cv, const void* ch,
+                    const void* wv, const void* wh, const void* dv, const void* dh, int max_iters, void* cand, void* r,
+                    void* p0, void* p1, void* spec, void* ctrl, double* res_norms, double* out, void* stream);
+
 /* CUDA-graph replay of pu_irls_step (default on): each (budget, pointers,
  * scalars) combination is captured once and relaunched as one graph when the
  * stream is not the legacy default stream and the budget is <= 64. */

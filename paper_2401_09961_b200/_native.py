@@ -49,6 +49,8 @@ SIGNATURES = {
     "pu_accept_center": (_i, [_vp] + [_vp] * 10 + [_vp, _vp]),
     "pu_pcg_solve": (_i, [_vp] + [_vp] * 10 + [_i, _d, _vp, _vp, _vp]),
     "pu_irls_step": (_i, [_vp] + [_vp] * 10 + [_d, _i, _d] + [_vp] * 7 + [_vp, _vp]),
+    "pu_irls_begin": (_i, [_vp] + [_vp] * 10 + [_d, _d] + [_vp] * 7 + [_vp]),
+    "pu_irls_iterate": (_i, [_vp] + [_vp] * 9 + [_i] + [_vp] * 7 + [_vp, _vp]),
     "pu_accept_weights": (_i, [_vp] + [_vp] * 15 + [_vp]),
     "pu_set_graphs": (_i, [_vp, _i]),
     "pu_timing_enable": (_i, [_vp, _i]),

@@ -46,6 +46,12 @@ static std::atomic<long long> g_launches{0};
     PU_CUDA(call);                                         \
   } while (0)
 
+#define PU_RC(call)                 \
+  do {                              \
+    const int rc_ = (call);         \
+    if (rc_ != PU_OK) return rc_;   \
+  } while (0)
+
 
 typedef long double ld_t;
 static const ld_t kPi = 3.141592653589793238462643383279502884L;
@@ -479,6 +485,14 @@ struct Impl : HandleBase {
   int pcg(const T* b, const T* x0, T* x, const T* dv, const T* dh, T* r, T* z, T* p0, T* p1, T* spec,
           int max_iters, double rel_tol, PcgCtrl* ctrl, double* norms, cudaStream_t st,
           const CandArgs<T>* cand = nullptr) {
+    PU_RC(pcg_setup(b, x0, x, dv, dh, r, p0, p1, spec, max_iters, rel_tol, ctrl, norms, st, cand));
+    return pcg_iterate(x, dv, dh, r, p0, p1, spec, max_iters, ctrl, norms, st);
+  }
+
+  // pcg.py:59-79: start-up (+ the candidate step) and z0 = M r0, p0 = z0
+  int pcg_setup(const T* b, const T* x0, T* x, const T* dv, const T* dh, T* r, T* p0, T* p1, T* spec,
+                int max_iters, double rel_tol, PcgCtrl* ctrl, double* norms, cudaStream_t st,
+                const CandArgs<T>* cand) {
     const int vg = vec_grid();
     cudaEvent_t e = tm.begin(st);
     if (cand) {
@@ -502,6 +516,15 @@ struct Impl : HandleBase {
     e = tm.begin(st);
     PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, pbuf[0], ctrl, pbuf[1], 1, Pack{}));
     tm.end(st, e, TK_K4, -1);
+    return PU_OK;
+  }
+
+  // pcg.py:81-108: the iterations of one budget
+  int pcg_iterate(T* x, const T* dv, const T* dh, T* r, T* p0, T* p1, T* spec, int max_iters, PcgCtrl* ctrl,
+                  double* norms, cudaStream_t st) {
+    const int vg = vec_grid();
+    cudaEvent_t e;
+    T* pbuf[2] = {p0, p1};
     const int chunk = 64;
     for (int it = 0; it < max_iters; ++it) {
       if (it > 0 && it % chunk == 0) {
@@ -922,6 +945,103 @@ int pu_accept_center(pu_handle* h, const void* xa, const void* xb, const double*
   return PU_OK;
 }
 
+}  // extern "C"
+
+// Replays `body` (which enqueues kernels on st) as a CUDA graph cached under
+// `key` when graphs are on and the stream is capturable; else runs it eagerly.
+template <typename I_t, typename F>
+static int run_graph(I_t& I, std::vector<unsigned long long> key, cudaStream_t st, bool eligible, F&& body) {
+  if (!I.use_graphs || st == nullptr || !eligible) return body();
+  key.push_back((unsigned long long)I.tm.on);
+  key.push_back((unsigned long long)(uintptr_t)st);
+  auto found = I.graphs.m.find(key);
+  if (found == I.graphs.m.end()) {
+    if (I.graphs.m.size() >= 96) I.graphs.clear();
+    GraphEntry ent;
+    I.tm.sink = &ent.timed;
+    PU_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    const long long l0 = g_launches.load();
+    const int rc = body();
+    ent.kernels = g_launches.load() - l0;
+    g_launches.fetch_sub(ent.kernels);  // counted per replay below
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    I.tm.sink = nullptr;
+    if (rc != PU_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
+    PU_CUDA(ce);
+    const cudaError_t ie = cudaGraphInstantiate(&ent.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    PU_CUDA(ie);
+    found = I.graphs.m.emplace(key, std::move(ent)).first;
+  }
+  PU_CUDA(cudaGraphLaunch(found->second.exec, st));
+  g_launches.fetch_add(found->second.kernels);
+  if (I.tm.on)
+    for (const auto& rec : found->second.timed) I.tm.recs.push_back(Timer::Rec{rec.kind, rec.it, rec.a, rec.b, false});
+  return PU_OK;
+}
+
+static unsigned long long dbits(double v) {
+  union { double d; unsigned long long u; } x{v};
+  return x.u;
+}
+#define PU_KP(p) ((unsigned long long)(uintptr_t)(p))
+
+// the budget of a loop whose start-up ran with a placeholder (pu_irls_begin)
+__global__ void k_set_max_iters(PcgCtrl* ctrl, int max_iters) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) ctrl->max_iters = max_iters;
+}
+
+extern "C" {
+
+int pu_irls_begin(pu_handle* h, void* state, const void* b, const void* gv, const void* gh, const void* cv,
+                  const void* ch, const void* wv, const void* wh, const void* dv, const void* dh, double lipschitz,
+                  double rel_tol, void* cand, void* r, void* p0, void* p1, void* spec, void* ctrl, double* res_norms,
+                  void* stream) {
+  if (rel_tol < 0) return fail(PU_ERR_ARG, "rel_tol must be >= 0");
+  if (!(lipschitz > 0)) return fail(PU_ERR_ARG, "lipschitz constant must be positive");
+  if ((cv == nullptr) != (ch == nullptr)) return fail(PU_ERR_ARG, "cv and ch must both be given or both NULL");
+  PU_DISPATCH(h, {
+    cudaStream_t st = ST(stream);
+    auto body = [&]() -> int {
+      const CandArgs<T> ca{CP(gv), CP(gh), CP(cv), CP(ch), CP(wv), CP(wh), (T)(-1.0 / lipschitz), MP(cand)};
+      // the budget is not known yet: a placeholder (never 0) until pu_irls_iterate sets it
+      return I.pcg_setup(CP(b), CP(state), MP(state), CP(dv), CP(dh), MP(r), MP(p0), MP(p1), MP(spec), 1 << 30,
+                         rel_tol, reinterpret_cast<PcgCtrl*>(ctrl), res_norms, st, &ca);
+    };
+    return run_graph(I, {1ull, dbits(lipschitz), dbits(rel_tol), PU_KP(state), PU_KP(b), PU_KP(gv), PU_KP(gh),
+                         PU_KP(cv), PU_KP(ch), PU_KP(wv), PU_KP(wh), PU_KP(dv), PU_KP(dh), PU_KP(cand), PU_KP(r),
+                         PU_KP(p0), PU_KP(p1), PU_KP(spec), PU_KP(ctrl), PU_KP(res_norms)},
+                     st, true, body);
+  });
+}
+
+int pu_irls_iterate(pu_handle* h, void* state, const void* gv, const void* gh, const void* cv, const void* ch,
+                    const void* wv, const void* wh, const void* dv, const void* dh, int max_iters, void* cand, void* r,
+                    void* p0, void* p1, void* spec, void* ctrl, double* res_norms, double* out, void* stream) {
+  if (max_iters < 0) return fail(PU_ERR_ARG, "max_iters must be >= 0");
+  if ((cv == nullptr) != (ch == nullptr)) return fail(PU_ERR_ARG, "cv and ch must both be given or both NULL");
+  PU_DISPATCH(h, {
+    cudaStream_t st = ST(stream);
+    auto body = [&]() -> int {
+      PcgCtrl* c = reinterpret_cast<PcgCtrl*>(ctrl);
+      k_set_max_iters<<<1, 32, 0, st>>>(c, max_iters);
+      PU_LAUNCH_CHECK();
+      PU_RC(I.pcg_iterate(MP(state), CP(dv), CP(dh), MP(r), MP(p0), MP(p1), MP(spec), max_iters, c, res_norms, st));
+      cudaEvent_t te_ = I.tm.begin(st);
+      k_hpair_states_v<T><<<I.vec_grid(), 256, 0, st>>>(I.g, CP(state), CP(cand), CP(wv), CP(wh), CP(gv), CP(gh),
+                                                         CP(cv), CP(ch), I.rs, S_HPAIR, out);
+      PU_LAUNCH_CHECK();
+      I.tm.end(st, te_, TK_HPAIR, -1);
+      return PU_OK;
+    };
+    return run_graph(I, {2ull, (unsigned long long)max_iters, PU_KP(state), PU_KP(gv), PU_KP(gh), PU_KP(cv),
+                         PU_KP(ch), PU_KP(wv), PU_KP(wh), PU_KP(dv), PU_KP(dh), PU_KP(cand), PU_KP(r), PU_KP(p0),
+                         PU_KP(p1), PU_KP(spec), PU_KP(ctrl), PU_KP(res_norms), PU_KP(out)},
+                     st, max_iters <= 64, body);
+  });
+}
+
 int pu_irls_step(pu_handle* h, void* state, const void* b, const void* gv, const void* gh, const void* cv,
                  const void* ch, const void* wv, const void* wh, const void* dv, const void* dh, double lipschitz,
                  int max_iters, double rel_tol, void* cand, void* r, void* p0, void* p1, void* spec, void* ctrl,
@@ -946,43 +1066,12 @@ int pu_irls_step(pu_handle* h, void* state, const void* b, const void* gv, const
     };
     // graphs need a capturable (non-legacy) stream and a budget that the
     // enqueue loop runs without polling (<= 64 iterations)
-    if (!I.use_graphs || st == nullptr || max_iters > 64) return body();
-    union { double d; unsigned long long u; } lp{lipschitz}, tl{rel_tol};
-    const std::vector<unsigned long long> key = {
-        (unsigned long long)max_iters, lp.u, tl.u, (unsigned long long)I.tm.on,
-        (unsigned long long)(uintptr_t)state, (unsigned long long)(uintptr_t)b, (unsigned long long)(uintptr_t)gv,
-        (unsigned long long)(uintptr_t)gh, (unsigned long long)(uintptr_t)cv, (unsigned long long)(uintptr_t)ch,
-        (unsigned long long)(uintptr_t)wv, (unsigned long long)(uintptr_t)wh, (unsigned long long)(uintptr_t)dv,
-        (unsigned long long)(uintptr_t)dh, (unsigned long long)(uintptr_t)cand, (unsigned long long)(uintptr_t)r,
-        (unsigned long long)(uintptr_t)p0, (unsigned long long)(uintptr_t)p1, (unsigned long long)(uintptr_t)spec,
-        (unsigned long long)(uintptr_t)ctrl, (unsigned long long)(uintptr_t)res_norms, (unsigned long long)(uintptr_t)out,
-        (unsigned long long)(uintptr_t)st};
-    auto found = I.graphs.m.find(key);
-    if (found == I.graphs.m.end()) {
-      if (I.graphs.m.size() >= 64) I.graphs.clear();
-      GraphEntry ent;
-      I.tm.sink = &ent.timed;
-      PU_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      const long long l0 = g_launches.load();
-      const int rc = body();
-      ent.kernels = g_launches.load() - l0;
-      g_launches.fetch_sub(ent.kernels);  // counted per replay below
-      cudaGraph_t graph = nullptr;
-      const cudaError_t ce = cudaStreamEndCapture(st, &graph);
-      I.tm.sink = nullptr;
-      if (rc != PU_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
-      PU_CUDA(ce);
-      const cudaError_t ie = cudaGraphInstantiate(&ent.exec, graph, 0);
-      cudaGraphDestroy(graph);
-      PU_CUDA(ie);
-      found = I.graphs.m.emplace(key, std::move(ent)).first;
-    }
-    PU_CUDA(cudaGraphLaunch(found->second.exec, st));
-    g_launches.fetch_add(found->second.kernels);
-    if (I.tm.on)
-      for (const auto& rec : found->second.timed) I.tm.recs.push_back(Timer::Rec{rec.kind, rec.it, rec.a, rec.b, false});
+    return run_graph(I, {0ull, (unsigned long long)max_iters, dbits(lipschitz), dbits(rel_tol), PU_KP(state),
+                         PU_KP(b), PU_KP(gv), PU_KP(gh), PU_KP(cv), PU_KP(ch), PU_KP(wv), PU_KP(wh), PU_KP(dv),
+                         PU_KP(dh), PU_KP(cand), PU_KP(r), PU_KP(p0), PU_KP(p1), PU_KP(spec), PU_KP(ctrl),
+                         PU_KP(res_norms), PU_KP(out)},
+                     st, max_iters <= 64, body);
   });
-  return PU_OK;
 }
 
 int pu_set_graphs(pu_handle* h, int on) {

@@ -203,6 +203,24 @@ class Workspace:
         n, m = self.n, self.m
         return self.unpack(x[0], n, m), self.unpack(x[1], n - 1, m), self.unpack(x[2], n, m - 1)
 
+    def snapshot(self):
+        """Enqueue a copy of the scalar block into pinned memory (read later with
+        read_snapshot, while the stream keeps going)."""
+        torch = _torch()
+        pin = self.pinned("block", tuple(self.block.shape), torch.uint8)
+        pin.copy_(self.block, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        self._snap = ev
+
+    def read_snapshot(self):
+        """Wait for the last snapshot only: (scalars[NSCAL], ctrl record)."""
+        self._snap.synchronize()
+        host = self.pinned("block", tuple(self.block.shape), _torch().uint8).numpy()
+        scal = host[: self.NSCAL * 8].view(np.float64).copy()
+        ctrl = host[self.NSCAL * 8:].view(self._ctrl_dtype)[0].copy()
+        return scal, ctrl
+
     def read_block(self):
         """Synchronising read of the scalar block: (scalars[NSCAL], ctrl record)."""
         host = self.block.cpu().numpy()

@@ -75,15 +75,33 @@ class DeviceUnwrap:
 
     def step(self, k, m_cg, params: IrlsParams, lip):
         """irls.py:191-215 for iteration k, then the weights of k + 1."""
+        self.begin(k, params, lip)
+        self.finish(k, m_cg, params)
+
+    def begin(self, k, params: IrlsParams, lip):
+        """The budget-independent half of iteration k (pu_irls_begin): candidate
+        step, PCG start-up, z0 = M r0.  Leaves the state untouched, so it may run
+        before the host has decided whether iteration k happens at all."""
+        ws, st = self.ws, self.ws.stream()
+        cv, ch = self._c()
+        w = self.Wt[k & 1]
+        norms = ws.ensure_norms(64)
+        ws.call("pu_irls_begin", _ptr(self.S[self.cur]), _ptr(self.B), _ptr(self.G[0]), _ptr(self.G[1]), cv, ch,
+                _ptr(w[0]), _ptr(w[1]), _ptr(self.D[0]), _ptr(self.D[1]), float(lip), float(params.cg_rel_tol),
+                _ptr(self.C), _ptr(self.R), _ptr(self.P[0]), _ptr(self.P[1]), _ptr(self.spec), _ptr(ws.ctrl),
+                _ptr(norms), st)
+
+    def finish(self, k, m_cg, params: IrlsParams):
+        """The budget's PCG iterations + H pair (pu_irls_iterate), then the
+        acceptance and the weights of k + 1 (pu_accept_weights)."""
         ws, st = self.ws, self.ws.stream()
         cv, ch = self._c()
         cur, nxt = self.S[self.cur], self.S[1 - self.cur]
         w, wn = self.Wt[k & 1], self.Wt[(k + 1) & 1]
-        norms = ws.ensure_norms(m_cg)
-        ws.call("pu_irls_step", _ptr(cur), _ptr(self.B), _ptr(self.G[0]), _ptr(self.G[1]), cv, ch, _ptr(w[0]),
-                _ptr(w[1]), _ptr(self.D[0]), _ptr(self.D[1]), float(lip), int(m_cg), float(params.cg_rel_tol),
-                _ptr(self.C), _ptr(self.R), _ptr(self.P[0]), _ptr(self.P[1]), _ptr(self.spec), _ptr(ws.ctrl),
-                _ptr(norms), ws.sp(ws.S_HPROP), st)
+        norms = ws.ensure_norms(max(m_cg, 64))
+        ws.call("pu_irls_iterate", _ptr(cur), _ptr(self.G[0]), _ptr(self.G[1]), cv, ch, _ptr(w[0]), _ptr(w[1]),
+                _ptr(self.D[0]), _ptr(self.D[1]), int(m_cg), _ptr(self.C), _ptr(self.R), _ptr(self.P[0]),
+                _ptr(self.P[1]), _ptr(self.spec), _ptr(ws.ctrl), _ptr(norms), ws.sp(ws.S_HPROP), st)
         ws.call("pu_accept_weights", _ptr(cur), _ptr(self.C), ws.sp(ws.S_MEAN), _ptr(nxt), _ptr(self.G[0]),
                 _ptr(self.G[1]), cv, ch, _ptr(w[0]), _ptr(w[1]), _ptr(wn[0]), _ptr(wn[1]), _ptr(self.D[0]),
                 _ptr(self.D[1]), ws.sp(ws.S_HACC), st)
@@ -150,16 +168,28 @@ class _LoopJob:
         self.pending = None  # (k, m_cg, delta_rel) of the enqueued iteration awaiting its scalars
         self.k = 0
         if params.max_outer_iters > 0:
-            self.run.step(0, self.m_history[0], params, self.lip)
+            self._enqueue(0, self.m_history[0])
             self.pending = (0, self.m_history[0], None)
             self.k = 1
+
+    def _enqueue(self, k, m_cg):
+        """finish iteration k, snapshot its scalars, and start k + 1 speculatively
+        (pu_irls_begin does not depend on the budget and leaves the state
+        untouched), so the GPU keeps working while the host reads the snapshot
+        and applies the budget rule."""
+        if k == 0:
+            self.run.begin(0, self.params, self.lip)
+        self.run.finish(k, m_cg, self.params)
+        self.ws.snapshot()
+        if k + 1 < self.params.max_outer_iters:
+            self.run.begin(k + 1, self.params, self.lip)
 
     def advance(self):
         """Returns True once the loop has finished (trace complete)."""
         if self.pending is None:
             return True
         ws, params = self.ws, self.params
-        scal, ctrl = ws.read_block()
+        scal, ctrl = ws.read_snapshot()
         self.trace.append(_record(*self.pending, scal, ctrl, ws))
         self.pending = None
         k = self.k
@@ -175,7 +205,7 @@ class _LoopJob:
             return True
         m_cg = decision.m_cg
         self.m_history.append(m_cg)
-        self.run.step(k, m_cg, params, self.lip)
+        self._enqueue(k, m_cg)
         self.pending = (k, m_cg, delta_rel)
         self.k = k + 1
         return False
