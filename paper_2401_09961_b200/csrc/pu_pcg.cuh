@@ -1,8 +1,9 @@
 // DCT preconditioner passes and the fused PCG iteration (sm_100a).
 //
-// One PCG iteration of pcg.py:81-108 is four kernels:
-//   K1 k_pcg_p_v   p <- beta p + z (z at it = 0); A p recomputed on the fly; p'Ap;
-//                  last block: alpha = rho / p'Ap, curvature exits (pcg.py:82-89)
+// One PCG iteration of pcg.py:81-108 is five kernels:
+//   K1 k_pcg_p_v   slack p_s <- beta p_s + z_s (z at it = 0; p_u came from K4);
+//                  p'Ap as a quadratic form; last block: alpha = rho / p'Ap,
+//                  curvature exits (pcg.py:82-89)
 //   K2a k_pcg_r_v  x += alpha p; r -= alpha A p (A p recomputed from p);
 //                  ||r||^2; slack preconditioner z_s = r_s / (d + 1/tau); rho_s;
 //                  last block: ||r|| exits            (pu_vec.cuh)
@@ -10,7 +11,7 @@
 //   K3 k_cols_spec column DCT-II, x tau/(lam_i + lam_j) with (0,0) -> 0,
 //                  rho_u = <r_hat, z_hat> (Parseval), column DCT-III;
 //                  last block: beta = (rho_s + rho_u) / rho
-//   K4 k_rows_pipe<true>  row DCT-III of T -> z_u (pu_pipe.cuh)
+//   K4 k_rows_pipe<true>  row DCT-III of T -> z_u, p_u = beta p_u + z_u (pu_pipe.cuh)
 // The standalone preconditioner (preconditioner.py:86-115) is K2..K4 with the
 // plain policies.  Every PCG kernel returns immediately once ctrl->done is set.
 #pragma once

@@ -6,11 +6,12 @@
 // padding (j >= m) is read as zero and written back as zero.
 //
 //   k_pcg_p_v     K1: slack p_s <- beta p_s + r_s / (d + 1/tau) (p_u came from
-//                 K4); A p from the stencil of the new p; p'Ap; alpha (pcg.py:82-89)
+//                 K4); p'Ap as the quadratic form of A; alpha (pcg.py:82-89)
 //   k_pcg_r_v     K2a: x += alpha p; r -= alpha A p; optional mean re-projection;
 //                 ||r||; rho_s = <r_s, r_s / (d + 1/tau)> (pcg.py:90-104,
 //                 preconditioner.py:115); the row DCT of r_u runs next (K2b)
-//   k_pcg_start_v x = x0, r = b - A x0, ||b||, ||r0|| (pcg.py:59-75)
+//   k_pcg_start_v x = x0, r = b - A x0, ||b||, ||r0||, rho_s of r0 (pcg.py:59-79),
+//                 optionally fused with the candidate step (objective.py:118-125)
 #pragma once
 
 #include "pu_kernels.cuh"
@@ -116,8 +117,8 @@ __global__ void k_ghost_pslack(Grid g, const T* __restrict__ r, const T* __restr
 // K1.  The u block of the new search direction, p_u = beta p_u_old + z_u, was
 // already written by the row DCT-III kernel (K4) of the previous iteration;
 // here the slack blocks follow: z_s = r_s / (d + 1/tau) (never stored) and
-// p_s = beta p_s_old + z_s (z_s at it = 0).  Then A p from the stencil of the
-// new p (neighbours recomputed the same way) and p'Ap.  (pcg.py:82-89, 102-108)
+// p_s = beta p_s_old + z_s (z_s at it = 0).  Then p'Ap of the new p from the
+// forward differences only (pcg.py:82-89, 102-108).
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(256, PU_MINB(T, 4)) k_pcg_p_v(Grid g, const T* __restrict__ r, const T* __restrict__ pold,
