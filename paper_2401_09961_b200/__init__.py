@@ -23,3 +23,14 @@ from .synth import SceneSpec, add_phase_noise, config_scene, generate_scene, wra
 from .wrapped import wrapped_gradients
 
 __version__ = "0.1.0"
+
+
+def release_workspaces():
+    """Free the cached per-size device workspaces (single-grid, concurrent and
+    row-sharded solvers); the next unwrap of a size plans it again."""
+    import gc
+    from .band import RowSharded
+    from .device import Workspace
+    Workspace.release_all()
+    RowSharded._cache.clear()
+    gc.collect()

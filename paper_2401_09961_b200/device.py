@@ -54,6 +54,13 @@ class Workspace:
                 cls._cache[key] = ws
             return ws
 
+    @classmethod
+    def release_all(cls):
+        """Drop every cached workspace (their HBM buffers and plans are freed once
+        no unwrap result refers to them)."""
+        with cls._lock:
+            cls._cache.clear()
+
     def __init__(self, n, m, dtype="fp64", tau=1e-2, delta=1e-6, device=None):
         self.lib = nat.ensure()
         torch = _torch()

@@ -153,3 +153,11 @@ def test_odd_sizes_vs_oracle(shape):
     res32 = pu.unwrap(x, dtype="fp32")
     f32 = port.f_l1(port.Triple(res32.u, res32.vv, res32.vh), gv, gh, *ones, 1e-2)
     assert abs(f32 - f_ref) <= max(1e-3 * f_ref, 1e-6)
+
+
+def test_release_workspaces_and_replan():
+    x = pu.wrap_scene(pu.generate_scene(pu.SceneSpec("ramp", 20, 16, 3.0, 4.0, 0)))
+    a = pu.unwrap(x, dtype="fp32")
+    pu.release_workspaces()
+    b = pu.unwrap(x, dtype="fp32")
+    np.testing.assert_array_equal(a.u, b.u)
