@@ -249,13 +249,16 @@ int pu_create_band(pu_handle** out, int m, const pu_band* band, int dtype, doubl
 /* Device fp64 [PU_NSITES * PU_MAX_SUMS_ABI] that receives band totals; NULL
  * restores single-grid finalisation. */
 int pu_set_band_totals(pu_handle* h, double* totals);
-/* Fused transpose: `table` (device, nq uint64) holds the address of every
- * rank's column block (N x mb, pitch mb) -- on this GPU, or a peer's block
- * mapped with pu_ipc_open over NVLink.  The row DCT-II then stores each
- * chunk straight into its owner's block and the row DCT-III fetches its rows
- * from them (spec_out / spec_in are ignored); the caller orders the kernels
- * across ranks (the all-reduces between them do).  NULL: packed buffers. */
-int pu_set_band_peers(pu_handle* h, const uint64_t* table);
+/* Fused transpose, push model (every cross-GPU access is a store): the
+ * device tables (nq uint64 each) hold every rank's column block (N x mb,
+ * pitch mb) and every rank's back buffer (packed rows, as spec_in) -- on this
+ * GPU, or a peer's mapped with pu_ipc_open over NVLink.  The row DCT-II
+ * stores each chunk straight into its owner's column block (spec_out is
+ * ignored), the column transform stores each output row into the owner's
+ * back buffer, and the row DCT-III reads its own back buffer (spec_in).  The
+ * caller orders the kernels across ranks (the all-reduces between them do).
+ * NULL, NULL: the packed all-to-all layout. */
+int pu_set_band_peers(pu_handle* h, const uint64_t* col_blocks, const uint64_t* back_buffers);
 /* CUDA IPC for the peer tables: a 64-byte handle of a pu_dev_alloc block,
  * opened in another process on a peer GPU. */
 int pu_ipc_handle(const void* dev_ptr, void* handle);

@@ -61,7 +61,7 @@ SIGNATURES = {
     # row-sharded grids (band.py)
     "pu_create_band": (_i, [ctypes.POINTER(_vp), _i, _vp, _i, _d, _d]),
     "pu_set_band_totals": (_i, [_vp, _vp]),
-    "pu_set_band_peers": (_i, [_vp, _vp]),
+    "pu_set_band_peers": (_i, [_vp, _vp, _vp]),
     "pu_ipc_handle": (_i, [_vp, _vp]),
     "pu_ipc_open": (_i, [_vp, ctypes.POINTER(_vp)]),
     "pu_ipc_close": (_i, [_vp]),

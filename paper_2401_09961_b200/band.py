@@ -112,15 +112,19 @@ class BandState:
         self.P = [z(3), z(3)]
         self.W, self.use_w = None, False
         self.peer = bool(peer)
-        self.col_ptr, self.peer_table, self._opened = None, None, []
+        self.col_ptr, self.back_ptr, self.peer_tables, self._opened = None, None, None, []
         if self.peer:
-            # fused transpose (pu_set_band_peers): the column block is a plain
-            # cudaMalloc block so other ranks can map it over NVLink (CUDA IPC)
-            ptr = ctypes.c_void_p()
-            with torch.cuda.device(device):
-                nat.check(self.lib.pu_dev_alloc(self.n * self.mb * (4 if self.code == nat.PU_F32 else 8),
-                                                ctypes.byref(ptr)))
-            self.col_ptr = ptr.value
+            # fused transpose (pu_set_band_peers): the column block and the back
+            # buffer are plain cudaMalloc blocks so other ranks can map them
+            # over NVLink (CUDA IPC) and store into them
+            esz = 4 if self.code == nat.PU_F32 else 8
+            ptrs = []
+            for elems in (self.n * self.mb, self.nq * self.rows * self.mb):
+                ptr = ctypes.c_void_p()
+                with torch.cuda.device(device):
+                    nat.check(self.lib.pu_dev_alloc(elems * esz, ctypes.byref(ptr)))
+                ptrs.append(ptr.value)
+            self.col_ptr, self.back_ptr = ptrs
             self.spec_send = self.spec_col = None
         else:
             self.spec_send = torch.zeros(self.nq * self.rows * self.mb, dtype=self.tdtype, device=device)
@@ -141,22 +145,24 @@ class BandState:
                 self.lib.pu_destroy(self.h)
             for q in getattr(self, "_opened", []):
                 self.lib.pu_ipc_close(ctypes.c_void_p(q))
-            if getattr(self, "col_ptr", None):
-                self.lib.pu_dev_free(ctypes.c_void_p(self.col_ptr))
+            for q in (getattr(self, "col_ptr", None), getattr(self, "back_ptr", None)):
+                if q:
+                    self.lib.pu_dev_free(ctypes.c_void_p(q))
         except Exception:
             pass
 
-    def set_peers(self, addresses):
-        """Column-block addresses of every rank (rank order) -> fused transpose."""
+    def set_peers(self, cols, backs):
+        """Column-block and back-buffer addresses of every rank (rank order) -> fused transpose."""
         torch = _torch()
-        self.peer_table = torch.tensor([int(a) for a in addresses], dtype=torch.int64, device=self.device)
-        nat.check(self.lib.pu_set_band_peers(self.h, _ptr(self.peer_table)))
+        self.peer_tables = torch.tensor([[int(a) for a in cols], [int(a) for a in backs]], dtype=torch.int64,
+                                        device=self.device)
+        nat.check(self.lib.pu_set_band_peers(self.h, _ptr(self.peer_tables[0]), _ptr(self.peer_tables[1])))
 
     def col(self):
         return ctypes.c_void_p(self.col_ptr) if self.peer else _ptr(self.spec_col)
 
     def send(self):
-        return ctypes.c_void_p(0) if self.peer else _ptr(self.spec_send)
+        return ctypes.c_void_p(self.back_ptr) if self.peer else _ptr(self.spec_send)
 
     # pointers -------------------------------------------------------------
     @staticmethod
@@ -618,28 +624,32 @@ class RowSharded:
         self._pins = {}
 
     def _wire_peers(self):
-        """Every band learns the column-block address of every rank."""
+        """Every band learns the column-block and back-buffer addresses of every rank."""
         if not self.distributed:
-            addrs = [b.col_ptr for b in self.bands]
+            cols, backs = [b.col_ptr for b in self.bands], [b.back_ptr for b in self.bands]
             for b in self.bands:
-                b.set_peers(addrs)
+                b.set_peers(cols, backs)
             return
         import torch.distributed as dist
         (b,) = self.bands
-        handle = ctypes.create_string_buffer(64)
-        nat.check(b.lib.pu_ipc_handle(ctypes.c_void_p(b.col_ptr), handle))
+        mine = []
+        for ptr in (b.col_ptr, b.back_ptr):
+            handle = ctypes.create_string_buffer(64)
+            nat.check(b.lib.pu_ipc_handle(ctypes.c_void_p(ptr), handle))
+            mine.append(bytes(handle.raw))
         handles = [None] * self.layout.world
-        dist.all_gather_object(handles, bytes(handle.raw), group=self.group)
-        addrs = []
+        dist.all_gather_object(handles, mine, group=self.group)
+        tables = ([], [])
         for q, hq in enumerate(handles):
-            if q == b.rank:
-                addrs.append(b.col_ptr)
-                continue
-            ptr = ctypes.c_void_p()
-            nat.check(b.lib.pu_ipc_open(ctypes.create_string_buffer(hq, 64), ctypes.byref(ptr)))
-            b._opened.append(ptr.value)
-            addrs.append(ptr.value)
-        b.set_peers(addrs)
+            for t, (own, h) in enumerate(zip((b.col_ptr, b.back_ptr), hq)):
+                if q == b.rank:
+                    tables[t].append(own)
+                    continue
+                ptr = ctypes.c_void_p()
+                nat.check(b.lib.pu_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(ptr)))
+                b._opened.append(ptr.value)
+                tables[t].append(ptr.value)
+        b.set_peers(*tables)
 
     def rows_of(self, r):
         """Rows of x band r reads: its own and the first row of the band below."""

@@ -352,6 +352,7 @@ struct Impl : HandleBase {
   Grid gc{};           // grid of the column transform (band: the column block, else g)
   Pack pk{};           // packed transpose layout of the band's spectrum (nq = 0: plain)
   int col0 = 0;        // first global column of the band's column block
+  Push push{};         // peer mode: K3 sends its output rows to their owners' buffers
 
   ~Impl() override {
     prow.release();
@@ -469,7 +470,7 @@ struct Impl : HandleBase {
   // ---- preconditioner passes ----
   int sylvester(const T* r, T* z, T* spec, cudaStream_t st) {
     PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, nullptr, nullptr, 0, Pack{}));
-    PU_DCT(cops.cols(MODE_API, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, nullptr, rs, S_K3, 0));
+    PU_DCT(cops.cols(MODE_API, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, nullptr, rs, S_K3, 0, Push{}));
     PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, z, nullptr, nullptr, 0, Pack{}));
     return PU_OK;
   }
@@ -509,7 +510,7 @@ struct Impl : HandleBase {
     PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl, nullptr, 0, Pack{}));
     tm.end(st, e, TK_K2B, -1);
     e = tm.begin(st);
-    PU_DCT(cops.cols(MODE_INIT, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, ctrl, rs, S_K3, -1));
+    PU_DCT(cops.cols(MODE_INIT, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, ctrl, rs, S_K3, -1, Push{}));
     tm.end(st, e, TK_K3, -1);
     // p of iteration k lives in pbuf[k & 1]; K4 writes its u block (p = z at k = 0)
     T* pbuf[2] = {p0, p1};
@@ -557,7 +558,7 @@ struct Impl : HandleBase {
       PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl, nullptr, 0, Pack{}));
       tm.end(st, e, TK_K2B, it);
       e = tm.begin(st);
-      PU_DCT(cops.cols(MODE_ITER, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, ctrl, rs, S_K3, it));
+      PU_DCT(cops.cols(MODE_ITER, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, ctrl, rs, S_K3, it, Push{}));
       tm.end(st, e, TK_K3, it);
       e = tm.begin(st);  // u block of p for iteration it + 1: beta p_u + z_u
       PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, pbuf[(it + 1) & 1], ctrl, pn, 0, Pack{}));
@@ -620,7 +621,7 @@ struct Impl : HandleBase {
   int pcg_columns(T* spec, PcgCtrl* ctrl, int it, cudaStream_t st) {
     cudaEvent_t e = tm.begin(st);
     PU_DCT(cops.cols(it < 0 ? MODE_INIT : MODE_ITER, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec,
-                     ctrl, rs, S_K3, it));
+                     ctrl, rs, S_K3, it, push));
     tm.end(st, e, TK_K3, it);
     return PU_OK;
   }
@@ -628,7 +629,9 @@ struct Impl : HandleBase {
   // K4: u block of the next direction, pnew_u = beta pold_u + DCT-III rows (first: no axpy)
   int pcg_rows_inv(const T* spec_in, T* pnew, const T* pold, int first, PcgCtrl* ctrl, int it, cudaStream_t st) {
     cudaEvent_t e = tm.begin(st);
-    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec_in, pnew, ctrl, pold, first, pk));
+    Pack local = pk;  // the packed rows come from the local buffer (pushed there by K3 in peer mode)
+    local.peers = nullptr;
+    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec_in, pnew, ctrl, pold, first, local));
     tm.end(st, e, TK_K4, it);
     return PU_OK;
   }
@@ -1153,10 +1156,14 @@ int pu_create_band(pu_handle** out, int m, const pu_band* b, int dtype, double t
   return PU_OK;
 }
 
-int pu_set_band_peers(pu_handle* h, const uint64_t* table) {
+int pu_set_band_peers(pu_handle* h, const uint64_t* col_blocks, const uint64_t* back_buffers) {
+  if ((col_blocks == nullptr) != (back_buffers == nullptr)) return fail(PU_ERR_ARG, "give both tables or neither");
   PU_DISPATCH(h, {
     if (!I.band) return fail(PU_ERR_ARG, "pu_set_band_peers needs a band handle");
-    I.pk.peers = reinterpret_cast<const unsigned long long*>(table);
+    I.pk.peers = reinterpret_cast<const unsigned long long*>(col_blocks);
+    const int nq = I.pk.nq;
+    I.push = Push{reinterpret_cast<const unsigned long long*>(back_buffers), I.g.n_glob / nq, I.g.n_glob % nq,
+                  I.pk.mb, I.col0 / I.pk.mb};
   });
   return PU_OK;
 }

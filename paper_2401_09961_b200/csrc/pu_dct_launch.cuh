@@ -27,7 +27,7 @@ struct DctLaunch {
                                const PcgCtrl* ctrl, const T* pold, int first, Pack pk);
   static int rows_pipe_blocks_per_sm(int threads, size_t smem);
   static cudaError_t cols(int mode, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const T* lam_cols,
-                          int cpc, T* data, PcgCtrl* ctrl, RedScratch rs, int site, int it);
+                          int cpc, T* data, PcgCtrl* ctrl, RedScratch rs, int site, int it, Push ps);
 };
 
 #ifdef PU_DCT_DEFINE
@@ -66,13 +66,13 @@ int DctLaunch<T, LS>::rows_pipe_blocks_per_sm(int threads, size_t smem) {
 template <typename T, int LS>
 cudaError_t DctLaunch<T, LS>::cols(int mode, const XLaunch& c, const Grid& g, const FftPlan<T>& pl,
                                    const T* lam_cols, int cpc, T* data, PcgCtrl* ctrl, RedScratch rs, int site,
-                                   int it) {
+                                   int it, Push ps) {
   if (mode == MODE_API)
-    k_cols_spec<T, EM, LS, MODE_API><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it);
+    k_cols_spec<T, EM, LS, MODE_API><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it, ps);
   else if (mode == MODE_INIT)
-    k_cols_spec<T, EM, LS, MODE_INIT><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it);
+    k_cols_spec<T, EM, LS, MODE_INIT><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it, ps);
   else
-    k_cols_spec<T, EM, LS, MODE_ITER><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it);
+    k_cols_spec<T, EM, LS, MODE_ITER><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it, ps);
   return cudaGetLastError();
 }
 #endif  // PU_DCT_DEFINE

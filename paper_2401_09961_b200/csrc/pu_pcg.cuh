@@ -77,10 +77,34 @@ __device__ __forceinline__ void panel_load(const Grid& g, const FftPlan<T>& pl, 
   }
 }
 
+// Row-sharded push mode (band.py, peer transpose): the column transform sends
+// each output row straight to the packed input buffer of the rank that owns
+// the row (element (local row i_r, column q mb + j) of rank r's band at
+// q rows_r mb + i_r mb + j), so every cross-GPU access of the fused
+// transpose is a store.  backs == null: write the column block in place.
+struct Push {
+  const unsigned long long* backs;  // device: every rank's back-buffer address
+  int base, extra;                  // row bands: rows_r = base + (r < extra)
+  int mb, q;                        // chunk width; this rank's chunk index
+};
+
+// destination row pointer of global row i
+template <typename T>
+__device__ __forceinline__ T* push_row(const Push& ps, int i) {
+  const int big = ps.base + 1, cut = ps.extra * big;
+  int r, ir, rows;
+  if (i < cut) {
+    r = i / big; ir = i - r * big; rows = big;
+  } else {
+    r = ps.extra + (i - cut) / ps.base; ir = i - cut - (r - ps.extra) * ps.base; rows = ps.base;
+  }
+  return reinterpret_cast<T*>(__ldg(ps.backs + r)) + (long long)ps.q * rows * ps.mb + (long long)ir * ps.mb;
+}
+
 // inverse of panel_load after the DCT-III FFT: column 2s = Re/n, 2s+1 = -Im/n
 template <typename T>
 __device__ __forceinline__ void panel_store(const Grid& g, const FftPlan<T>& pl, T* data, int j0, int W, int ncols,
-                                            int nseq, const cplx<T>* buf, const int n) {
+                                            int nseq, const cplx<T>* buf, const int n, const Push& ps) {
   using V = typename V16<T>::type;
   constexpr int VN = V16<T>::N;
   if (ncols == W && W % VN == 0) {
@@ -97,14 +121,16 @@ __device__ __forceinline__ void panel_store(const Grid& g, const FftPlan<T>& pl,
         const cplx<T> a = buf[v * pl.ldseq + p];
         o.x = a.x; o.y = -a.y;
       }
-      *reinterpret_cast<V*>(data + (long long)i * g.ld + j0 + v * VN) = o;
+      T* row = ps.backs ? push_row<T>(ps, i) : data + (long long)i * g.ld;
+      *reinterpret_cast<V*>(row + j0 + v * VN) = o;
     }
   } else {
     for (int e = threadIdx.x; e < n * 2 * nseq; e += blockDim.x) {
       const int i = e / (2 * nseq), c = e - i * (2 * nseq);
       if (c < ncols) {
         const cplx<T> v = buf[(c >> 1) * pl.ldseq + spad(mperm(i, n))];
-        data[(long long)i * g.ld + j0 + c] = (c & 1) ? -v.y : v.x;
+        T* row = ps.backs ? push_row<T>(ps, i) : data + (long long)i * g.ld;
+        row[j0 + c] = (c & 1) ? -v.y : v.x;
       }
     }
   }
@@ -117,7 +143,7 @@ __device__ __forceinline__ void panel_store(const Grid& g, const FftPlan<T>& pl,
 // ---------------------------------------------------------------------------
 template <typename T, int EMAX, int LS, int MODE>
 __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, EMAX)) k_cols_spec(Grid g, FftPlan<T> pl, const T* __restrict__ lam_cols, int cols_per_cta, T* data,
-                            PcgCtrl* ctrl, RedScratch rs, int site, int it) {
+                            PcgCtrl* ctrl, RedScratch rs, int site, int it, Push ps) {
   extern __shared__ __align__(16) unsigned char smraw[];
   cplx<T>* buf = reinterpret_cast<cplx<T>*>(smraw);
   if (MODE != MODE_API && ctrl->done) return;
@@ -162,7 +188,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   }
   __syncthreads();
   fft_n<T, EMAX, LS>(buf, nseq, pl);
-  panel_store<T>(g, pl, data, j0, W, ncols, nseq, buf, n);
+  panel_store<T>(g, pl, data, j0, W, ncols, nseq, buf, n, ps);
   if (MODE != MODE_API) {
     double acc[1] = {(double)accT};
     double tot[1];
