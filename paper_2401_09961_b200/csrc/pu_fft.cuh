@@ -373,6 +373,25 @@ __device__ __forceinline__ void fft_stages_s(cplx<T>* buf, int seq0, int nseq, c
   }
 }
 
+// Stages NS in [NS, STOP) of the static plan (the column kernel runs the
+// first / last stage itself, straight from / to global memory).
+template <typename T, int EMAX, int L, int NS, int OFF, int STOP>
+__device__ __forceinline__ void fft_stages_range(cplx<T>* buf, int seq0, int nseq, const cplx<T>* stw) {
+  if constexpr (NS < STOP) {
+    constexpr int R = (NS == 1) ? first_radix<L, EMAX>() : (EMAX >= 16 ? 16 : 8);
+    fft_stage_s<T, R, EMAX, L, NS, OFF>(buf, seq0, nseq, stw);
+    fft_stages_range<T, EMAX, L, NS * R, (NS == 1 ? OFF : OFF + NS), STOP>(buf, seq0, nseq, stw);
+  }
+}
+
+// offset of stage NS's twiddle block in pl.stw (mirrors fft_stages_s)
+template <int L, int EMAX>
+__host__ __device__ constexpr int stage_off(int target) {
+  int ns = first_radix<L, EMAX>(), off = 0;
+  while (ns < target) { off += ns; ns *= (EMAX >= 16 ? 16 : 8); }
+  return off;
+}
+
 // Forward FFT of internal length L on all sequences; LS > 0 selects the
 // compile-time plan (requires pl.L == LS), LS == 0 the runtime plan.
 template <typename T, int EMAX, int LS>

@@ -138,6 +138,79 @@ __device__ __forceinline__ void panel_store(const Grid& g, const FftPlan<T>& pl,
 }
 
 // ---------------------------------------------------------------------------
+// Static column plans with a twiddle-free radix-EMAX first stage (one
+// butterfly per thread, e.g. 4096 = 16^3 fp32, 8^4 fp64): the first forward
+// stage reads its butterfly straight from global memory and the last inverse
+// stage stores straight to global memory, so the panel never makes the extra
+// shared-memory round trip of panel_load / panel_store.  Thread t works on
+// sequence t % NSEQ, butterfly t / NSEQ: the NSEQ threads of one butterfly
+// index cover one full 2 NSEQ-column row segment (32 bytes).
+// Makhoul order: FFT index idx holds row 2 idx (idx < L/2) or
+// 2L - 1 - 2 idx (idx >= L/2); butterfly j's inputs / last-stage outputs sit
+// at idx = j + r L/R, so rows are 2 j + 2 r L/R (r < R/2) and
+// 2L - 1 - 2 j - 2 r L/R.
+// ---------------------------------------------------------------------------
+template <int L, int EMAX>
+__host__ __device__ constexpr bool col_fused_ok() {
+  constexpr int big = EMAX >= 16 ? 16 : 8;
+  return first_radix<L, EMAX>() == EMAX && L >= EMAX * big && (L / big) % 16 == 0;
+}
+
+template <typename T, int EMAX, int L>
+__device__ __forceinline__ void col_first_stage(const Grid& g, const T* __restrict__ data, int j0, cplx<T>* buf) {
+  constexpr int R = EMAX, NB = L / R, NSEQ = static_panel_cols(L, EMAX) / 2, LD = ldseq_for(L);
+  const int s = threadIdx.x % NSEQ, j = threadIdx.x / NSEQ;
+  const long long ld = g.ld, step = 2LL * NB * ld;
+  const T* pa = data + (long long)(2 * j) * ld + j0 + 2 * s;
+  const T* pb = data + (long long)(2 * L - 1 - 2 * j) * ld + j0 + 2 * s;
+  cplx<T> v[R];
+#pragma unroll
+  for (int r = 0; r < R / 2; ++r) v[r] = __ldg(reinterpret_cast<const cplx<T>*>(pa + r * step));
+#pragma unroll
+  for (int r = R / 2; r < R; ++r) v[r] = __ldg(reinterpret_cast<const cplx<T>*>(pb - r * step));
+  Dft<T, R>::run(v);
+  cplx<T>* dst = buf + s * LD + spad(j * R);  // spad(j R + r) = spad(j R) + r for R in {8, 16}
+#pragma unroll
+  for (int r = 0; r < R; ++r) dst[r] = v[r];
+  __syncthreads();
+}
+
+// last inverse stage (NS = L / R, one butterfly per thread): twiddle, DFT,
+// store column 2s = Re, 2s + 1 = -Im (as panel_store) of each output row
+template <typename T, int EMAX, int L>
+__device__ __forceinline__ void col_last_stage(const Grid& g, T* data, int j0, const cplx<T>* buf,
+                                               const cplx<T>* __restrict__ stw, const Push& ps) {
+  constexpr int R = EMAX >= 16 ? 16 : 8, NS = L / R, NSEQ = static_panel_cols(L, EMAX) / 2, LD = ldseq_for(L);
+  constexpr int OFF = stage_off<L, EMAX>(NS);
+  const int s = threadIdx.x % NSEQ, j = threadIdx.x / NSEQ;
+  const cplx<T>* src = buf + s * LD + spad(j);
+  cplx<T> v[R], w[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = src[r * (NS + NS / 16)];
+  w[1] = __ldg(stw + OFF + j);
+#pragma unroll
+  for (int r = 2; r < R; ++r) w[r] = cmul<T>(w[r / 2], w[r - r / 2]);
+#pragma unroll
+  for (int r = 1; r < R; ++r) v[r] = cmul<T>(v[r], w[r]);
+  Dft<T, R>::run(v);
+  if (ps.backs) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = r < R / 2 ? 2 * j + 2 * r * NS : 2 * L - 1 - 2 * j - 2 * r * NS;
+      *reinterpret_cast<cplx<T>*>(push_row<T>(ps, i) + j0 + 2 * s) = mk<T>(v[r].x, -v[r].y);
+    }
+  } else {
+    const long long ld = g.ld, step = 2LL * NS * ld;
+    T* pa = data + (long long)(2 * j) * ld + j0 + 2 * s;
+    T* pb = data + (long long)(2 * L - 1 - 2 * j) * ld + j0 + 2 * s;
+#pragma unroll
+    for (int r = 0; r < R / 2; ++r) *reinterpret_cast<cplx<T>*>(pa + r * step) = mk<T>(v[r].x, -v[r].y);
+#pragma unroll
+    for (int r = R / 2; r < R; ++r) *reinterpret_cast<cplx<T>*>(pb - r * step) = mk<T>(v[r].x, -v[r].y);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K3 / API: column DCT-II, spectral division, column DCT-III, in place on a
 // panel of `cols_per_cta` columns; reduces rho_u = <r_hat, z_hat>.
 // ---------------------------------------------------------------------------
@@ -153,9 +226,19 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   const int j0 = blockIdx.x * W;
   const int ncols = min(W, g.m - j0);
   const int nseq = (ncols + 1) >> 1;
-  panel_load<T>(g, pl, data, j0, W, ncols, nseq, buf, n);
-  __syncthreads();
-  fft_n<T, EMAX, LS>(buf, nseq, pl);
+  constexpr bool FUSE = LS > 0 && col_fused_ok<(LS > 0 ? LS : 4096), EMAX>();
+  constexpr int LF = LS > 0 ? LS : 4096;  // (LS == 0: FUSE is false, LF unused)
+  const bool fuse = FUSE && ncols == W;
+  if (fuse) {
+    if constexpr (FUSE) {
+      col_first_stage<T, EMAX, LF>(g, data, j0, buf);
+      fft_stages_range<T, EMAX, LF, EMAX, 0, LF>(buf, 0, nseq, pl.stw);
+    }
+  } else {
+    panel_load<T>(g, pl, data, j0, W, ncols, nseq, buf, n);
+    __syncthreads();
+    fft_n<T, EMAX, LS>(buf, nseq, pl);
+  }
   T accT = (T)0;  // per-thread partial of rho_u in T (a few dozen terms), fp64 across threads
   const int half = n / 2 + 1;
   const double tau = g.tau;
@@ -187,8 +270,15 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
     if (nk != k) sb[spad(nk)] = cnk;
   }
   __syncthreads();
-  fft_n<T, EMAX, LS>(buf, nseq, pl);
-  panel_store<T>(g, pl, data, j0, W, ncols, nseq, buf, n, ps);
+  if (fuse) {
+    if constexpr (FUSE) {
+      fft_stages_range<T, EMAX, LF, 1, 0, LF / (EMAX >= 16 ? 16 : 8)>(buf, 0, nseq, pl.stw);
+      col_last_stage<T, EMAX, LF>(g, data, j0, buf, pl.stw, ps);
+    }
+  } else {
+    fft_n<T, EMAX, LS>(buf, nseq, pl);
+    panel_store<T>(g, pl, data, j0, W, ncols, nseq, buf, n, ps);
+  }
   if (MODE != MODE_API) {
     double acc[1] = {(double)accT};
     double tot[1];
