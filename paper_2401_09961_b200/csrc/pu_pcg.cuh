@@ -138,13 +138,12 @@ __device__ __forceinline__ void panel_store(const Grid& g, const FftPlan<T>& pl,
 }
 
 // ---------------------------------------------------------------------------
-// Static column plans with a twiddle-free radix-EMAX first stage (one
-// butterfly per thread, e.g. 4096 = 16^3 fp32, 8^4 fp64): the first forward
+// Static (power-of-two) column plans: the first forward
 // stage reads its butterfly straight from global memory and the last inverse
 // stage stores straight to global memory, so the panel never makes the extra
 // shared-memory round trip of panel_load / panel_store.  Thread t works on
 // sequence t % NSEQ, butterfly t / NSEQ: the NSEQ threads of one butterfly
-// index cover one full 2 NSEQ-column row segment (32 bytes).
+// index cover one full 2 NSEQ-column row segment (up to 32 bytes).
 // Makhoul order: FFT index idx holds row 2 idx (idx < L/2) or
 // 2L - 1 - 2 idx (idx >= L/2); butterfly j's inputs / last-stage outputs sit
 // at idx = j + r L/R, so rows are 2 j + 2 r L/R (r < R/2) and
@@ -153,25 +152,35 @@ __device__ __forceinline__ void panel_store(const Grid& g, const FftPlan<T>& pl,
 template <int L, int EMAX>
 __host__ __device__ constexpr bool col_fused_ok() {
   constexpr int big = EMAX >= 16 ? 16 : 8;
-  return first_radix<L, EMAX>() == EMAX && L >= EMAX * big && (L / big) % 16 == 0;
+  constexpr int r0 = first_radix<L, EMAX>();
+  return (r0 == 2 || r0 == 4 || r0 == 8 || r0 == 16) && EMAX % r0 == 0 && L >= r0 * big && (L / big) % 16 == 0;
 }
 
+// first forward stage, Q = EMAX / R butterflies per thread (all loads in flight first)
 template <typename T, int EMAX, int L>
 __device__ __forceinline__ void col_first_stage(const Grid& g, const T* __restrict__ data, int j0, cplx<T>* buf) {
-  constexpr int R = EMAX, NB = L / R, NSEQ = static_panel_cols(L, EMAX) / 2, LD = ldseq_for(L);
-  const int s = threadIdx.x % NSEQ, j = threadIdx.x / NSEQ;
+  constexpr int R = first_radix<L, EMAX>(), Q = EMAX / R, NB = L / R;
+  constexpr int NSEQ = static_panel_cols(L, EMAX) / 2, LD = ldseq_for(L);
   const long long ld = g.ld, step = 2LL * NB * ld;
-  const T* pa = data + (long long)(2 * j) * ld + j0 + 2 * s;
-  const T* pb = data + (long long)(2 * L - 1 - 2 * j) * ld + j0 + 2 * s;
-  cplx<T> v[R];
+  cplx<T> v[Q][R];
 #pragma unroll
-  for (int r = 0; r < R / 2; ++r) v[r] = __ldg(reinterpret_cast<const cplx<T>*>(pa + r * step));
+  for (int q = 0; q < Q; ++q) {
+    const int b = threadIdx.x + q * blockDim.x, s = b % NSEQ, j = b / NSEQ;
+    const T* pa = data + (long long)(2 * j) * ld + j0 + 2 * s;
+    const T* pb = data + (long long)(2 * L - 1 - 2 * j) * ld + j0 + 2 * s;
 #pragma unroll
-  for (int r = R / 2; r < R; ++r) v[r] = __ldg(reinterpret_cast<const cplx<T>*>(pb - r * step));
-  Dft<T, R>::run(v);
-  cplx<T>* dst = buf + s * LD + spad(j * R);  // spad(j R + r) = spad(j R) + r for R in {8, 16}
+    for (int r = 0; r < R / 2; ++r) v[q][r] = __ldg(reinterpret_cast<const cplx<T>*>(pa + r * step));
 #pragma unroll
-  for (int r = 0; r < R; ++r) dst[r] = v[r];
+    for (int r = R / 2; r < R; ++r) v[q][r] = __ldg(reinterpret_cast<const cplx<T>*>(pb - r * step));
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int b = threadIdx.x + q * blockDim.x, s = b % NSEQ, j = b / NSEQ;
+    Dft<T, R>::run(v[q]);
+    cplx<T>* dst = buf + s * LD + spad(j * R);  // spad(j R + r) = spad(j R) + r for R | 16
+#pragma unroll
+    for (int r = 0; r < R; ++r) dst[r] = v[q][r];
+  }
   __syncthreads();
 }
 
@@ -232,7 +241,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   if (fuse) {
     if constexpr (FUSE) {
       col_first_stage<T, EMAX, LF>(g, data, j0, buf);
-      fft_stages_range<T, EMAX, LF, EMAX, 0, LF>(buf, 0, nseq, pl.stw);
+      fft_stages_range<T, EMAX, LF, first_radix<LF, EMAX>(), 0, LF>(buf, 0, nseq, pl.stw);
     }
   } else {
     panel_load<T>(g, pl, data, j0, W, ncols, nseq, buf, n);

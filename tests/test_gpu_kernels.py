@@ -81,7 +81,7 @@ def test_sylvester_golden(golden_kernels, shape):
                                    (2048, 2), (1, 4096), (4095, 3), (97, 1000),
                                    # columns through the fused global-memory first / last FFT stage
                                    # (4096 fp32 / fp64, 256 fp32, 512 fp64) with a ragged last panel
-                                   (4096, 22), (256, 13), (512, 7)])
+                                   (4096, 22), (256, 13), (512, 7), (2048, 10), (1024, 9), (8192, 6)])
 def test_sylvester_vs_dct_oracle(rng, shape):
     n, m = shape
     r = rng.standard_normal((n, m))
