@@ -166,6 +166,7 @@ __device__ __forceinline__ void col_first_stage(const Grid& g, const T* __restri
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
     const int b = threadIdx.x + q * blockDim.x, s = b % NSEQ, j = b / NSEQ;
+    if (b >= NSEQ * NB) break;  // CTAs may be rounded up
     const T* pa = data + (long long)(2 * j) * ld + j0 + 2 * s;
     const T* pb = data + (long long)(2 * L - 1 - 2 * j) * ld + j0 + 2 * s;
 #pragma unroll
@@ -176,6 +177,7 @@ __device__ __forceinline__ void col_first_stage(const Grid& g, const T* __restri
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
     const int b = threadIdx.x + q * blockDim.x, s = b % NSEQ, j = b / NSEQ;
+    if (b >= NSEQ * NB) break;
     Dft<T, R>::run(v[q]);
     cplx<T>* dst = buf + s * LD + spad(j * R);  // spad(j R + r) = spad(j R) + r for R | 16
 #pragma unroll
@@ -192,30 +194,32 @@ __device__ __forceinline__ void col_last_stage(const Grid& g, T* data, int j0, c
   constexpr int R = EMAX >= 16 ? 16 : 8, NS = L / R, NSEQ = static_panel_cols(L, EMAX) / 2, LD = ldseq_for(L);
   constexpr int OFF = stage_off<L, EMAX>(NS);
   const int s = threadIdx.x % NSEQ, j = threadIdx.x / NSEQ;
-  const cplx<T>* src = buf + s * LD + spad(j);
-  cplx<T> v[R], w[R];
+  if (j < NS) {  // CTAs may be rounded up (no early return: a grid reduction follows)
+    const cplx<T>* src = buf + s * LD + spad(j);
+    cplx<T> v[R], w[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) v[r] = src[r * (NS + NS / 16)];
-  w[1] = __ldg(stw + OFF + j);
+    for (int r = 0; r < R; ++r) v[r] = src[r * (NS + NS / 16)];
+    w[1] = __ldg(stw + OFF + j);
 #pragma unroll
-  for (int r = 2; r < R; ++r) w[r] = cmul<T>(w[r / 2], w[r - r / 2]);
+    for (int r = 2; r < R; ++r) w[r] = cmul<T>(w[r / 2], w[r - r / 2]);
 #pragma unroll
-  for (int r = 1; r < R; ++r) v[r] = cmul<T>(v[r], w[r]);
-  Dft<T, R>::run(v);
-  if (ps.backs) {
+    for (int r = 1; r < R; ++r) v[r] = cmul<T>(v[r], w[r]);
+    Dft<T, R>::run(v);
+    if (ps.backs) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = r < R / 2 ? 2 * j + 2 * r * NS : 2 * L - 1 - 2 * j - 2 * r * NS;
-      *reinterpret_cast<cplx<T>*>(push_row<T>(ps, i) + j0 + 2 * s) = mk<T>(v[r].x, -v[r].y);
+      for (int r = 0; r < R; ++r) {
+        const int i = r < R / 2 ? 2 * j + 2 * r * NS : 2 * L - 1 - 2 * j - 2 * r * NS;
+        *reinterpret_cast<cplx<T>*>(push_row<T>(ps, i) + j0 + 2 * s) = mk<T>(v[r].x, -v[r].y);
+      }
+    } else {
+      const long long ld = g.ld, step = 2LL * NS * ld;
+      T* pa = data + (long long)(2 * j) * ld + j0 + 2 * s;
+      T* pb = data + (long long)(2 * L - 1 - 2 * j) * ld + j0 + 2 * s;
+#pragma unroll
+      for (int r = 0; r < R / 2; ++r) *reinterpret_cast<cplx<T>*>(pa + r * step) = mk<T>(v[r].x, -v[r].y);
+#pragma unroll
+      for (int r = R / 2; r < R; ++r) *reinterpret_cast<cplx<T>*>(pb - r * step) = mk<T>(v[r].x, -v[r].y);
     }
-  } else {
-    const long long ld = g.ld, step = 2LL * NS * ld;
-    T* pa = data + (long long)(2 * j) * ld + j0 + 2 * s;
-    T* pb = data + (long long)(2 * L - 1 - 2 * j) * ld + j0 + 2 * s;
-#pragma unroll
-    for (int r = 0; r < R / 2; ++r) *reinterpret_cast<cplx<T>*>(pa + r * step) = mk<T>(v[r].x, -v[r].y);
-#pragma unroll
-    for (int r = R / 2; r < R; ++r) *reinterpret_cast<cplx<T>*>(pb - r * step) = mk<T>(v[r].x, -v[r].y);
   }
 }
 

@@ -61,6 +61,48 @@ __host__ __device__ constexpr size_t rows_pipe_smem(int n, int tsize, int ldseq,
   return 128 + (size_t)rows_staged * stage_row_bytes(n, tsize) + (size_t)ldseq * 2 * tsize;
 }
 
+// Forward row transform of a static power-of-two plan (K2b): the first FFT
+// stage gathers its butterflies straight from the two staged rows (Makhoul
+// order: FFT index idx holds column 2 idx, or 2n - 1 - 2 idx past n/2) into
+// registers, so the packing pass disappears and, once every thread holds its
+// inputs, the FFT buffer may overwrite the staging: the forward kernel needs
+// max(2 rows, FFT buffer) of shared memory instead of their sum (4 instead of
+// 3 CTAs per SM at 4096 fp32).
+template <int L, int EMAX>
+__host__ __device__ constexpr bool rows_fused_ok() {
+  constexpr int r0 = first_radix<L, EMAX>();
+  return (r0 == 2 || r0 == 4 || r0 == 8 || r0 == 16) && EMAX % r0 == 0;
+}
+__host__ __device__ constexpr size_t rows_fwd_fused_smem(int n, int tsize, int ldseq) {
+  return 128 + (2 * (size_t)stage_row_bytes(n, tsize) > (size_t)ldseq * 2 * tsize
+                    ? 2 * (size_t)stage_row_bytes(n, tsize) : (size_t)ldseq * 2 * tsize);
+}
+
+template <typename T, int EMAX, int L>
+__device__ __forceinline__ void rows_first_stage(const T* sa, const T* sb, bool hasb, cplx<T>* buf) {
+  constexpr int R = first_radix<L, EMAX>(), Q = EMAX / R, NB = L / R;
+  cplx<T> v[Q][R];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int j = threadIdx.x + q * blockDim.x;
+    if (j >= NB) break;  // the launch may round the CTA up (>= 64 threads)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int m = r < R / 2 ? 2 * (j + r * NB) : 2 * L - 1 - 2 * (j + r * NB);
+      v[q][r] = mk<T>(sa[m], hasb ? sb[m] : (T)0);
+    }
+    Dft<T, R>::run(v[q]);
+  }
+  __syncthreads();  // every staged value is in registers: buf may overwrite the staging
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    if (threadIdx.x + q * blockDim.x >= NB) break;
+    cplx<T>* dst = buf + spad((threadIdx.x + q * blockDim.x) * R);
+#pragma unroll
+    for (int r = 0; r < R; ++r) dst[r] = v[q][r];
+  }
+}
+
 // Row-sharded grids (pu_create_band): the spectrum travels between the row
 // bands and the column bands of the all-to-all transpose in a packed layout,
 // chunk q = columns [q mb, (q + 1) mb) of the band's rows, row pitch mb:
@@ -102,8 +144,10 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw);
   T* sa = reinterpret_cast<T*>(smraw + 128);
   const bool one = pl.stage1 != 0;
+  constexpr bool FFUSE = !INV && LS > 0 && rows_fused_ok<(LS > 0 ? LS : 512), EMAX>();
+  const bool ffuse = FFUSE && !one;  // launched with rows_fwd_fused_smem (DctLaunch::rows_pipe)
   T* sb = one ? sa : reinterpret_cast<T*>(smraw + 128 + RB);
-  cplx<T>* buf0 = reinterpret_cast<cplx<T>*>(smraw + 128 + (one ? 1 : 2) * RB);
+  cplx<T>* buf0 = reinterpret_cast<cplx<T>*>(smraw + 128 + (ffuse ? 0 : (one ? 1 : 2) * RB));
   if (threadIdx.x == 0) {
     mbar_init(mbar, 1);
     fence_mbar_init();
@@ -183,6 +227,9 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
         }
       }
     } else if constexpr (!INV) {
+      if (ffuse) {
+        if constexpr (FFUSE) rows_first_stage<T, EMAX, LS>(sa, sb, hasb, buf);
+      } else {
       // Makhoul permutation + (a + i b) packing
       for (int j0 = 4 * threadIdx.x; j0 < n; j0 += 4 * blockDim.x) {
         if (j0 + 4 <= n) {
@@ -193,6 +240,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
         } else {
           for (int j = j0; j < n; ++j) buf[spad(mperm(j, n))] = mk<T>(sa[j], hasb ? sb[j] : (T)0);
         }
+      }
       }
     } else {
       for (int k = threadIdx.x; k < half; k += blockDim.x) {
@@ -212,7 +260,11 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
       bulk_g2s(sa, pold + (long long)ia * g.ld, RBrow, mbar);
       if (hasb) bulk_g2s(sb, pold + (long long)(ia + 1) * g.ld, RBrow, mbar);
     }
-    fft_n<T, EMAX, LS>(buf, 1, pl);
+    if (ffuse) {
+      if constexpr (FFUSE) fft_stages_range<T, EMAX, LS, first_radix<LS, EMAX>(), 0, LS>(buf, 0, 1, pl.stw);
+    } else {
+      fft_n<T, EMAX, LS>(buf, 1, pl);
+    }
     const long long oa = (long long)ia * g.ld, ob = oa + g.ld;
     if constexpr (!INV) {
       if (pout) {
