@@ -26,8 +26,8 @@ struct DctLaunch {
   static cudaError_t rows_pipe(bool inv, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const T* in, T* out,
                                const PcgCtrl* ctrl, const T* pold, int first, Pack pk);
   static int rows_pipe_blocks_per_sm(int threads, size_t smem);
-  // forward row kernel of a static plan: FFT buffer aliases the staging rows
-  static bool fwd_fused(const FftPlan<T>& pl);
+  // row kernels of a static plan: FFT buffer aliases the staging rows
+  static bool rows_fused(const FftPlan<T>& pl);
   static cudaError_t cols(int mode, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const T* lam_cols,
                           int cpc, T* data, PcgCtrl* ctrl, RedScratch rs, int site, int it, Push ps);
 };
@@ -50,18 +50,16 @@ cudaError_t DctLaunch<T, LS>::set_attrs(size_t row_smem, size_t col_smem) {
 template <typename T, int LS>
 cudaError_t DctLaunch<T, LS>::rows_pipe(bool inv, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const T* in,
                                         T* out, const PcgCtrl* ctrl, const T* pold, int first, Pack pk) {
+  const size_t smem = rows_fused(pl) ? rows_fused_smem(c.smem, sizeof(T), pl.ldseq) : c.smem;
   if (inv)
-    k_rows_pipe<T, EM, LS, true><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, in, out, ctrl, pold, first, pk);
-  else if (fwd_fused(pl))
-    k_rows_pipe<T, EM, LS, false><<<c.grid, c.threads, rows_fwd_fused_smem(pl.n, sizeof(T), pl.ldseq), c.st>>>(
-        g, pl, in, out, ctrl, nullptr, 0, pk);
+    k_rows_pipe<T, EM, LS, true><<<c.grid, c.threads, smem, c.st>>>(g, pl, in, out, ctrl, pold, first, pk);
   else
-    k_rows_pipe<T, EM, LS, false><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, in, out, ctrl, nullptr, 0, pk);
+    k_rows_pipe<T, EM, LS, false><<<c.grid, c.threads, smem, c.st>>>(g, pl, in, out, ctrl, nullptr, 0, pk);
   return cudaGetLastError();
 }
 
 template <typename T, int LS>
-bool DctLaunch<T, LS>::fwd_fused(const FftPlan<T>& pl) {
+bool DctLaunch<T, LS>::rows_fused(const FftPlan<T>& pl) {
   if constexpr (LS > 0) return rows_fused_ok<LS, EM>() && !pl.stage1;
   return false;
 }

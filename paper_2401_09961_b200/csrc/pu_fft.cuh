@@ -483,6 +483,20 @@ __device__ __forceinline__ void dct3_pre(T ak, T ank, T bk, T bnk, int k, int nk
   }
 }
 
+// conj(Z'_k) alone (the out_k half of dct3_pre, same arithmetic)
+template <typename T>
+__device__ __forceinline__ cplx<T> dct3_pre_k(T ak, T ank, T bk, T bnk, int k, const FftPlan<T>& pl) {
+  const cplx<T> wk = __ldg(pl.dct3w + k);
+  T vaRe, vaIm, vbRe, vbIm;
+  if (k == 0) {
+    vaRe = ak * wk.x; vaIm = 0; vbRe = bk * wk.x; vbIm = 0;
+  } else {
+    vaRe = wk.x * ak + wk.y * ank; vaIm = wk.y * ak - wk.x * ank;
+    vbRe = wk.x * bk + wk.y * bnk; vbIm = wk.y * bk - wk.x * bnk;
+  }
+  return mk<T>(vaRe - vbIm, -(vaIm + vbRe));
+}
+
 // division for the spectral scaling: a * MUFU reciprocal (~1 ulp) in fp32,
 // rcp-based in fp64; deterministic, so repeated applications agree bitwise
 __device__ __forceinline__ float rcp_approx(float x) {

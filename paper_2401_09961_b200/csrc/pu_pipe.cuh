@@ -73,9 +73,10 @@ __host__ __device__ constexpr bool rows_fused_ok() {
   constexpr int r0 = first_radix<L, EMAX>();
   return (r0 == 2 || r0 == 4 || r0 == 8 || r0 == 16) && EMAX % r0 == 0;
 }
-__host__ __device__ constexpr size_t rows_fwd_fused_smem(int n, int tsize, int ldseq) {
-  return 128 + (2 * (size_t)stage_row_bytes(n, tsize) > (size_t)ldseq * 2 * tsize
-                    ? 2 * (size_t)stage_row_bytes(n, tsize) : (size_t)ldseq * 2 * tsize);
+// shared memory of a fused launch from that of the plain one (128 + 2 staged rows + buffer)
+__host__ __device__ constexpr size_t rows_fused_smem(size_t plain, int tsize, int ldseq) {
+  return 128 + (plain - 128 - (size_t)ldseq * 2 * tsize > (size_t)ldseq * 2 * tsize
+                    ? plain - 128 - (size_t)ldseq * 2 * tsize : (size_t)ldseq * 2 * tsize);
 }
 
 template <typename T, int EMAX, int L>
@@ -94,6 +95,37 @@ __device__ __forceinline__ void rows_first_stage(const T* sa, const T* sb, bool 
     Dft<T, R>::run(v[q]);
   }
   __syncthreads();  // every staged value is in registers: buf may overwrite the staging
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    if (threadIdx.x + q * blockDim.x >= NB) break;
+    cplx<T>* dst = buf + spad((threadIdx.x + q * blockDim.x) * R);
+#pragma unroll
+    for (int r = 0; r < R; ++r) dst[r] = v[q][r];
+  }
+}
+
+// Inverse row transform (K4), same scheme: the first FFT stage builds its
+// inputs with the DCT-III pre-twiddle straight from the staged spectrum rows
+// (bins k and n - k), the buffer aliases the staging, and the axpy reads the
+// old direction from global memory (no staging left for its prefetch).
+template <typename T, int EMAX, int L>
+__device__ __forceinline__ void rows_first_stage_inv(const T* sa, const T* sb, bool hasb, cplx<T>* buf,
+                                                     const FftPlan<T>& pl) {
+  constexpr int R = first_radix<L, EMAX>(), Q = EMAX / R, NB = L / R;
+  cplx<T> v[Q][R];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int j = threadIdx.x + q * blockDim.x;
+    if (j >= NB) break;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int k = j + r * NB, nk = k == 0 ? 0 : L - k;
+      v[q][r] = hasb ? dct3_pre_k<T>(sa[k], sa[nk], sb[k], sb[nk], k, pl)
+                     : dct3_pre_k<T>(sa[k], sa[nk], (T)0, (T)0, k, pl);
+    }
+    Dft<T, R>::run(v[q]);
+  }
+  __syncthreads();
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
     if (threadIdx.x + q * blockDim.x >= NB) break;
@@ -144,8 +176,8 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw);
   T* sa = reinterpret_cast<T*>(smraw + 128);
   const bool one = pl.stage1 != 0;
-  constexpr bool FFUSE = !INV && LS > 0 && rows_fused_ok<(LS > 0 ? LS : 512), EMAX>();
-  const bool ffuse = FFUSE && !one;  // launched with rows_fwd_fused_smem (DctLaunch::rows_pipe)
+  constexpr bool FFUSE = LS > 0 && rows_fused_ok<(LS > 0 ? LS : 512), EMAX>();
+  const bool ffuse = FFUSE && !one;  // launched with rows_fused_smem (DctLaunch::rows_pipe)
   T* sb = one ? sa : reinterpret_cast<T*>(smraw + 128 + RB);
   cplx<T>* buf0 = reinterpret_cast<cplx<T>*>(smraw + 128 + (ffuse ? 0 : (one ? 1 : 2) * RB));
   if (threadIdx.x == 0) {
@@ -242,6 +274,8 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
         }
       }
       }
+    } else if (ffuse) {
+      if constexpr (FFUSE) rows_first_stage_inv<T, EMAX, LS>(sa, sb, hasb, buf, pl);
     } else {
       for (int k = threadIdx.x; k < half; k += blockDim.x) {
         const int nk = k == 0 ? 0 : n - k;
@@ -253,7 +287,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
     }
     __syncthreads();
     const bool axpy = INV && pold != nullptr && !first;
-    if (axpy && !one && threadIdx.x == 0) {
+    if (axpy && !one && !ffuse && threadIdx.x == 0) {
       // staging is free now: fetch the old search direction rows behind the FFT
       fence_proxy_async();
       mbar_expect_tx(mbar, hasb ? 2 * RBrow : RBrow);
@@ -303,7 +337,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
     } else {
       const int cpr = (n + 3) >> 2;
       const T beta = axpy ? (T)ctrl->beta : (T)0;
-      if (axpy && !one) mbar_wait(mbar, 1);
+      if (axpy && !one && !ffuse) mbar_wait(mbar, 1);
       for (int e = threadIdx.x; e < 2 * cpr; e += blockDim.x) {
         const int rr = e >= cpr, j0 = (e - rr * cpr) * 4;
         if (rr && !hasb) continue;
@@ -320,7 +354,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
         }
         const long long oo = (rr ? ob : oa) + j0;
         if (axpy) {
-          const Q4<T> pp = one ? ldg4(pold + oo) : ld4((rr ? sb : sa) + j0);
+          const Q4<T> pp = (one || ffuse) ? ldg4(pold + oo) : ld4((rr ? sb : sa) + j0);
 #pragma unroll
           for (int k = 0; k < 4; ++k) o.a[k] = (j0 + k < n) ? add_rn(mul_rn(beta, pp.a[k]), o.a[k]) : (T)0;
         }
