@@ -80,10 +80,13 @@ def _obj_fresh(src, obj):
 
 def _compile(job):
     src, obj, defs = job
+    log = obj + ".log"  # per-object ptxas output, reused while the object is up to date
     if not FORCE and _obj_fresh(src, obj):
-        return obj, 0, "(up to date)"
+        return obj, 0, open(log).read() if os.path.exists(log) else "(up to date)"
     cmd = [nvcc(), *ARCH, *CFLAGS, *defs, f"-I{INCLUDE}", f"-I{CSRC}", "-c", src, "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
+    with open(log, "w") as fh:
+        fh.write(res.stdout + res.stderr)
     return obj, res.returncode, res.stdout + res.stderr
 
 

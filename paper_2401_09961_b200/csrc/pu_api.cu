@@ -217,6 +217,7 @@ struct DctOps {
   decltype(&DctLaunch<T, 0>::rows_pipe) rows_pipe;
   decltype(&DctLaunch<T, 0>::rows_pipe_blocks_per_sm) rows_pipe_bps;
   decltype(&DctLaunch<T, 0>::cols) cols;
+  decltype(&DctLaunch<T, 0>::cols_blocks_per_sm) cols_bps;
   int ls;
 };
 
@@ -224,7 +225,7 @@ template <typename T, int LS>
 static DctOps<T> make_ops() {
   using D = DctLaunch<T, LS>;
   return DctOps<T>{&D::set_attrs, &D::rows_pipe, &D::rows_pipe_blocks_per_sm,
-                   &D::cols, LS};
+                   &D::cols, &D::cols_blocks_per_sm, LS};
 }
 
 template <typename T>
@@ -337,6 +338,7 @@ struct Impl : HandleBase {
   Grid g{};
   HostPlan<T> prow, pcol;  // row transforms (length m), column transforms (length n)
   int cols_per_cta = 2, col_threads = 64;
+  int col_nfull = 1 << 30, col_nhalf = 0;  // balanced column grid: full panels, then half panels
   size_t col_smem = 0;
   int ew_grid = 1, ew_threads = 32;
   int pipe_grid = 1, pipe_threads = 64;
@@ -424,7 +426,8 @@ struct Impl : HandleBase {
     // element-wise kernels: block-strided rows, thread-strided columns
     ew_threads = std::min(256, std::max(32, (m + 31) / 32 * 32));
     ew_grid = std::min(n, 148 * 8);
-    rs.stride = std::max(148 * 8, (m + cols_per_cta - 1) / cols_per_cta) + 1;
+    // (a balanced column grid has at most twice the panels)
+    rs.stride = std::max(148 * 8, 2 * ((std::max(m, gc.m) + cols_per_cta - 1) / cols_per_cta)) + 1;
     PU_CUDA(cudaMalloc(&rs.partials, sizeof(double) * PU_MAX_SUMS * rs.stride));
     PU_CUDA(cudaMalloc(&rs.ticket, sizeof(unsigned int) * 32));
     PU_CUDA(cudaMemset(rs.ticket, 0, sizeof(unsigned int) * 32));
@@ -448,6 +451,24 @@ struct Impl : HandleBase {
     // that handles of different sizes sharing an instantiation never shrink it
     PU_CUDA(rops.set_attrs(kSmemLimit, kSmemLimit));
     PU_CUDA(cops.set_attrs(kSmemLimit, kSmemLimit));
+    {
+      // k_cols_spec is one CTA per SM (shared memory); when the panels leave a
+      // partial last wave, turn it into half panels spread over every SM
+      // (4096 fp32: 444 panels of 8 columns + 136 of 4 instead of 3.46 waves)
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int per_sm = cops.cols_bps(col_threads, col_smem);
+      const int slots = sms * std::max(1, per_sm);
+      const int npan = (gc.m + cols_per_cta - 1) / cols_per_cta;
+      const int nfull = npan / slots * slots;
+      const int nhalf = (gc.m - nfull * cols_per_cta + cols_per_cta / 2 - 1) / (cols_per_cta / 2);
+      if (col_is_static && col_fused_rt(pcol.dev.L, EM) && cols_per_cta >= 4 && nfull > 0 && npan % slots != 0 &&
+          nhalf <= slots && std::getenv("PU_COL_NOBALANCE") == nullptr) {
+        col_nfull = nfull;
+        col_nhalf = nhalf;
+      }
+    }
     // persistent pipelined row kernels: one row pair per iteration
     pipe_threads = prow.threads_for(1);
     pipe_smem = pipe_bytes(prow.dev.stage1 ? 1 : 2);
@@ -465,12 +486,12 @@ struct Impl : HandleBase {
   XLaunch cl(cudaStream_t st) const { return XLaunch{col_grid(), col_threads, col_smem, st}; }
   XLaunch pl_(cudaStream_t st) const { return XLaunch{pipe_grid, pipe_threads, pipe_smem, st}; }
 
-  int col_grid() const { return (gc.m + cols_per_cta - 1) / cols_per_cta; }
+  int col_grid() const { return col_nhalf ? col_nfull + col_nhalf : (gc.m + cols_per_cta - 1) / cols_per_cta; }
 
   // ---- preconditioner passes ----
   int sylvester(const T* r, T* z, T* spec, cudaStream_t st) {
     PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, nullptr, nullptr, 0, Pack{}));
-    PU_DCT(cops.cols(MODE_API, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, nullptr, rs, S_K3, 0, Push{}));
+    PU_DCT(cops.cols(MODE_API, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, nullptr, rs, S_K3, 0, Push{}, col_nfull));
     PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, z, nullptr, nullptr, 0, Pack{}));
     return PU_OK;
   }
@@ -510,7 +531,7 @@ struct Impl : HandleBase {
     PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl, nullptr, 0, Pack{}));
     tm.end(st, e, TK_K2B, -1);
     e = tm.begin(st);
-    PU_DCT(cops.cols(MODE_INIT, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, ctrl, rs, S_K3, -1, Push{}));
+    PU_DCT(cops.cols(MODE_INIT, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, ctrl, rs, S_K3, -1, Push{}, col_nfull));
     tm.end(st, e, TK_K3, -1);
     // p of iteration k lives in pbuf[k & 1]; K4 writes its u block (p = z at k = 0)
     T* pbuf[2] = {p0, p1};
@@ -558,7 +579,7 @@ struct Impl : HandleBase {
       PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl, nullptr, 0, Pack{}));
       tm.end(st, e, TK_K2B, it);
       e = tm.begin(st);
-      PU_DCT(cops.cols(MODE_ITER, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, ctrl, rs, S_K3, it, Push{}));
+      PU_DCT(cops.cols(MODE_ITER, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, ctrl, rs, S_K3, it, Push{}, col_nfull));
       tm.end(st, e, TK_K3, it);
       e = tm.begin(st);  // u block of p for iteration it + 1: beta p_u + z_u
       PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, pbuf[(it + 1) & 1], ctrl, pn, 0, Pack{}));
@@ -621,7 +642,7 @@ struct Impl : HandleBase {
   int pcg_columns(T* spec, PcgCtrl* ctrl, int it, cudaStream_t st) {
     cudaEvent_t e = tm.begin(st);
     PU_DCT(cops.cols(it < 0 ? MODE_INIT : MODE_ITER, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec,
-                     ctrl, rs, S_K3, it, push));
+                     ctrl, rs, S_K3, it, push, col_nfull));
     tm.end(st, e, TK_K3, it);
     return PU_OK;
   }
@@ -737,10 +758,11 @@ int pu_describe(const pu_handle* h, char* buf, int cap) {
                   "{\"n\":%d,\"m\":%d,\"ld\":%lld,\"dtype\":\"%s\",\"row_fft\":{\"n\":%d,\"L\":%d,\"bluestein\":%d,"
                   "\"stages\":%d},\"col_fft\":{\"n\":%d,\"L\":%d,\"bluestein\":%d,\"stages\":%d},"
                   "\"row_pipe_grid\":%d,\"row_threads\":%d,\"row_smem\":%zu,\"cols_per_cta\":%d,"
-                  "\"col_threads\":%d,\"col_smem\":%zu,\"ew_grid\":%d,\"ew_threads\":%d}",
+                  "\"col_grid\":%d,\"col_half_panels\":%d,\"col_threads\":%d,\"col_smem\":%zu,\"ew_grid\":%d,"
+                  "\"ew_threads\":%d}",
                   I.g.n, I.g.m, I.g.ld, h->dtype == PU_F32 ? "f32" : "f64", I.prow.dev.n, I.prow.dev.L,
                   I.prow.dev.bluestein, I.prow.dev.nst, I.pcol.dev.n, I.pcol.dev.L, I.pcol.dev.bluestein,
-                  I.pcol.dev.nst, I.pipe_grid, I.pipe_threads, I.pipe_smem, I.cols_per_cta, I.col_threads,
+                  I.pcol.dev.nst, I.pipe_grid, I.pipe_threads, I.pipe_smem, I.cols_per_cta, I.col_grid(), I.col_nhalf, I.col_threads,
                   I.col_smem, I.ew_grid, I.ew_threads);
   };
   if (h->dtype == PU_F32) fmt(*h->f); else fmt(*h->d);

@@ -26,10 +26,11 @@ struct DctLaunch {
   static cudaError_t rows_pipe(bool inv, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const T* in, T* out,
                                const PcgCtrl* ctrl, const T* pold, int first, Pack pk);
   static int rows_pipe_blocks_per_sm(int threads, size_t smem);
+  static int cols_blocks_per_sm(int threads, size_t smem);
   // row kernels of a static plan: FFT buffer aliases the staging rows
   static bool rows_fused(const FftPlan<T>& pl);
   static cudaError_t cols(int mode, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const T* lam_cols,
-                          int cpc, T* data, PcgCtrl* ctrl, RedScratch rs, int site, int it, Push ps);
+                          int cpc, T* data, PcgCtrl* ctrl, RedScratch rs, int site, int it, Push ps, int nfull);
 };
 
 #ifdef PU_DCT_DEFINE
@@ -59,6 +60,13 @@ cudaError_t DctLaunch<T, LS>::rows_pipe(bool inv, const XLaunch& c, const Grid& 
 }
 
 template <typename T, int LS>
+int DctLaunch<T, LS>::cols_blocks_per_sm(int threads, size_t smem) {
+  int a = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_cols_spec<T, EM, LS, MODE_ITER>, threads, smem);
+  return a;
+}
+
+template <typename T, int LS>
 bool DctLaunch<T, LS>::rows_fused(const FftPlan<T>& pl) {
   if constexpr (LS > 0) return rows_fused_ok<LS, EM>() && !pl.stage1;
   return false;
@@ -75,13 +83,13 @@ int DctLaunch<T, LS>::rows_pipe_blocks_per_sm(int threads, size_t smem) {
 template <typename T, int LS>
 cudaError_t DctLaunch<T, LS>::cols(int mode, const XLaunch& c, const Grid& g, const FftPlan<T>& pl,
                                    const T* lam_cols, int cpc, T* data, PcgCtrl* ctrl, RedScratch rs, int site,
-                                   int it, Push ps) {
+                                   int it, Push ps, int nfull) {
   if (mode == MODE_API)
-    k_cols_spec<T, EM, LS, MODE_API><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it, ps);
+    k_cols_spec<T, EM, LS, MODE_API><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it, ps, nfull);
   else if (mode == MODE_INIT)
-    k_cols_spec<T, EM, LS, MODE_INIT><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it, ps);
+    k_cols_spec<T, EM, LS, MODE_INIT><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it, ps, nfull);
   else
-    k_cols_spec<T, EM, LS, MODE_ITER><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it, ps);
+    k_cols_spec<T, EM, LS, MODE_ITER><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it, ps, nfull);
   return cudaGetLastError();
 }
 #endif  // PU_DCT_DEFINE

@@ -283,13 +283,14 @@ __device__ __forceinline__ void fft_pow(cplx<T>* buf, int nseq, const FftPlan<T>
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr int ldseq_for(int L) { return (L + (L >> 4) + 2) + ((L + (L >> 4) + 2) & 1); }
 
-template <int L, int EMAX>
-__host__ __device__ constexpr int first_radix() {
-  const int big = EMAX >= 16 ? 16 : 8;
+__host__ __device__ constexpr int first_radix_rt(int L, int emax) {
+  const int big = emax >= 16 ? 16 : 8;
   int rem = L;
   while (rem > 1 && rem % big == 0) rem /= big;
   return rem == 1 ? big : rem;
 }
+template <int L, int EMAX>
+__host__ __device__ constexpr int first_radix() { return first_radix_rt(L, EMAX); }
 
 template <typename T, int R, int EMAX, int L, int NS, int OFF>
 __device__ __forceinline__ void fft_stage_s(cplx<T>* buf, int seq0, int nseq, const cplx<T>* __restrict__ stw) {

@@ -149,18 +149,17 @@ __device__ __forceinline__ void panel_store(const Grid& g, const FftPlan<T>& pl,
 // at idx = j + r L/R, so rows are 2 j + 2 r L/R (r < R/2) and
 // 2L - 1 - 2 j - 2 r L/R.
 // ---------------------------------------------------------------------------
-template <int L, int EMAX>
-__host__ __device__ constexpr bool col_fused_ok() {
-  constexpr int big = EMAX >= 16 ? 16 : 8;
-  constexpr int r0 = first_radix<L, EMAX>();
-  return (r0 == 2 || r0 == 4 || r0 == 8 || r0 == 16) && EMAX % r0 == 0 && L >= r0 * big && (L / big) % 16 == 0;
+__host__ __device__ constexpr bool col_fused_rt(int L, int emax) {
+  const int big = emax >= 16 ? 16 : 8, r0 = first_radix_rt(L, emax);
+  return (r0 == 2 || r0 == 4 || r0 == 8 || r0 == 16) && emax % r0 == 0 && L >= r0 * big && (L / big) % 16 == 0;
 }
+template <int L, int EMAX>
+__host__ __device__ constexpr bool col_fused_ok() { return col_fused_rt(L, EMAX); }
 
 // first forward stage, Q = EMAX / R butterflies per thread (all loads in flight first)
-template <typename T, int EMAX, int L>
+template <typename T, int EMAX, int L, int NSEQ>
 __device__ __forceinline__ void col_first_stage(const Grid& g, const T* __restrict__ data, int j0, cplx<T>* buf) {
-  constexpr int R = first_radix<L, EMAX>(), Q = EMAX / R, NB = L / R;
-  constexpr int NSEQ = static_panel_cols(L, EMAX) / 2, LD = ldseq_for(L);
+  constexpr int R = first_radix<L, EMAX>(), Q = EMAX / R, NB = L / R, LD = ldseq_for(L);
   const long long ld = g.ld, step = 2LL * NB * ld;
   cplx<T> v[Q][R];
 #pragma unroll
@@ -188,10 +187,10 @@ __device__ __forceinline__ void col_first_stage(const Grid& g, const T* __restri
 
 // last inverse stage (NS = L / R, one butterfly per thread): twiddle, DFT,
 // store column 2s = Re, 2s + 1 = -Im (as panel_store) of each output row
-template <typename T, int EMAX, int L>
+template <typename T, int EMAX, int L, int NSEQ>
 __device__ __forceinline__ void col_last_stage(const Grid& g, T* data, int j0, const cplx<T>* buf,
                                                const cplx<T>* __restrict__ stw, const Push& ps) {
-  constexpr int R = EMAX >= 16 ? 16 : 8, NS = L / R, NSEQ = static_panel_cols(L, EMAX) / 2, LD = ldseq_for(L);
+  constexpr int R = EMAX >= 16 ? 16 : 8, NS = L / R, LD = ldseq_for(L);
   constexpr int OFF = stage_off<L, EMAX>(NS);
   const int s = threadIdx.x % NSEQ, j = threadIdx.x / NSEQ;
   if (j < NS) {  // CTAs may be rounded up (no early return: a grid reduction follows)
@@ -229,22 +228,31 @@ __device__ __forceinline__ void col_last_stage(const Grid& g, T* data, int j0, c
 // ---------------------------------------------------------------------------
 template <typename T, int EMAX, int LS, int MODE>
 __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, EMAX)) k_cols_spec(Grid g, FftPlan<T> pl, const T* __restrict__ lam_cols, int cols_per_cta, T* data,
-                            PcgCtrl* ctrl, RedScratch rs, int site, int it, Push ps) {
+                            PcgCtrl* ctrl, RedScratch rs, int site, int it, Push ps, int nfull) {
   extern __shared__ __align__(16) unsigned char smraw[];
   cplx<T>* buf = reinterpret_cast<cplx<T>*>(smraw);
   if (MODE != MODE_API && ctrl->done) return;
   const int n = LS > 0 ? LS : g.n;  // static plans are only used when n == L
   // static plans: compile-time panel width; runtime plans: 4 or 2 (smem)
-  const int W = LS > 0 ? static_panel_cols(LS, EMAX) : cols_per_cta;
-  const int j0 = blockIdx.x * W;
+  const int W0 = LS > 0 ? static_panel_cols(LS, EMAX) : cols_per_cta;
+  // balanced grid (static plans): CTAs past `nfull` take half panels, so the
+  // last wave is spread over every SM instead of a few full panels
+  const bool halfp = (int)blockIdx.x >= nfull;
+  const int W = halfp ? W0 / 2 : W0;
+  const int j0 = halfp ? nfull * W0 + ((int)blockIdx.x - nfull) * W : (int)blockIdx.x * W0;
   const int ncols = min(W, g.m - j0);
   const int nseq = (ncols + 1) >> 1;
   constexpr bool FUSE = LS > 0 && col_fused_ok<(LS > 0 ? LS : 4096), EMAX>();
   constexpr int LF = LS > 0 ? LS : 4096;  // (LS == 0: FUSE is false, LF unused)
-  const bool fuse = FUSE && ncols == W;
+  const bool fuse = FUSE && ncols == W && (!halfp || static_panel_cols(LF, EMAX) >= 4);
   if (fuse) {
     if constexpr (FUSE) {
-      col_first_stage<T, EMAX, LF>(g, data, j0, buf);
+      constexpr int NSF = static_panel_cols(LF, EMAX) / 2;
+      if (halfp) {
+        if constexpr (NSF >= 2) col_first_stage<T, EMAX, LF, NSF / 2>(g, data, j0, buf);
+      } else {
+        col_first_stage<T, EMAX, LF, NSF>(g, data, j0, buf);
+      }
       fft_stages_range<T, EMAX, LF, first_radix<LF, EMAX>(), 0, LF>(buf, 0, nseq, pl.stw);
     }
   } else {
@@ -286,7 +294,12 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   if (fuse) {
     if constexpr (FUSE) {
       fft_stages_range<T, EMAX, LF, 1, 0, LF / (EMAX >= 16 ? 16 : 8)>(buf, 0, nseq, pl.stw);
-      col_last_stage<T, EMAX, LF>(g, data, j0, buf, pl.stw, ps);
+      constexpr int NSF = static_panel_cols(LF, EMAX) / 2;
+      if (halfp) {
+        if constexpr (NSF >= 2) col_last_stage<T, EMAX, LF, NSF / 2>(g, data, j0, buf, pl.stw, ps);
+      } else {
+        col_last_stage<T, EMAX, LF, NSF>(g, data, j0, buf, pl.stw, ps);
+      }
     }
   } else {
     fft_n<T, EMAX, LS>(buf, nseq, pl);
