@@ -31,6 +31,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                "l"(src), "r"(bytes), "r"(smem_u32(m))
                : "memory");
 }
+// bulk prefetch of `bytes` (multiple of 16) global bytes into L2 (TMA engine)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* m, unsigned parity) {
   asm volatile(
       "{\n"
@@ -219,7 +223,15 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
     mbar_wait(mbar, 1);
   };
   const int s = blockIdx.x;
-  if (threadIdx.x == 0 && s < S) issue(s);
+  if (threadIdx.x == 0 && s < S) {
+    issue(s);
+    if (INV && ffuse && pold != nullptr && !first) {
+      // fused K4 reads the old direction from global memory in its output
+      // pass: start pulling its two rows into L2 now, behind the FFT
+      bulk_prefetch_l2(pold + (long long)(2 * s) * g.ld, RBrow);
+      if (2 * s + 1 < g.n) bulk_prefetch_l2(pold + (long long)(2 * s + 1) * g.ld, RBrow);
+    }
+  }
   const int half = n / 2 + 1;
   if (s < S) {
     cplx<T>* buf = buf0;
