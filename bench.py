@@ -502,7 +502,8 @@ def main():
             e2e_ms.append((t1 - t0) * 1e3)
     e2e_step = max_over_ranks(statistics.mean(e2e_ms), device=dev)
     h2d = n_img * n * m * 8
-    d2h = n_img * (res.u.size + res.vv.size + res.vh.size) * 8
+    # the results travel in the compute dtype and are widened to fp64 on the host
+    d2h = n_img * (res.u.size + res.vv.size + res.vh.size) * (4 if args.dtype == "fp32" else 8)
 
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config != "c5":
@@ -649,7 +650,7 @@ def main_rows(args, rank, local_rank, world, dev, lib):
             e2e_ms.append((t1 - t0) * 1e3)
     e2e_step = max_over_ranks(statistics.mean(e2e_ms), device=dev)
     h2d = (n + world - 1) * m * 8
-    d2h = (n * m + (n - 1) * m + n * (m - 1)) * 8
+    d2h = (n * m + (n - 1) * m + n * (m - 1)) * (4 if args.dtype == "fp32" else 8)  # compute dtype, widened on host
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -463,7 +463,7 @@ struct Impl : HandleBase {
       const int npan = (gc.m + cols_per_cta - 1) / cols_per_cta;
       const int nfull = npan / slots * slots;
       const int nhalf = (gc.m - nfull * cols_per_cta + cols_per_cta / 2 - 1) / (cols_per_cta / 2);
-      if (col_is_static && col_fused_rt(pcol.dev.L, EM) && cols_per_cta >= 4 && nfull > 0 && npan % slots != 0 &&
+      if (col_is_static && col_fused_rt(pcol.dev.L, EM) && cols_per_cta >= 8 && nfull > 0 && npan % slots != 0 &&
           nhalf <= slots && std::getenv("PU_COL_NOBALANCE") == nullptr) {
         col_nfull = nfull;
         col_nhalf = nhalf;

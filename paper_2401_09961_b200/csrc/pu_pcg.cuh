@@ -237,19 +237,20 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   const int W0 = LS > 0 ? static_panel_cols(LS, EMAX) : cols_per_cta;
   // balanced grid (static plans): CTAs past `nfull` take half panels, so the
   // last wave is spread over every SM instead of a few full panels
-  const bool halfp = (int)blockIdx.x >= nfull;
+  constexpr bool HALF_OK = LS > 0 && static_panel_cols(LS > 0 ? LS : 4096, EMAX) >= 8;  // host: cols_per_cta >= 8
+  const bool halfp = HALF_OK && (int)blockIdx.x >= nfull;
   const int W = halfp ? W0 / 2 : W0;
   const int j0 = halfp ? nfull * W0 + ((int)blockIdx.x - nfull) * W : (int)blockIdx.x * W0;
   const int ncols = min(W, g.m - j0);
   const int nseq = (ncols + 1) >> 1;
   constexpr bool FUSE = LS > 0 && col_fused_ok<(LS > 0 ? LS : 4096), EMAX>();
   constexpr int LF = LS > 0 ? LS : 4096;  // (LS == 0: FUSE is false, LF unused)
-  const bool fuse = FUSE && ncols == W && (!halfp || static_panel_cols(LF, EMAX) >= 4);
+  const bool fuse = FUSE && ncols == W;
   if (fuse) {
     if constexpr (FUSE) {
       constexpr int NSF = static_panel_cols(LF, EMAX) / 2;
       if (halfp) {
-        if constexpr (NSF >= 2) col_first_stage<T, EMAX, LF, NSF / 2>(g, data, j0, buf);
+        if constexpr (NSF >= 4) col_first_stage<T, EMAX, LF, NSF / 2>(g, data, j0, buf);
       } else {
         col_first_stage<T, EMAX, LF, NSF>(g, data, j0, buf);
       }
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
       fft_stages_range<T, EMAX, LF, 1, 0, LF / (EMAX >= 16 ? 16 : 8)>(buf, 0, nseq, pl.stw);
       constexpr int NSF = static_panel_cols(LF, EMAX) / 2;
       if (halfp) {
-        if constexpr (NSF >= 2) col_last_stage<T, EMAX, LF, NSF / 2>(g, data, j0, buf, pl.stw, ps);
+        if constexpr (NSF >= 4) col_last_stage<T, EMAX, LF, NSF / 2>(g, data, j0, buf, pl.stw, ps);
       } else {
         col_last_stage<T, EMAX, LF, NSF>(g, data, j0, buf, pl.stw, ps);
       }
