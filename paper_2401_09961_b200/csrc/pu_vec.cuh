@@ -311,9 +311,22 @@ __global__ void __launch_bounds__(256, 2) k_pcg_start_v(Grid g, const T* __restr
     s.ul = ldg_or0(x0 + o - 1, j0 > 0);
     s.hl = ldg_or0(x0 + o - 1 + 2 * P, j0 > 0);
     s.ur = ldg_or0(x0 + o + 4, j0 + 4 < g.m);
+    const Q4<T> bu = ldg4(b + o), bv = ldg4(b + o + P), bh = ldg4(b + o + 2 * P);
+    // candidate-step operands: in fp32 issued with the start-up loads, so the
+    // chunk waits for memory once instead of twice (fp64 would spill)
+    Q4<T> g1, g2, ga, w1, w2, c1, c2;
+    T gl = (T)0;
+    auto load_cand = [&]() {
+      g1 = ldg4(ca.gv + o); g2 = ldg4(ca.gh + o);
+      ga = up_ok(g, i) ? ldg4(ca.gv + o - ld) : zero4<T>();
+      gl = ldg_or0(ca.gh + o - 1, j0 > 0);
+      w1 = ldg4(ca.wv + o); w2 = ldg4(ca.wh + o);
+      if (ca.cv) { c1 = ldg4(ca.cv + o); c2 = ldg4(ca.ch + o); }
+    };
+    constexpr bool EARLY = sizeof(T) == 4;
+    if constexpr (CAND && EARLY) load_cand();
     Q4<T> au, av, ah;
     apply4<T>(g, i, j0, s, d1, d2, au, av, ah);
-    const Q4<T> bu = ldg4(b + o), bv = ldg4(b + o + P), bh = ldg4(b + o + 2 * P);
     Q4<T> ru, rv, rh;
     T pb = (T)0, pr = (T)0, prz = (T)0;
 #pragma unroll
@@ -335,12 +348,7 @@ __global__ void __launch_bounds__(256, 2) k_pcg_start_v(Grid g, const T* __restr
     if (copy) { st4(x + o, s.u); st4(x + o + P, s.v); st4(x + o + 2 * P, s.h); }
     st4(r + o, ru); st4(r + o + P, rv); st4(r + o + 2 * P, rh);
     if constexpr (CAND) {
-      const Q4<T> g1 = ldg4(ca.gv + o), g2 = ldg4(ca.gh + o);
-      const Q4<T> ga = up_ok(g, i) ? ldg4(ca.gv + o - ld) : zero4<T>();
-      const T gl = ldg_or0(ca.gh + o - 1, j0 > 0);
-      const Q4<T> w1 = ldg4(ca.wv + o), w2 = ldg4(ca.wh + o);
-      Q4<T> c1, c2;
-      if (ca.cv) { c1 = ldg4(ca.cv + o); c2 = ldg4(ca.ch + o); }
+      if constexpr (!EARLY) load_cand();
       const bool hasb = dn_ok(g, i), hasa = up_ok(g, i);
       Q4<T> ou, ov, oh;
 #pragma unroll
