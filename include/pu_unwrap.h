@@ -146,7 +146,10 @@ int pu_accept_center(pu_handle* h, const void* xa, const void* xb, const double*
  * the start-up residual share one pass over the state), then
  * out[0] = H(proposal, w), out[1] = H(cand, w), out[2] = mean u of the
  * accepted one, out[3] = 1.0 if the proposal is accepted.  cv/ch may both be
- * NULL for uniform unit weights.  PCG scratch and ctrl as in pu_pcg_solve. */
+ * NULL for uniform unit weights.  PCG scratch and ctrl as in pu_pcg_solve.
+ * b may be NULL: b = build_rhs(gv, gh) (pu_build_rhs) is then formed inside
+ * the start-up kernel from the gradient loads the candidate step makes
+ * anyway (bit-identical; the three b planes are never read). */
 int pu_irls_step(pu_handle* h, void* state, const void* b, const void* gv, const void* gh, const void* cv,
                  const void* ch, const void* wv, const void* wh, const void* dv, const void* dh, double lipschitz,
                  int max_iters, double rel_tol, void* cand, void* r, void* p0, void* p1, void* spec, void* ctrl,
@@ -273,7 +276,8 @@ int pu_dev_free(void* dev_ptr);
 int pu_finalize(pu_handle* h, unsigned mask, int mode, int it, void* ctrl, double* res_norms, double* out,
                 double rel_tol, int max_iters, void* stream);
 /* pcg.py:59-75 (+ the candidate step objective.py:118-125 when cand != NULL,
- * as in pu_irls_step).  x may alias x0. */
+ * as in pu_irls_step).  x may alias x0.  b may be NULL when cand != NULL
+ * (b = build_rhs(gv, gh) formed in the kernel, as in pu_irls_step). */
 int pu_pcg_begin(pu_handle* h, const void* b, const void* x0, void* x, const void* dv, const void* dh, void* r,
                  void* ctrl, double* res_norms, int max_iters, double rel_tol, const void* gv, const void* gh,
                  const void* cv, const void* ch, const void* wv, const void* wh, double lipschitz, void* cand,

@@ -107,7 +107,7 @@ class BandState:
         self.ld = int(self.lib.pu_pitch(h))
         z = lambda k: torch.zeros((k, self.rows + 2, self.ld), dtype=self.tdtype, device=device)  # noqa: E731
         self.S = [z(3), z(3)]
-        self.C, self.B, self.G, self.D, self.R = z(3), z(3), z(2), z(2), z(3)
+        self.C, self.G, self.D, self.R = z(3), z(2), z(2), z(3)
         self.Wt = [z(2), z(2)]
         self.P = [z(3), z(3)]
         self.W, self.use_w = None, False
@@ -381,9 +381,8 @@ class BandUnwrap:
                 self._keep += [b.pack_rows(c.cv, b.W, 0, b.row0, nv), b.pack_rows(c.ch, b.W, 1, b.row0, b.rows)]
             self._keep.append(xr)
             b.call("pu_wrapped_gradients", _ptr(xr), int(xr.shape[1]), P(b.G, 0), P(b.G, 1), float(lo), b.stream())
-        self.comm.halo(self.bands, [(lambda b: b.G, 0, "down")])  # gv[-1]: rhs and candidate stencils
+        self.comm.halo(self.bands, [(lambda b: b.G, 0, "down")])  # gv[-1]: rhs (formed in pu_pcg_begin) and candidate stencils
         for b in self.bands:
-            b.call("pu_build_rhs", P(b.G, 0), P(b.G, 1), P(b.B), b.stream())
             b.call("pu_init_state", P(b.G, 0), P(b.G, 1), P(b.S[0]), b.stream())
             b.cur = 0
         self._state_halo(lambda b: b.S[0])
@@ -432,7 +431,7 @@ class BandUnwrap:
         for b in self.bands:
             cv, ch = self._c(b)
             w = b.Wt[k & 1]
-            b.call("pu_pcg_begin", P(b.B), P(cur(b)), P(cur(b)), P(b.D, 0), P(b.D, 1), P(b.R), _ptr(b.ctrl),
+            b.call("pu_pcg_begin", None, P(cur(b)), P(cur(b)), P(b.D, 0), P(b.D, 1), P(b.R), _ptr(b.ctrl),
                    _ptr(b.norms), int(m_cg), tol, P(b.G, 0), P(b.G, 1), cv, ch, P(w, 0), P(w, 1), float(lip),
                    P(b.C), b.stream())
         self._reduce(nat.SITE_START, nat.SITE_START, _mask(nat.SITE_START), 1, -1, rel_tol=tol, max_iters=m_cg)

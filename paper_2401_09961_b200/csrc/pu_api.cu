@@ -517,7 +517,10 @@ struct Impl : HandleBase {
                 const CandArgs<T>* cand) {
     const int vg = vec_grid();
     cudaEvent_t e = tm.begin(st);
-    if (cand) {
+    if (cand && !b) {  // b = build_rhs(gv, gh) formed in the kernel
+      k_pcg_start_v<T, true, true><<<vg, 256, 0, st>>>(g, b, x0, x, r, dv, dh, ctrl, norms, rel_tol, max_iters, rs,
+                                                        S_START, *cand);
+    } else if (cand) {
       k_pcg_start_v<T, true><<<vg, 256, 0, st>>>(g, b, x0, x, r, dv, dh, ctrl, norms, rel_tol, max_iters, rs, S_START,
                                                   *cand);
     } else {
@@ -595,7 +598,10 @@ struct Impl : HandleBase {
                 double rel_tol, int max_iters, const CandArgs<T>* cand, cudaStream_t st) {
     const int vg = vec_grid();
     cudaEvent_t e = tm.begin(st);
-    if (cand)
+    if (cand && !b)  // b = build_rhs(gv, gh) formed in the kernel
+      k_pcg_start_v<T, true, true><<<vg, 256, 0, st>>>(g, b, x0, x, r, dv, dh, ctrl, norms, rel_tol, max_iters, rs,
+                                                        S_START, *cand);
+    else if (cand)
       k_pcg_start_v<T, true><<<vg, 256, 0, st>>>(g, b, x0, x, r, dv, dh, ctrl, norms, rel_tol, max_iters, rs, S_START,
                                                   *cand);
     else
@@ -1138,6 +1144,7 @@ int pu_pcg_solve(pu_handle* h, const void* b, const void* x0, void* x, const voi
                  void* stream) {
   if (max_iters < 0) return fail(PU_ERR_ARG, "max_iters must be >= 0");
   if (rel_tol < 0) return fail(PU_ERR_ARG, "rel_tol must be >= 0");
+  if (!b) return fail(PU_ERR_ARG, "b must not be NULL");
   PU_DISPATCH(h, {
     return I.pcg(CP(b), CP(x0), MP(x), CP(dv), CP(dh), MP(r), MP(z), MP(p0), MP(p1), MP(spec), max_iters, rel_tol,
                  reinterpret_cast<PcgCtrl*>(ctrl), res_norms, ST(stream));
@@ -1246,6 +1253,7 @@ int pu_pcg_begin(pu_handle* h, const void* b, const void* x0, void* x, const voi
   if (max_iters < 0) return fail(PU_ERR_ARG, "max_iters must be >= 0");
   if (rel_tol < 0) return fail(PU_ERR_ARG, "rel_tol must be >= 0");
   if (cand && !(lipschitz > 0)) return fail(PU_ERR_ARG, "lipschitz constant must be positive");
+  if (!b && !(cand && gv && gh)) return fail(PU_ERR_ARG, "b may be NULL only with the candidate step (gv, gh, cand)");
   if ((cv == nullptr) != (ch == nullptr)) return fail(PU_ERR_ARG, "cv and ch must both be given or both NULL");
   PU_DISPATCH(h, {
     const CandArgs<T> ca{CP(gv), CP(gh), CP(cv), CP(ch), CP(wv), CP(wh), (T)(cand ? -1.0 / lipschitz : 0.0),

@@ -282,13 +282,16 @@ __global__ void __launch_bounds__(256) k_pcg_upd_sum_v(Grid g, const T* __restri
 // setup: x = x0 (skipped when x aliases x0), r = b - A x0, ||b||, ||r0||
 // (pcg.py:59-75).  CAND: also the explicit gradient step of the same state,
 // cand = x0 - (1/L) grad H(x0, w) (objective.py:108-125), from the same loads.
-// cv/ch == nullptr means uniform unit arc weights.
+// cv/ch == nullptr means uniform unit arc weights.  RHSG (b == nullptr at the
+// C ABI): b = build_rhs(gv, gh) (operators.py:156-162) is formed in registers
+// from the candidate step's gradient loads with k_rhs's arithmetic (bit-
+// identical), so the three b planes are never read (18 -> 15 planes moved).
 template <typename T>
 struct CandArgs {
   const T* gv; const T* gh; const T* cv; const T* ch; const T* wv; const T* wh; T neg_inv_lip; T* out;
 };
 
-template <typename T, bool CAND>
+template <typename T, bool CAND, bool RHSG = false>
 __global__ void __launch_bounds__(256, 2) k_pcg_start_v(Grid g, const T* __restrict__ b, const T* x0, T* x,
                                                         T* __restrict__ r, const T* __restrict__ dv,
                                                         const T* __restrict__ dh, PcgCtrl* ctrl, double* res_norms,
@@ -311,7 +314,8 @@ __global__ void __launch_bounds__(256, 2) k_pcg_start_v(Grid g, const T* __restr
     s.ul = ldg_or0(x0 + o - 1, j0 > 0);
     s.hl = ldg_or0(x0 + o - 1 + 2 * P, j0 > 0);
     s.ur = ldg_or0(x0 + o + 4, j0 + 4 < g.m);
-    const Q4<T> bu = ldg4(b + o), bv = ldg4(b + o + P), bh = ldg4(b + o + 2 * P);
+    Q4<T> bu, bv, bh;
+    if constexpr (!RHSG) { bu = ldg4(b + o); bv = ldg4(b + o + P); bh = ldg4(b + o + 2 * P); }
     // candidate-step operands: in fp32 issued with the start-up loads, so the
     // chunk waits for memory once instead of twice (fp64 would spill)
     Q4<T> g1, g2, ga, w1, w2, c1, c2;
@@ -323,8 +327,21 @@ __global__ void __launch_bounds__(256, 2) k_pcg_start_v(Grid g, const T* __restr
       w1 = ldg4(ca.wv + o); w2 = ldg4(ca.wh + o);
       if (ca.cv) { c1 = ldg4(ca.cv + o); c2 = ldg4(ca.ch + o); }
     };
-    constexpr bool EARLY = sizeof(T) == 4;
+    constexpr bool EARLY = sizeof(T) == 4 || RHSG;
     if constexpr (CAND && EARLY) load_cand();
+    if constexpr (RHSG) {  // k_rhs (pu_kernels.cuh) per cell, from the loaded gradients
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = j0 + k;
+        const bool ok = j < g.m;
+        const T gvo = (ok && dn_ok(g, i)) ? g1.a[k] : (T)0, gvm = ok ? ga.a[k] : (T)0;
+        const T gho = (j < g.m - 1) ? g2.a[k] : (T)0;
+        const T ghm = (ok && j > 0) ? ((k == 0) ? gl : g2.a[k - 1]) : (T)0;
+        bu.a[k] = ok ? inv * ((gvm - gvo) + (ghm - gho)) : (T)0;
+        bv.a[k] = ok ? -inv * gvo : (T)0;
+        bh.a[k] = ok ? -inv * gho : (T)0;
+      }
+    }
     Q4<T> au, av, ah;
     apply4<T>(g, i, j0, s, d1, d2, au, av, ah);
     Q4<T> ru, rv, rh;

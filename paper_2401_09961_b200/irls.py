@@ -40,7 +40,6 @@ class DeviceUnwrap:
         self.ws = ws
         self.S = [ws.buf("state0", 3), ws.buf("state1", 3)]  # state ping-pong
         self.C = ws.buf("cand", 3)       # explicit-gradient candidate
-        self.B = ws.buf("rhs", 3)
         self.G = ws.buf("grad", 2)       # gv, gh
         self.W = None                    # arc weights cv, ch (None: uniform)
         self.Wt = [ws.buf("w0", 2), ws.buf("w1", 2)]
@@ -65,7 +64,6 @@ class DeviceUnwrap:
         self._x = x64.contiguous()
         ws.call("pu_wrapped_gradients", _ptr(self._x), int(self._x.shape[1]), _ptr(self.G[0]), _ptr(self.G[1]),
                 float(lo), st)
-        ws.call("pu_build_rhs", _ptr(self.G[0]), _ptr(self.G[1]), _ptr(self.B), st)
         ws.call("pu_init_state", _ptr(self.G[0]), _ptr(self.G[1]), _ptr(self.S[0]), st)
         self.cur = 0
         cv, ch = self._c()
@@ -86,7 +84,9 @@ class DeviceUnwrap:
         cv, ch = self._c()
         w = self.Wt[k & 1]
         norms = ws.ensure_norms(64)
-        ws.call("pu_irls_begin", _ptr(self.S[self.cur]), _ptr(self.B), _ptr(self.G[0]), _ptr(self.G[1]), cv, ch,
+        # b = NULL: the right-hand side build_rhs(gv, gh) (operators.py:156-162)
+        # is formed inside the start-up kernel from its gradient loads
+        ws.call("pu_irls_begin", _ptr(self.S[self.cur]), None, _ptr(self.G[0]), _ptr(self.G[1]), cv, ch,
                 _ptr(w[0]), _ptr(w[1]), _ptr(self.D[0]), _ptr(self.D[1]), float(lip), float(params.cg_rel_tol),
                 _ptr(self.C), _ptr(self.R), _ptr(self.P[0]), _ptr(self.P[1]), _ptr(self.spec), _ptr(ws.ctrl),
                 _ptr(norms), st)
