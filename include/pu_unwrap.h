@@ -181,6 +181,24 @@ int pu_accept_weights(pu_handle* h, const void* xa, const void* xb, const double
                       const void* gh, const void* cv, const void* ch, const void* wkv, const void* wkh, void* wnv,
                       void* wnh, void* dv, void* dh, double* out, void* stream);
 
+/* pu_accept_weights of iteration k fused with the budget-free start of
+ * iteration k + 1 (the start-up kernel of pu_irls_begin with b = NULL):
+ * besides dst, w_next, d and out[0..1] it writes r = b - A dst
+ * (b = build_rhs(gv, gh)) and cand = dst - (1/L) grad H(dst, w_next) from the
+ * same registers, one pass over the accepted state instead of two.  The
+ * start-up sums are held in the handle; ctrl is not touched until
+ * pu_irls_begin_z0 finalises them.  Whole grids only (bands: pu_pcg_begin).
+ * Every value is bit-identical to pu_accept_weights + pu_irls_begin. */
+int pu_accept_weights_start(pu_handle* h, const void* xa, const void* xb, const double* sel, void* dst,
+                            const void* gv, const void* gh, const void* cv, const void* ch, const void* wkv,
+                            const void* wkh, void* wnv, void* wnh, void* dv, void* dh, double* out, double lipschitz,
+                            void* r, void* cand, void* stream);
+/* The rest of pu_irls_begin after pu_accept_weights_start: finalise the held
+ * start-up sums into ctrl/res_norms (pcg.py:59-75) and z0 = M r0, rho0,
+ * p0 = z0 (pcg.py:77-79).  Replayed as a CUDA graph. */
+int pu_irls_begin_z0(pu_handle* h, const void* dv, const void* dh, double rel_tol, void* r, void* p0, void* p1,
+                     void* spec, void* ctrl, double* res_norms, void* stream);
+
 /* pcg.py:47-116 pcg_solve with apply_system and apply_preconditioner fused
  * in (5 kernels per iteration).  x = x0 on entry (x may alias x0: solve in
  * place); otherwise x0 is not modified.  z is unused (kept for ABI stability).

@@ -52,6 +52,8 @@ SIGNATURES = {
     "pu_irls_begin": (_i, [_vp] + [_vp] * 10 + [_d, _d] + [_vp] * 7 + [_vp]),
     "pu_irls_iterate": (_i, [_vp] + [_vp] * 9 + [_i] + [_vp] * 7 + [_vp, _vp]),
     "pu_accept_weights": (_i, [_vp] + [_vp] * 15 + [_vp]),
+    "pu_accept_weights_start": (_i, [_vp] + [_vp] * 15 + [_d, _vp, _vp, _vp]),
+    "pu_irls_begin_z0": (_i, [_vp, _vp, _vp, _d] + [_vp] * 7),
     "pu_set_graphs": (_i, [_vp, _i]),
     "pu_timing_enable": (_i, [_vp, _i]),
     "pu_timing_read": (_i, [_vp, _vp, _vp, _vp, _i]),

@@ -346,6 +346,7 @@ struct Impl : HandleBase {
   size_t pipe_smem = 0;
   RedScratch rs{};
   int* pinned_done = nullptr;
+  double* held = nullptr;  // start-up sums of k_accept_start_v, finalised by pu_irls_begin_z0
   DctOps<T> rops{}, cops{};  // transform kernels for the row / column internal lengths
   Timer tm;
   GraphCache graphs;
@@ -362,6 +363,7 @@ struct Impl : HandleBase {
     if (rs.partials) cudaFree(rs.partials);
     if (rs.ticket) cudaFree(rs.ticket);
     if (pinned_done) cudaFreeHost(pinned_done);
+    if (held) cudaFree(held);
   }
 
   // b == nullptr: the whole N x M grid.  Otherwise one row band of a
@@ -432,6 +434,7 @@ struct Impl : HandleBase {
     PU_CUDA(cudaMalloc(&rs.ticket, sizeof(unsigned int) * 32));
     PU_CUDA(cudaMemset(rs.ticket, 0, sizeof(unsigned int) * 32));
     PU_CUDA(cudaMallocHost(&pinned_done, sizeof(int)));
+    PU_CUDA(cudaMalloc(&held, sizeof(double) * PU_MAX_SUMS));
     return set_smem_attrs();
   }
 
@@ -514,10 +517,12 @@ struct Impl : HandleBase {
   // pcg.py:59-79: start-up (+ the candidate step) and z0 = M r0, p0 = z0
   int pcg_setup(const T* b, const T* x0, T* x, const T* dv, const T* dh, T* r, T* p0, T* p1, T* spec,
                 int max_iters, double rel_tol, PcgCtrl* ctrl, double* norms, cudaStream_t st,
-                const CandArgs<T>* cand) {
+                const CandArgs<T>* cand, bool prestarted = false) {
     const int vg = vec_grid();
     cudaEvent_t e = tm.begin(st);
-    if (cand && !b) {  // b = build_rhs(gv, gh) formed in the kernel
+    if (prestarted) {  // r and cand came from k_accept_start_v; its sums wait in `held`
+      k_fin_start_held<<<1, 32, 0, st>>>(ctrl, norms, held, rel_tol, max_iters);
+    } else if (cand && !b) {  // b = build_rhs(gv, gh) formed in the kernel
       k_pcg_start_v<T, true, true><<<vg, 256, 0, st>>>(g, b, x0, x, r, dv, dh, ctrl, norms, rel_tol, max_iters, rs,
                                                         S_START, *cand);
     } else if (cand) {
@@ -1127,6 +1132,41 @@ int pu_accept_weights(pu_handle* h, const void* xa, const void* xb, const double
     I.tm.end(ST(stream), te_, TK_ACCEPT, -1);
   });
   return PU_OK;
+}
+
+int pu_accept_weights_start(pu_handle* h, const void* xa, const void* xb, const double* sel, void* dst,
+                            const void* gv, const void* gh, const void* cv, const void* ch, const void* wkv,
+                            const void* wkh, void* wnv, void* wnh, void* dv, void* dh, double* out, double lipschitz,
+                            void* r, void* cand, void* stream) {
+  if (dst == xa || dst == xb) return fail(PU_ERR_ARG, "dst must not alias xa or xb");
+  if ((cv == nullptr) != (ch == nullptr)) return fail(PU_ERR_ARG, "cv and ch must both be given or both NULL");
+  if (!(lipschitz > 0)) return fail(PU_ERR_ARG, "lipschitz constant must be positive");
+  if (!r || !cand || !gv || !gh) return fail(PU_ERR_ARG, "r, cand, gv and gh are required");
+  PU_DISPATCH(h, {
+    if (I.band) return fail(PU_ERR_ARG, "pu_accept_weights_start runs on whole grids (bands use pu_pcg_begin)");
+    cudaEvent_t te_ = I.tm.begin(ST(stream));
+    k_accept_start_v<T><<<I.vec_grid(), 256, 0, ST(stream)>>>(
+        I.g, CP(xa), CP(xb), sel, MP(dst), CP(gv), CP(gh), CP(cv), CP(ch), CP(wkv), CP(wkh), MP(wnv), MP(wnh),
+        MP(dv), MP(dh), I.rs, S_ACC, out, MP(r), (T)(-1.0 / lipschitz), MP(cand), I.held);
+    PU_LAUNCH_CHECK();
+    I.tm.end(ST(stream), te_, TK_ACCEPT, -1);
+  });
+  return PU_OK;
+}
+
+int pu_irls_begin_z0(pu_handle* h, const void* dv, const void* dh, double rel_tol, void* r, void* p0, void* p1,
+                     void* spec, void* ctrl, double* res_norms, void* stream) {
+  if (rel_tol < 0) return fail(PU_ERR_ARG, "rel_tol must be >= 0");
+  PU_DISPATCH(h, {
+    cudaStream_t st = ST(stream);
+    auto body = [&]() -> int {
+      return I.pcg_setup(nullptr, nullptr, nullptr, CP(dv), CP(dh), MP(r), MP(p0), MP(p1), MP(spec), 1 << 30,
+                         rel_tol, reinterpret_cast<PcgCtrl*>(ctrl), res_norms, st, nullptr, true);
+    };
+    return run_graph(I, {3ull, dbits(rel_tol), PU_KP(dv), PU_KP(dh), PU_KP(r), PU_KP(p0), PU_KP(p1), PU_KP(spec),
+                         PU_KP(ctrl), PU_KP(res_norms)},
+                     st, true, body);
+  });
 }
 
 int pu_timing_enable(pu_handle* h, int on) {

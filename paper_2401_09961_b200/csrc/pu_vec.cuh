@@ -683,4 +683,152 @@ __global__ void __launch_bounds__(256, PU_MINB(T, 2)) k_accept_weights_v(Grid g,
   if (red_final<6>(acc, rs, site, tot) && threadIdx.x == 0) fin_hpair6(g, tot, out);
 }
 
+
+// k_accept_weights_v of iteration k fused with the budget-free start of
+// iteration k + 1 (k_pcg_start_v<T, true, true> on the accepted state):
+// dst = (sel[1] ? xa : xb) with u -= sel[0]; w_next, d; H(dst, w_k),
+// H(dst, w_next) -> out[0..1] (fin_hpair6); then from the same registers
+// r = b - A dst with b = build_rhs(gv, gh), cand = dst - (1/L) grad H(dst,
+// w_next), and the start-up sums ||b||^2, ||r0||^2, rho_s(r0) -> held[0..2]
+// (fin_start runs later, in pu_irls_begin_z0, so the PCG control block is
+// untouched until the host has snapshot iteration k).  One pass over the
+// accepted state instead of two: 20 planes moved instead of 14 + 15.  Same
+// per-cell arithmetic and per-thread accumulation order as the two kernels
+// (same grid), so every value and sum is bit-identical to them.
+template <typename T>
+__global__ void __launch_bounds__(256, PU_MINB(T, 2)) k_accept_start_v(
+    Grid g, const T* __restrict__ xa, const T* __restrict__ xb, const double* sel, T* __restrict__ dst,
+    const T* __restrict__ gv, const T* __restrict__ gh, const T* __restrict__ cv, const T* __restrict__ ch,
+    const T* __restrict__ wkv, const T* __restrict__ wkh, T* __restrict__ wnv, T* __restrict__ wnh,
+    T* __restrict__ dv, T* __restrict__ dh, RedScratch rs, int site, double* out, T* __restrict__ r,
+    T neg_inv_lip, T* __restrict__ cand, double* held) {
+  const long long P = g.plane, ld = g.ld;
+  const T* x = sel[1] != 0.0 ? xa : xb;
+  const T mean = (T)sel[0];
+  const T d2 = (T)(g.delta * g.delta);
+  const T inv = (T)g.inv_tau;
+  // old_v, old_h, new_v, new_h, pen_v, pen_h | ||b||^2, ||r0||^2, rho_s
+  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  PU_FOR_CHUNKS(g, i, j0) {
+    const long long o = (long long)i * ld + j0;
+    const bool hasb = dn_ok(g, i), hasa = up_ok(g, i);
+    Stencil4<T> s;  // the accepted state, centred (as k_pcg_start_v reads dst)
+    s.u = ldg4(x + o);
+    s.v = ldg4(x + o + P);
+    s.h = ldg4(x + o + 2 * P);
+    s.ua = hasa ? ldg4(x + o - ld) : zero4<T>();
+    s.va = hasa ? ldg4(x + o - ld + P) : zero4<T>();
+    s.ub = hasb ? ldg4(x + o + ld) : zero4<T>();
+    s.ul = ldg_or0(x + o - 1, j0 > 0);
+    s.hl = ldg_or0(x + o - 1 + 2 * P, j0 > 0);
+    s.ur = ldg_or0(x + o + 4, j0 + 4 < g.m);
+    const Q4<T> g1 = ldg4(gv + o), g2 = ldg4(gh + o);
+    const Q4<T> ga = hasa ? ldg4(gv + o - ld) : zero4<T>();
+    const T gl = ldg_or0(gh + o - 1, j0 > 0);
+    Q4<T> c1 = ones4<T>(), c2 = ones4<T>();
+    if (cv) { c1 = ldg4(cv + o); c2 = ldg4(ch + o); }
+    const Q4<T> p1 = ldg4(wkv + o), p2 = ldg4(wkh + o);
+    // centring (irls.py:210): cells past the last column stay zero, as stored
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool ok = j0 + k < g.m;
+      s.u.a[k] = ok ? s.u.a[k] - mean : (T)0;
+      s.ua.a[k] = (ok && hasa) ? s.ua.a[k] - mean : (T)0;
+      s.ub.a[k] = (ok && hasb) ? s.ub.a[k] - mean : (T)0;
+    }
+    if (j0 > 0) s.ul = s.ul - mean;
+    if (j0 + 4 < g.m) s.ur = s.ur - mean;
+    // weights of k + 1 and the H pair (k_accept_weights_v)
+    Q4<T> w1, w2, e1, e2;
+    T part[4] = {(T)0, (T)0, (T)0, (T)0};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
+      const bool okv = hasb && j < g.m, okh = j < g.m - 1;
+      const T a = c1.a[k] * s.v.a[k], bb = c2.a[k] * s.h.a[k];
+      const T wa = sqrt(a * a + d2), wb = sqrt(bb * bb + d2);
+      w1.a[k] = okv ? wa : (T)1;
+      w2.a[k] = okh ? wb : (T)1;
+      e1.a[k] = okv ? c1.a[k] * c1.a[k] / wa : (T)0;
+      e2.a[k] = okh ? c2.a[k] * c2.a[k] / wb : (T)0;
+      if (okv) {
+        part[0] += slack4(c1.a[k], s.v.a[k], p1.a[k], d2);
+        part[2] += slack4(c1.a[k], s.v.a[k], wa, d2);
+      }
+      if (okh) {
+        part[1] += slack4(c2.a[k], s.h.a[k], p2.a[k], d2);
+        part[3] += slack4(c2.a[k], s.h.a[k], wb, d2);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] += (double)part[q];
+    pen4<T>(g, i, j0, s.u, s.ub, s.ur, s.v, s.h, g1, g2, acc[4], acc[5]);
+    st4(dst + o, s.u); st4(dst + o + P, s.v); st4(dst + o + 2 * P, s.h);
+    st4(wnv + o, w1); st4(wnh + o, w2); st4(dv + o, e1); st4(dh + o, e2);
+    // start-up of k + 1 (k_pcg_start_v<T, true, true>)
+    Q4<T> au, av, ah;
+    apply4<T>(g, i, j0, s, e1, e2, au, av, ah);
+    T pb = (T)0, pr = (T)0, prz = (T)0;
+    Q4<T> ru, rv, rh;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
+      const bool ok = j < g.m;
+      const T gvo = (ok && hasb) ? g1.a[k] : (T)0, gvm = ok ? ga.a[k] : (T)0;
+      const T gho = (j < g.m - 1) ? g2.a[k] : (T)0;
+      const T ghm = (ok && j > 0) ? ((k == 0) ? gl : g2.a[k - 1]) : (T)0;
+      const T bu = ok ? inv * ((gvm - gvo) + (ghm - gho)) : (T)0;
+      const T bv = ok ? -inv * gvo : (T)0;
+      const T bh = ok ? -inv * gho : (T)0;
+      ru.a[k] = add_rn(bu, -au.a[k]);
+      rv.a[k] = add_rn(bv, -av.a[k]);
+      rh.a[k] = add_rn(bh, -ah.a[k]);
+      pb += bu * bu + bv * bv + bh * bh;
+      pr += ru.a[k] * ru.a[k] + rv.a[k] * rv.a[k] + rh.a[k] * rh.a[k];
+      const T zv = (hasb && j < g.m) ? slack_div(rv.a[k], e1.a[k] + inv) : (T)0;
+      const T zh = (j < g.m - 1) ? slack_div(rh.a[k], e2.a[k] + inv) : (T)0;
+      prz += rv.a[k] * zv + rh.a[k] * zh;
+    }
+    acc[6] += (double)pb;
+    acc[7] += (double)pr;
+    acc[8] += (double)prz;
+    st4(r + o, ru); st4(r + o + P, rv); st4(r + o + 2 * P, rh);
+    Q4<T> ou, ov, oh;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
+      const bool ok = j < g.m, hash = j < g.m - 1;
+      const T uo = s.u.a[k];
+      const T left = (k == 0) ? s.ul : s.u.a[k - 1];
+      const T right = (k == 3) ? s.ur : s.u.a[k + 1];
+      const T hleft = (k == 0) ? s.hl : s.h.a[k - 1];
+      const T gleft = (k == 0) ? gl : g2.a[k - 1];
+      T rvv = 0, rvm = 0, rhh = 0, rhm = 0;
+      if (hasb) rvv = ((s.ub.a[k] - uo) - g1.a[k]) - s.v.a[k];
+      if (hasa) rvm = ((uo - s.ua.a[k]) - ga.a[k]) - s.va.a[k];
+      if (hash) rhh = ((right - uo) - g2.a[k]) - s.h.a[k];
+      if (j > 0) rhm = ((uo - left) - gleft) - hleft;
+      const T gu = inv * ((rvm - rvv) + (rhm - rhh));
+      const T cv2 = cv ? c1.a[k] * c1.a[k] : (T)1, ch2 = cv ? c2.a[k] * c2.a[k] : (T)1;
+      const T gvv = slack_div(cv2, w1.a[k]) * s.v.a[k] - inv * rvv;
+      const T gvh = slack_div(ch2, w2.a[k]) * s.h.a[k] - inv * rhh;
+      ou.a[k] = ok ? add_rn(uo, mul_rn(neg_inv_lip, gu)) : (T)0;
+      ov.a[k] = (ok && hasb) ? add_rn(s.v.a[k], mul_rn(neg_inv_lip, gvv)) : (T)0;
+      oh.a[k] = hash ? add_rn(s.h.a[k], mul_rn(neg_inv_lip, gvh)) : (T)0;
+    }
+    st4(cand + o, ou); st4(cand + o + P, ov); st4(cand + o + 2 * P, oh);
+  }
+  double tot[9];
+  if (grid_reduce<9>(acc, rs, site, tot) && threadIdx.x == 0) {
+    fin_hpair6(g, tot, out);
+    held[0] = tot[6]; held[1] = tot[7]; held[2] = tot[8];
+  }
+}
+
+// pu_irls_begin_z0: fin_start from the start-up sums held by k_accept_start_v
+__global__ void k_fin_start_held(PcgCtrl* ctrl, double* res_norms, const double* held, double rel_tol,
+                                 int max_iters) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) fin_start(ctrl, res_norms, held, rel_tol, max_iters);
+}
+
 }  // namespace pu

@@ -10,6 +10,8 @@ outer iteration, to read the H_delta pair that drives the budget decision
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from .device import Workspace, _ptr
@@ -17,6 +19,21 @@ from .params import (BudgetDecision, IrlsParams, IrlsTrace, IterationRecord, Mod
                      UnwrapResult, cg_budget_update, lipschitz_constant, relative_improvement)
 from .pcg import raise_if_breakdown
 from .phase import WeightField, validate_wrapped
+
+# pu_accept_weights_start: acceptance of k and the start-up of k + 1 in one
+# pass.  Used in fp32 on grids of >= 2048^2 cells: the fp64 build of the fused
+# kernel spills (measured slower than two kernels), and on small grids the
+# start-up is what keeps the GPU busy while the host applies the budget rule
+# (C1 512^2: 10.3 -> 10.6 ms fused; C3 fp32: 120.1 -> 116.5 ms).
+# PU_FUSED_START=0 / 1 forces it off / on (A/B timing).
+FUSED_START = os.environ.get("PU_FUSED_START", "auto")
+FUSED_START_MIN_CELLS = 2048 * 2048
+
+
+def _fuse_start(ws):
+    if FUSED_START in ("0", "1"):
+        return FUSED_START == "1"
+    return ws.tdtype == _torch().float32 and ws.n * ws.m >= FUSED_START_MIN_CELLS
 
 
 def _torch():
@@ -39,7 +56,10 @@ class DeviceUnwrap:
     def __init__(self, ws: Workspace):
         self.ws = ws
         self.S = [ws.buf("state0", 3), ws.buf("state1", 3)]  # state ping-pong
-        self.C = ws.buf("cand", 3)       # explicit-gradient candidate
+        # explicit-gradient candidate of iteration k in Cs[k & 1] (the fused
+        # acceptance of k reads Cs[k & 1] while it writes the candidate of k + 1)
+        self.Cs = [ws.buf("cand", 3), ws.buf("cand1", 3)]
+        self.prestarted = False
         self.G = ws.buf("grad", 2)       # gv, gh
         self.W = None                    # arc weights cv, ch (None: uniform)
         self.Wt = [ws.buf("w0", 2), ws.buf("w1", 2)]
@@ -66,6 +86,7 @@ class DeviceUnwrap:
                 float(lo), st)
         ws.call("pu_init_state", _ptr(self.G[0]), _ptr(self.G[1]), _ptr(self.S[0]), st)
         self.cur = 0
+        self.prestarted = False
         cv, ch = self._c()
         w = self.Wt[0]  # w_0, d_0 (irls.py:173, 191)
         ws.call("pu_weights_hpair", _ptr(self.S[0]), cv, ch, _ptr(self.G[0]), _ptr(self.G[1]), None, None,
@@ -74,37 +95,51 @@ class DeviceUnwrap:
     def step(self, k, m_cg, params: IrlsParams, lip):
         """irls.py:191-215 for iteration k, then the weights of k + 1."""
         self.begin(k, params, lip)
-        self.finish(k, m_cg, params)
+        self.finish(k, m_cg, params, lip)
 
     def begin(self, k, params: IrlsParams, lip):
         """The budget-independent half of iteration k (pu_irls_begin): candidate
         step, PCG start-up, z0 = M r0.  Leaves the state untouched, so it may run
-        before the host has decided whether iteration k happens at all."""
+        before the host has decided whether iteration k happens at all.  When
+        the previous finish() already ran the candidate step and start-up
+        (pu_accept_weights_start), only their finalisation and z0 remain."""
         ws, st = self.ws, self.ws.stream()
         cv, ch = self._c()
         w = self.Wt[k & 1]
         norms = ws.ensure_norms(64)
+        if self.prestarted:
+            self.prestarted = False
+            ws.call("pu_irls_begin_z0", _ptr(self.D[0]), _ptr(self.D[1]), float(params.cg_rel_tol), _ptr(self.R),
+                    _ptr(self.P[0]), _ptr(self.P[1]), _ptr(self.spec), _ptr(ws.ctrl), _ptr(norms), st)
+            return
         # b = NULL: the right-hand side build_rhs(gv, gh) (operators.py:156-162)
         # is formed inside the start-up kernel from its gradient loads
         ws.call("pu_irls_begin", _ptr(self.S[self.cur]), None, _ptr(self.G[0]), _ptr(self.G[1]), cv, ch,
                 _ptr(w[0]), _ptr(w[1]), _ptr(self.D[0]), _ptr(self.D[1]), float(lip), float(params.cg_rel_tol),
-                _ptr(self.C), _ptr(self.R), _ptr(self.P[0]), _ptr(self.P[1]), _ptr(self.spec), _ptr(ws.ctrl),
+                _ptr(self.Cs[k & 1]), _ptr(self.R), _ptr(self.P[0]), _ptr(self.P[1]), _ptr(self.spec), _ptr(ws.ctrl),
                 _ptr(norms), st)
 
-    def finish(self, k, m_cg, params: IrlsParams):
+    def finish(self, k, m_cg, params: IrlsParams, lip=None):
         """The budget's PCG iterations + H pair (pu_irls_iterate), then the
-        acceptance and the weights of k + 1 (pu_accept_weights)."""
+        acceptance and the weights of k + 1 (pu_accept_weights; with `lip`,
+        pu_accept_weights_start, which also runs the candidate step and PCG
+        start-up of k + 1 in the same pass)."""
         ws, st = self.ws, self.ws.stream()
         cv, ch = self._c()
         cur, nxt = self.S[self.cur], self.S[1 - self.cur]
         w, wn = self.Wt[k & 1], self.Wt[(k + 1) & 1]
         norms = ws.ensure_norms(max(m_cg, 64))
         ws.call("pu_irls_iterate", _ptr(cur), _ptr(self.G[0]), _ptr(self.G[1]), cv, ch, _ptr(w[0]), _ptr(w[1]),
-                _ptr(self.D[0]), _ptr(self.D[1]), int(m_cg), _ptr(self.C), _ptr(self.R), _ptr(self.P[0]),
+                _ptr(self.D[0]), _ptr(self.D[1]), int(m_cg), _ptr(self.Cs[k & 1]), _ptr(self.R), _ptr(self.P[0]),
                 _ptr(self.P[1]), _ptr(self.spec), _ptr(ws.ctrl), _ptr(norms), ws.sp(ws.S_HPROP), st)
-        ws.call("pu_accept_weights", _ptr(cur), _ptr(self.C), ws.sp(ws.S_MEAN), _ptr(nxt), _ptr(self.G[0]),
-                _ptr(self.G[1]), cv, ch, _ptr(w[0]), _ptr(w[1]), _ptr(wn[0]), _ptr(wn[1]), _ptr(self.D[0]),
-                _ptr(self.D[1]), ws.sp(ws.S_HACC), st)
+        args = (_ptr(cur), _ptr(self.Cs[k & 1]), ws.sp(ws.S_MEAN), _ptr(nxt), _ptr(self.G[0]), _ptr(self.G[1]), cv, ch,
+                _ptr(w[0]), _ptr(w[1]), _ptr(wn[0]), _ptr(wn[1]), _ptr(self.D[0]), _ptr(self.D[1]),
+                ws.sp(ws.S_HACC))
+        if lip is not None and _fuse_start(ws):
+            ws.call("pu_accept_weights_start", *args, float(lip), _ptr(self.R), _ptr(self.Cs[(k + 1) & 1]), st)
+            self.prestarted = True
+        else:
+            ws.call("pu_accept_weights", *args, st)
         self.cur = 1 - self.cur
 
     @property
@@ -179,7 +214,7 @@ class _LoopJob:
         and applies the budget rule."""
         if k == 0:
             self.run.begin(0, self.params, self.lip)
-        self.run.finish(k, m_cg, self.params)
+        self.run.finish(k, m_cg, self.params, self.lip)
         self.ws.snapshot()
         if k + 1 < self.params.max_outer_iters:
             self.run.begin(k + 1, self.params, self.lip)

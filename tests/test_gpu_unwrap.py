@@ -161,3 +161,36 @@ def test_release_workspaces_and_replan():
     pu.release_workspaces()
     b = pu.unwrap(x, dtype="fp32")
     np.testing.assert_array_equal(a.u, b.u)
+
+
+@pytest.mark.parametrize("name", ["noisy96x80", "weighted40x36", "bumps24x31", "row1x30", "col30x1", "pixel1x1"])
+@pytest.mark.parametrize("dtype", ["fp32", "fp64"])
+def test_fused_accept_start_bit_identical(monkeypatch, golden_unwrap, golden_meta, name, dtype):
+    """pu_accept_weights_start (acceptance of k + start-up of k + 1 in one
+    pass) against pu_accept_weights + pu_irls_begin: identical trace and
+    bit-identical state, on ragged grids, edges and user arc weights."""
+    from paper_2401_09961_b200 import irls
+    x, cv, ch, tau, delta, prm, lo = case_inputs(golden_unwrap, golden_meta, name)
+    params = pu.IrlsParams(**prm.__dict__)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setattr(irls, "FUSED_START", mode)
+        out[mode] = pu.unwrap(x, _weights(cv, ch), pu.ModelParams(tau, delta), params, lo, dtype=dtype)
+    a, b = out["0"], out["1"]
+    assert [(r.m_cg, r.cg_iters, r.h_delta, r.sufficient_decrease) for r in a.trace.records] == \
+        [(r.m_cg, r.cg_iters, r.h_delta, r.sufficient_decrease) for r in b.trace.records]
+    for f in ("u", "vv", "vh"):
+        np.testing.assert_array_equal(getattr(a, f), getattr(b, f))
+
+
+def test_fused_accept_start_auto_rule():
+    """The fused start-up is used in fp32 from 2048^2 cells (the default
+    bench workload) and not in fp64 or on small grids."""
+    from paper_2401_09961_b200 import irls
+    from paper_2401_09961_b200.device import Workspace
+    import torch
+    dev = torch.device("cuda", 0)
+    assert irls._fuse_start(Workspace.get(2048, 2048, "fp32", 1e-2, 1e-6, dev))
+    assert not irls._fuse_start(Workspace.get(2048, 2048, "fp64", 1e-2, 1e-6, dev))
+    assert not irls._fuse_start(Workspace.get(512, 512, "fp32", 1e-2, 1e-6, dev))
+    pu.release_workspaces()
