@@ -695,8 +695,12 @@ __global__ void __launch_bounds__(256, PU_MINB(T, 2)) k_accept_weights_v(Grid g,
 // accepted state instead of two: 20 planes moved instead of 14 + 15.  Same
 // per-cell arithmetic and per-thread accumulation order as the two kernels
 // (same grid), so every value and sum is bit-identical to them.
+// (fp32: 2 CTAs/SM, 104 B of spills, 0.268 ms at C3; 1 CTA/SM at 196
+// registers without spills: 0.333 ms.  fp64 is not used: 0.865 ms spilling
+// vs 0.80 for the two kernels; 1 CTA/SM would win (0.70) but its FMA
+// contraction differs from the two-kernel build in the last bits.)
 template <typename T>
-__global__ void __launch_bounds__(256, PU_MINB(T, 2)) k_accept_start_v(
+__global__ void __launch_bounds__(256, 2) k_accept_start_v(
     Grid g, const T* __restrict__ xa, const T* __restrict__ xb, const double* sel, T* __restrict__ dst,
     const T* __restrict__ gv, const T* __restrict__ gh, const T* __restrict__ cv, const T* __restrict__ ch,
     const T* __restrict__ wkv, const T* __restrict__ wkh, T* __restrict__ wnv, T* __restrict__ wnh,
