@@ -195,7 +195,8 @@ int pu_accept_weights_start(pu_handle* h, const void* xa, const void* xb, const 
                             void* r, void* cand, void* stream);
 /* The rest of pu_irls_begin after pu_accept_weights_start: finalise the held
  * start-up sums into ctrl/res_norms (pcg.py:59-75) and z0 = M r0, rho0,
- * p0 = z0 (pcg.py:77-79).  Replayed as a CUDA graph. */
+ * p0 = z0 (pcg.py:77-79).  Replayed as a CUDA graph.  PU_ERR_ARG unless a
+ * pu_accept_weights_start on the same handle precedes it. */
 int pu_irls_begin_z0(pu_handle* h, const void* dv, const void* dh, double rel_tol, void* r, void* p0, void* p1,
                      void* spec, void* ctrl, double* res_norms, void* stream);
 

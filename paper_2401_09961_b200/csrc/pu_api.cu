@@ -347,6 +347,7 @@ struct Impl : HandleBase {
   RedScratch rs{};
   int* pinned_done = nullptr;
   double* held = nullptr;  // start-up sums of k_accept_start_v, finalised by pu_irls_begin_z0
+  bool held_pending = false;  // host-side: an accept_start was enqueued and not yet finalised
   DctOps<T> rops{}, cops{};  // transform kernels for the row / column internal lengths
   Timer tm;
   GraphCache graphs;
@@ -1149,6 +1150,7 @@ int pu_accept_weights_start(pu_handle* h, const void* xa, const void* xb, const 
         I.g, CP(xa), CP(xb), sel, MP(dst), CP(gv), CP(gh), CP(cv), CP(ch), CP(wkv), CP(wkh), MP(wnv), MP(wnh),
         MP(dv), MP(dh), I.rs, S_ACC, out, MP(r), (T)(-1.0 / lipschitz), MP(cand), I.held);
     PU_LAUNCH_CHECK();
+    I.held_pending = true;
     I.tm.end(ST(stream), te_, TK_ACCEPT, -1);
   });
   return PU_OK;
@@ -1158,6 +1160,8 @@ int pu_irls_begin_z0(pu_handle* h, const void* dv, const void* dh, double rel_to
                      void* spec, void* ctrl, double* res_norms, void* stream) {
   if (rel_tol < 0) return fail(PU_ERR_ARG, "rel_tol must be >= 0");
   PU_DISPATCH(h, {
+    if (!I.held_pending) return fail(PU_ERR_ARG, "pu_irls_begin_z0 must follow pu_accept_weights_start");
+    I.held_pending = false;
     cudaStream_t st = ST(stream);
     auto body = [&]() -> int {
       return I.pcg_setup(nullptr, nullptr, nullptr, CP(dv), CP(dh), MP(r), MP(p0), MP(p1), MP(spec), 1 << 30,

@@ -194,3 +194,17 @@ def test_fused_accept_start_auto_rule():
     assert not irls._fuse_start(Workspace.get(2048, 2048, "fp64", 1e-2, 1e-6, dev))
     assert not irls._fuse_start(Workspace.get(512, 512, "fp32", 1e-2, 1e-6, dev))
     pu.release_workspaces()
+
+
+def test_begin_z0_requires_accept_start():
+    """pu_irls_begin_z0 finalises sums that only pu_accept_weights_start
+    leaves behind; on its own it is an argument error, not garbage."""
+    from paper_2401_09961_b200.device import Workspace, _ptr
+    import torch
+    ws = Workspace.get(24, 20, "fp32", 1e-2, 1e-6, torch.device("cuda", 0))
+    r, p0, p1, d = ws.buf("t_r", 3), ws.buf("t_p0", 3), ws.buf("t_p1", 3), ws.buf("t_d", 2)
+    spec = ws.buf("t_spec", 1)
+    with pytest.raises(ValueError, match="must follow"):
+        ws.call("pu_irls_begin_z0", _ptr(d[0]), _ptr(d[1]), 1e-6, _ptr(r), _ptr(p0), _ptr(p1), _ptr(spec),
+                _ptr(ws.ctrl), _ptr(ws.ensure_norms(64)), ws.stream())
+    pu.release_workspaces()
