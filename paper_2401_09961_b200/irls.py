@@ -30,6 +30,19 @@ FUSED_START = os.environ.get("PU_FUSED_START", "auto")
 FUSED_START_MIN_CELLS = 2048 * 2048
 
 
+# b = build_rhs(gv, gh) formed inside the start-up kernel (b = NULL at the C
+# ABI) instead of stored once and read by every start-up: fp32 only (C3 fp32
+# -0.5%; in fp64 the extra registers spill and the start-up is 2.6% slower).
+# PU_RHS_IN_KERNEL=0 / 1 forces stored / formed (A/B timing).
+RHS_IN_KERNEL = os.environ.get("PU_RHS_IN_KERNEL", "auto")
+
+
+def _rhs_in_kernel(ws):
+    if RHS_IN_KERNEL in ("0", "1"):
+        return RHS_IN_KERNEL == "1"
+    return ws.tdtype == _torch().float32
+
+
 def _fuse_start(ws):
     if FUSED_START in ("0", "1"):
         return FUSED_START == "1"
@@ -59,6 +72,7 @@ class DeviceUnwrap:
         # explicit-gradient candidate of iteration k in Cs[k & 1] (the fused
         # acceptance of k reads Cs[k & 1] while it writes the candidate of k + 1)
         self.Cs = [ws.buf("cand", 3), ws.buf("cand1", 3)]
+        self.B = None                    # stored rhs (None: formed in the start-up kernel)
         self.prestarted = False
         self.G = ws.buf("grad", 2)       # gv, gh
         self.W = None                    # arc weights cv, ch (None: uniform)
@@ -84,6 +98,11 @@ class DeviceUnwrap:
         self._x = x64.contiguous()
         ws.call("pu_wrapped_gradients", _ptr(self._x), int(self._x.shape[1]), _ptr(self.G[0]), _ptr(self.G[1]),
                 float(lo), st)
+        if _rhs_in_kernel(ws):
+            self.B = None
+        else:
+            self.B = ws.buf("rhs", 3)
+            ws.call("pu_build_rhs", _ptr(self.G[0]), _ptr(self.G[1]), _ptr(self.B), st)
         ws.call("pu_init_state", _ptr(self.G[0]), _ptr(self.G[1]), _ptr(self.S[0]), st)
         self.cur = 0
         self.prestarted = False
@@ -114,7 +133,7 @@ class DeviceUnwrap:
             return
         # b = NULL: the right-hand side build_rhs(gv, gh) (operators.py:156-162)
         # is formed inside the start-up kernel from its gradient loads
-        ws.call("pu_irls_begin", _ptr(self.S[self.cur]), None, _ptr(self.G[0]), _ptr(self.G[1]), cv, ch,
+        ws.call("pu_irls_begin", _ptr(self.S[self.cur]), None if self.B is None else _ptr(self.B), _ptr(self.G[0]), _ptr(self.G[1]), cv, ch,
                 _ptr(w[0]), _ptr(w[1]), _ptr(self.D[0]), _ptr(self.D[1]), float(lip), float(params.cg_rel_tol),
                 _ptr(self.Cs[k & 1]), _ptr(self.R), _ptr(self.P[0]), _ptr(self.P[1]), _ptr(self.spec), _ptr(ws.ctrl),
                 _ptr(norms), st)

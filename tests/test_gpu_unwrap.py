@@ -183,6 +183,23 @@ def test_fused_accept_start_bit_identical(monkeypatch, golden_unwrap, golden_met
         np.testing.assert_array_equal(getattr(a, f), getattr(b, f))
 
 
+@pytest.mark.parametrize("dtype", ["fp32", "fp64"])
+def test_rhs_in_kernel_bit_identical(monkeypatch, golden_unwrap, golden_meta, dtype):
+    """b formed in the start-up kernel (b = NULL) against b stored by
+    pu_build_rhs: identical trace and bit-identical state."""
+    from paper_2401_09961_b200 import irls
+    x, cv, ch, tau, delta, prm, lo = case_inputs(golden_unwrap, golden_meta, "weighted40x36")
+    params = pu.IrlsParams(**prm.__dict__)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setattr(irls, "RHS_IN_KERNEL", mode)
+        monkeypatch.setattr(irls, "FUSED_START", "0")
+        out[mode] = pu.unwrap(x, _weights(cv, ch), pu.ModelParams(tau, delta), params, lo, dtype=dtype)
+    assert [r.cg_iters for r in out["0"].trace.records] == [r.cg_iters for r in out["1"].trace.records]
+    np.testing.assert_array_equal(out["0"].u, out["1"].u)
+    np.testing.assert_array_equal(out["0"].vh, out["1"].vh)
+
+
 def test_fused_accept_start_auto_rule():
     """The fused start-up is used in fp32 from 2048^2 cells (the default
     bench workload) and not in fp64 or on small grids."""
