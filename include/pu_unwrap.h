@@ -181,8 +181,8 @@ int pu_accept_weights(pu_handle* h, const void* xa, const void* xb, const double
                       const void* gh, const void* cv, const void* ch, const void* wkv, const void* wkh, void* wnv,
                       void* wnh, void* dv, void* dh, double* out, void* stream);
 
-/* pu_accept_weights of iteration k (irls.py:206-215, 173-177) fused with the
- * budget-free start of iteration k + 1 (irls.py:191-199: objective.py:118-125
+/* pu_accept_weights of iteration k (irls.py:203-215, 173-177) fused with the
+ * budget-free start of iteration k + 1 (irls.py:191-202: objective.py:118-125
  * candidate, pcg.py:59-75 start-up; the kernel of pu_irls_begin, b = NULL):
  * besides dst, w_next, d and out[0..1] it writes r = b - A dst
  * (b = build_rhs(gv, gh)) and cand = dst - (1/L) grad H(dst, w_next) from the
