@@ -66,3 +66,18 @@ def test_full_size_kmap_fp32_vs_fp64(scenes):
     r32 = pu.unwrap(x, dtype="fp32")
     frac = metrics.kmap_mismatch(r32.u, r64.u, x)
     assert frac <= 1e-3, frac
+
+
+def test_full_size_fused_start_bit_identical(scenes, monkeypatch):
+    """At C2 fp32 the default path fuses the acceptance with the next
+    start-up (pu_accept_weights_start); the two-kernel path gives the same
+    trace and bit-identical state."""
+    from paper_2401_09961_b200 import irls
+    x = scenes["c2"]
+    fused = pu.unwrap(x, dtype="fp32")
+    monkeypatch.setattr(irls, "FUSED_START", "0")
+    plain = pu.unwrap(x, dtype="fp32")
+    assert [(r.cg_iters, r.h_delta) for r in fused.trace.records] == \
+        [(r.cg_iters, r.h_delta) for r in plain.trace.records]
+    for f in ("u", "vv", "vh"):
+        np.testing.assert_array_equal(getattr(fused, f), getattr(plain, f))
