@@ -202,7 +202,8 @@ def test_rhs_in_kernel_bit_identical(monkeypatch, golden_unwrap, golden_meta, dt
 
 def test_fused_accept_start_auto_rule():
     """The fused start-up is used in fp32 from 2048^2 cells (the default
-    bench workload) and not in fp64 or on small grids."""
+    bench workload) or when unwraps run concurrently, and not in fp64 or on
+    small single grids."""
     from paper_2401_09961_b200 import irls
     from paper_2401_09961_b200.device import Workspace
     import torch
@@ -210,6 +211,7 @@ def test_fused_accept_start_auto_rule():
     assert irls._fuse_start(Workspace.get(2048, 2048, "fp32", 1e-2, 1e-6, dev))
     assert not irls._fuse_start(Workspace.get(2048, 2048, "fp64", 1e-2, 1e-6, dev))
     assert not irls._fuse_start(Workspace.get(512, 512, "fp32", 1e-2, 1e-6, dev))
+    assert irls._fuse_start(Workspace.get(512, 512, "fp32", 1e-2, 1e-6, dev), concurrent=True)
     pu.release_workspaces()
 
 
