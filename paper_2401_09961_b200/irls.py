@@ -67,6 +67,10 @@ class DeviceUnwrap:
                         of iteration k+1 and H(accepted, w_{k+1})
                         (irls.py:206-215, 173-177)
     so the host reads one scalar block per iteration for the budget rule.
+    pu_irls_step runs as its two halves (pu_irls_begin, budget-free, enqueued
+    speculatively; pu_irls_iterate).  With _fuse_start, the acceptance is
+    pu_accept_weights_start, which also runs the candidate step and PCG
+    start-up of k + 1, and the next begin shrinks to pu_irls_begin_z0.
     """
 
     def __init__(self, ws: Workspace):
