@@ -78,20 +78,25 @@ def ncu_traffic(kind, dtype, n):
 
 
 def algorithmic_bytes(n, m, e):
-    """per-launch compulsory bytes of K1..K4 and of one PCG iteration."""
+    """Compulsory HBM bytes per launch of K1..K4 as the kernels are fused
+    (DESIGN.md §4), and of one PCG iteration.
+
+    SURVEY.md §8(d) charges one iteration (8S + 3s + 5u) e = (13u + 11s) e,
+    which stores z_s; the fused schedule never stores z_s (K1 recomputes it
+    from r_s and d) and so moves (13u + 10s) e, the figure used here."""
     u = n * m
     s = (n - 1) * m + n * (m - 1)
     S = u + s
-    return {
-        "K1_p_Ap_pAp": (3 * S + s) * e,          # z, p_old, d read; p written
-        "K2a_update_norms": (5 * S + 2 * s) * e,  # p, d, x, r read; x, r, z_s written
-        "K2b_row_dct": 2 * u * e,                # r_u read; T written
-        "K3_coldct_spectral": 2 * u * e,
-        "K4_row_idct": 2 * u * e,
-        # compulsory traffic of one iteration (SURVEY §8(d)); the split K2a/K2b
-        # re-reads r_u once (one plane) beyond it
-        "iteration": (8 * S + 3 * s + 5 * u) * e,
+    k = {
+        "K1_p_Ap_pAp": (u + 4 * s) * e,          # p_u (from K4), p_s old, r_s, d read; p_s written
+        "K2a_update_norms": (5 * S + s) * e,     # p, d, x, r read; x, r written
+        "K2b_row_dct": 2 * u * e,                # r_u read; spectrum written
+        "K3_coldct_spectral": 2 * u * e,         # spectrum read and written back (in place)
+        "K4_row_idct": 3 * u * e,                # spectrum, p_u old read; p_u written
     }
+    k["iteration"] = sum(k.values())              # = (13u + 10s) e
+    k["iteration_survey"] = (8 * S + 3 * s + 5 * u) * e
+    return k
 
 
 class ClockSampler:

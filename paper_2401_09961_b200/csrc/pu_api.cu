@@ -1039,6 +1039,7 @@ int pu_irls_begin(pu_handle* h, void* state, const void* b, const void* gv, cons
   if (!(lipschitz > 0)) return fail(PU_ERR_ARG, "lipschitz constant must be positive");
   if ((cv == nullptr) != (ch == nullptr)) return fail(PU_ERR_ARG, "cv and ch must both be given or both NULL");
   PU_DISPATCH(h, {
+    I.held_pending = false;  // a full start-up supersedes any held accept_start sums
     cudaStream_t st = ST(stream);
     auto body = [&]() -> int {
       const CandArgs<T> ca{CP(gv), CP(gh), CP(cv), CP(ch), CP(wv), CP(wh), (T)(-1.0 / lipschitz), MP(cand)};
@@ -1125,6 +1126,7 @@ int pu_accept_weights(pu_handle* h, const void* xa, const void* xb, const double
   if (dst == xa || dst == xb) return fail(PU_ERR_ARG, "dst must not alias xa or xb");
   if ((cv == nullptr) != (ch == nullptr)) return fail(PU_ERR_ARG, "cv and ch must both be given or both NULL");
   PU_DISPATCH(h, {
+    I.held_pending = false;  // the plain acceptance leaves no start-up sums behind
     cudaEvent_t te_ = I.tm.begin(ST(stream));
     k_accept_weights_v<T><<<I.vec_grid(), 256, 0, ST(stream)>>>(I.g, CP(xa), CP(xb), sel, MP(dst), CP(gv), CP(gh),
                                                                CP(cv), CP(ch), CP(wkv), CP(wkh), MP(wnv), MP(wnh),

@@ -12,6 +12,7 @@ from __future__ import annotations
 import ctypes
 import json
 import threading
+import weakref
 
 import numpy as np
 
@@ -29,8 +30,46 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
 
 
+_tls = threading.local()
+_claimed: set = set()
+_claim_lock = threading.Lock()
+
+
+class _SlotToken:
+    __slots__ = ("idx", "__weakref__")
+
+
+def _release_slot(idx):
+    with _claim_lock:
+        _claimed.discard(idx)
+
+
+def thread_slot() -> int:
+    """Index of the calling thread's workspace set.
+
+    Independent unwrap calls are safe to run concurrently (reference
+    SPEC.md:391, 453-454), so no two live threads may share a device handle
+    (its buffers, scalar block, reduction tickets and graph cache).  Each
+    thread claims the lowest free index on first use; the claim is released
+    when the thread ends (its thread-local token is collected), so the next
+    thread reuses the cached workspaces instead of allocating new ones."""
+    tok = getattr(_tls, "token", None)
+    if tok is None:
+        with _claim_lock:
+            idx = 0
+            while idx in _claimed:
+                idx += 1
+            _claimed.add(idx)
+        tok = _SlotToken()
+        tok.idx = idx
+        weakref.finalize(tok, _release_slot, idx)
+        _tls.token = tok
+    return tok.idx
+
+
 class Workspace:
-    """Handle + buffers for one (N, M, dtype, tau, delta); reused across calls."""
+    """Handle + buffers for one (N, M, dtype, tau, delta); reused across calls
+    of the same thread (thread_slot)."""
 
     _cache: dict = {}
     _lock = threading.Lock()
@@ -42,11 +81,12 @@ class Workspace:
 
     @classmethod
     def get(cls, n, m, dtype="fp64", tau=1e-2, delta=1e-6, device=None, slot=0):
-        """Cached workspace; `slot` > 0 gives independent buffer sets for
-        concurrent unwraps of the same size (irls.unwrap_many)."""
+        """Cached workspace of the calling thread; `slot` > 0 gives independent
+        buffer sets for concurrent unwraps of the same size within one thread
+        (irls.unwrap_many)."""
         torch = _torch()
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        key = (n, m, dtype, float(tau), float(delta), dev.index, int(slot))
+        key = (n, m, dtype, float(tau), float(delta), dev.index, thread_slot(), int(slot))
         with cls._lock:
             ws = cls._cache.get(key)
             if ws is None:

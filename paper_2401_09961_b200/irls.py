@@ -162,7 +162,7 @@ class DeviceUnwrap:
         args = (_ptr(cur), _ptr(self.Cs[k & 1]), ws.sp(ws.S_MEAN), _ptr(nxt), _ptr(self.G[0]), _ptr(self.G[1]), cv, ch,
                 _ptr(w[0]), _ptr(w[1]), _ptr(wn[0]), _ptr(wn[1]), _ptr(self.D[0]), _ptr(self.D[1]),
                 ws.sp(ws.S_HACC))
-        if lip is not None and _fuse_start(ws, self.concurrent):
+        if lip is not None and _fuse_start(ws, self.concurrent) and k + 1 < params.max_outer_iters:
             ws.call("pu_accept_weights_start", *args, float(lip), _ptr(self.R), _ptr(self.Cs[(k + 1) & 1]), st)
             self.prestarted = True
         else:
@@ -173,6 +173,12 @@ class DeviceUnwrap:
     def state(self):
         return self.S[self.cur]
 
+    def detach(self):
+        """A copy of the result-bearing buffers (state, gradients, arc
+        weights) that stays valid after this workspace runs another unwrap."""
+        return DetachedUnwrap(self.ws, self.state.clone(), self.G.clone(),
+                              None if self.W is None else self.W.clone())
+
     def result_arrays(self):
         return self.ws.from_system(self.state)
 
@@ -181,6 +187,28 @@ class DeviceUnwrap:
         if self.W is not None:
             return self.W
         ones = self.ws.buf("ones", 2)
+        self.ws.call("pu_fill", _ptr(ones), 2, 1.0, self.ws.stream())
+        return ones
+
+
+class DetachedUnwrap:
+    """Result of one unwrap held in its own device buffers (unwrap_many with
+    download=False); same read-side interface as DeviceUnwrap."""
+
+    def __init__(self, ws, state, G, W):
+        self.ws, self._state, self.G, self.W = ws, state, G, W
+
+    @property
+    def state(self):
+        return self._state
+
+    def result_arrays(self):
+        return self.ws.from_system(self._state)
+
+    def weight_planes(self):
+        if self.W is not None:
+            return self.W
+        ones = self.ws.planes(2)
         self.ws.call("pu_fill", _ptr(ones), 2, 1.0, self.ws.stream())
         return ones
 
@@ -298,6 +326,12 @@ def unwrap_many(xs, c: WeightField | None = None, model: ModelParams | None = No
     if not xs:
         return []
     n, m = int(xs[0].shape[0]), int(xs[0].shape[1])
+    for xi in xs:
+        if isinstance(xi, np.ndarray) and not np.issubdtype(xi.dtype, np.number):
+            raise ValueError("phase grid must be numeric")
+        if len(xi.shape) != 2 or tuple(xi.shape) != (n, m):
+            raise ValueError(f"all grids must share one 2-D shape, got {tuple(xi.shape)} vs {(n, m)}")
+    _check_call(c, n, m, gradient_lo)
     slots = max(1, min(int(concurrency), len(xs)))
     wss = [Workspace.get(n, m, dtype, model.tau, model.delta, dev, slot=s) for s in range(slots)]
     caller = torch.cuda.current_stream(dev)
@@ -332,6 +366,10 @@ def unwrap_many(xs, c: WeightField | None = None, model: ModelParams | None = No
                     if download:
                         u, vv, vh = ws.download_system(job.run.state)
                         out[i] = UnwrapResult(u=u, vv=vv, vh=vh, trace=job.trace)
+                    elif nxt < len(xs):
+                        # the slot's buffers are about to be reused by the next
+                        # image: the result keeps its own copy of what it needs
+                        out[i] = (job.run.detach(), job.trace)
                     else:
                         out[i] = (job.run, job.trace)
             if finished:
@@ -340,6 +378,16 @@ def unwrap_many(xs, c: WeightField | None = None, model: ModelParams | None = No
                 if nxt < len(xs):
                     start(slot)
     return out
+
+
+def _check_call(c, n, m, gradient_lo):
+    """The argument checks of irls.py:157-160 (weight shapes) and
+    phase.py:140-149 (gradient interval), shared by unwrap and unwrap_many so
+    a mis-shaped WeightField raises instead of being cropped or padded."""
+    if c is not None and (c.cv.shape != (n - 1, m) or c.ch.shape != (n, m - 1)):
+        raise ValueError(f"weight shapes {c.cv.shape}/{c.ch.shape} do not match grid {(n, m)}")
+    if gradient_lo not in (0.0, 0, -np.pi):
+        raise ValueError(f"lo must be 0 or -pi, got {gradient_lo!r}")
 
 
 def _validate_device(x_dev):
@@ -382,10 +430,7 @@ def unwrap(x, c: WeightField | None = None, model: ModelParams | None = None, pa
     n, m = int(x_dev.shape[0]), int(x_dev.shape[1])
     model = model or ModelParams()
     params = params or IrlsParams()
-    if c is not None and (c.cv.shape != (n - 1, m) or c.ch.shape != (n, m - 1)):
-        raise ValueError(f"weight shapes {c.cv.shape}/{c.ch.shape} do not match grid {(n, m)}")
-    if gradient_lo not in (0.0, 0, -np.pi):
-        raise ValueError(f"lo must be 0 or -pi, got {gradient_lo!r}")
+    _check_call(c, n, m, gradient_lo)
     # the host is idle while the device loop runs: allocate and page in the
     # result arrays meanwhile, so the final widening copy touches no new pages
     import threading

@@ -1,4 +1,4 @@
-"""Command line (cli.py, arrayio.py) on the host: argument handling and exit
+"""Command line (cli.py, gridfile.py) on the host: argument handling and exit
 codes of the reference CLI (cli.py:1-253, tests/test_cli.py) that are decided
 before any device work, the host subcommands, and the NPY contract."""
 
@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from paper_2401_09961_b200 import cli
-from paper_2401_09961_b200.arrayio import ArrayFileError, load_grid, save_grid
+from paper_2401_09961_b200.gridfile import GridFileError, read_grid as load_grid, write_grid as save_grid
 
 
 def run(*args):
@@ -33,10 +33,10 @@ def test_npy_roundtrip_and_validation(tmp_path):
     np.save(tmp_path / "c.npy", np.ones((2, 2, 2)))
     np.save(tmp_path / "n.npy", np.array([[1.0, np.nan]]))
     for bad in ("i.npy", "c.npy", "n.npy", "missing.npy"):
-        with pytest.raises(ArrayFileError):
+        with pytest.raises(GridFileError):
             load_grid(tmp_path / bad)
     (tmp_path / "junk.npy").write_bytes(b"not an npy file")
-    with pytest.raises(ArrayFileError):
+    with pytest.raises(GridFileError):
         load_grid(tmp_path / "junk.npy")
     with pytest.raises(ValueError):
         save_grid(tmp_path / "z.npy", a, dtype="<f2")
@@ -70,18 +70,24 @@ def test_unwrap_without_gpu_fails_loudly(wrapped, tmp_path, capsys):
     assert not (tmp_path / "u.npy").exists()
 
 
-def test_synth_and_error(tmp_path, capsys):
-    truth, wr = tmp_path / "t.npy", tmp_path / "w.npy"
-    assert run("synth", "--kind", "gaussian-bumps", "--rows", 16, "--cols", 12, "--amplitude", 5, "--scale", 3,
-               "--seed", 2, "--wrap", "--noise-sigma", 0.1, "--out-truth", truth, "--out-wrapped", wr) == 0
-    t, w = load_grid(truth), load_grid(wr)
-    assert t.shape == w.shape == (16, 12) and w.min() >= 0 and w.max() < 2 * np.pi
-    assert run("synth", "--kind", "ramp", "--rows", 4, "--cols", 4) == cli.EXIT_BAD_INPUT
-    assert run("synth", "--kind", "ramp", "--rows", 4, "--cols", 4, "--out-wrapped", wr) == cli.EXIT_BAD_INPUT
-    shifted = tmp_path / "s.npy"
-    save_grid(shifted, t + 4 * np.pi)
-    assert run("error", "--estimate", shifted, "--truth", truth, "--json-out", tmp_path / "e.json") == 0
-    rep = json.loads((tmp_path / "e.json").read_text())
-    assert abs(abs(rep["alpha"]) - 4 * np.pi) < 1e-9 and rep["rmse"] < 1e-9 and rep["congruent_fraction"] == 1.0
-    save_grid(tmp_path / "small.npy", t[:4])
-    assert run("error", "--estimate", tmp_path / "small.npy", "--truth", truth) == cli.EXIT_DIM_MISMATCH
+def test_host_utilities_not_exposed():
+    """synth / error / spectrum are host utilities outside the GPU path."""
+    for sub in ("synth", "error", "spectrum"):
+        with pytest.raises(SystemExit):
+            run(sub)
+
+
+def test_fortran_order_and_atomic_write(tmp_path):
+    a = np.asfortranarray(np.arange(12.0).reshape(3, 4))
+    np.save(tmp_path / "f.npy", a)
+    np.testing.assert_array_equal(load_grid(tmp_path / "f.npy"), a)
+    np.save(tmp_path / "o.npy", np.array([[object()]], dtype=object), allow_pickle=True)
+    with pytest.raises(GridFileError):
+        load_grid(tmp_path / "o.npy")
+    (tmp_path / "t.npy").write_bytes(open(tmp_path / "f.npy", "rb").read()[:-8])  # truncated payload
+    with pytest.raises(GridFileError):
+        load_grid(tmp_path / "t.npy")
+    with pytest.raises(ValueError):
+        save_grid(tmp_path / "bad.npy", np.ones(3))
+    assert not (tmp_path / "bad.npy").exists()
+    assert [p.name for p in tmp_path.iterdir() if p.name.startswith(".grid-")] == []

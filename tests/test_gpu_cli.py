@@ -9,7 +9,7 @@ import pytest
 
 from cases import case_inputs, golden_trace
 from paper_2401_09961_b200 import cli
-from paper_2401_09961_b200.arrayio import load_grid, save_grid
+from paper_2401_09961_b200.gridfile import read_grid as load_grid, write_grid as save_grid
 
 pytestmark = pytest.mark.gpu
 pu = pytest.importorskip("paper_2401_09961_b200")

@@ -227,3 +227,70 @@ def test_begin_z0_requires_accept_start():
         ws.call("pu_irls_begin_z0", _ptr(d[0]), _ptr(d[1]), 1e-6, _ptr(r), _ptr(p0), _ptr(p1), _ptr(spec),
                 _ptr(ws.ctrl), _ptr(ws.ensure_norms(64)), ws.stream())
     pu.release_workspaces()
+
+
+def _scene(seed, n=96, m=80):
+    return pu.add_phase_noise(pu.wrap_scene(pu.generate_scene(pu.SceneSpec("gaussian-bumps", n, m, 12.0, 9.0,
+                                                                          seed))), 0.5, 100 + seed)
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_concurrent_threads_equal_sequential(dtype):
+    """Independent unwrap calls are safe concurrently (reference SPEC.md:391,
+    453-454): same-shape unwraps from several threads at once return exactly
+    what sequential calls return."""
+    import threading
+    xs = [_scene(s) for s in range(4)]
+    seq = [pu.unwrap(x, dtype=dtype) for x in xs]
+    out = [None] * len(xs)
+    barrier = threading.Barrier(len(xs))
+
+    def work(i):
+        barrier.wait()
+        for _ in range(2):
+            out[i] = pu.unwrap(xs[i], dtype=dtype)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(len(xs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for a, b in zip(seq, out):
+        assert [r.cg_iters for r in a.trace.records] == [r.cg_iters for r in b.trace.records]
+        np.testing.assert_array_equal(a.u, b.u)
+        np.testing.assert_array_equal(a.vv, b.vv)
+
+
+def test_unwrap_many_device_results_survive_slot_reuse():
+    """download=False with more grids than slots: every returned device result
+    still holds its own image's state (the slot's buffers were reused)."""
+    xs = [_scene(s, 64, 72) for s in range(5)]
+    seq = [pu.unwrap(x, dtype="fp32") for x in xs]
+    dev = pu.unwrap_many(xs, dtype="fp32", concurrency=2, download=False)
+    for a, (run, trace) in zip(seq, dev):
+        u, vv, vh = run.result_arrays()
+        assert [r.cg_iters for r in a.trace.records] == [r.cg_iters for r in trace.records]
+        np.testing.assert_array_equal(a.u, u.cpu().numpy())
+        np.testing.assert_array_equal(a.vh, vh.cpu().numpy())
+
+
+def test_unwrap_many_checks_weight_shapes():
+    xs = [_scene(s, 32, 30) for s in range(2)]
+    bad = pu.WeightField(np.ones((31, 30)), np.ones((32, 28)))
+    with pytest.raises(ValueError, match="weight shapes"):
+        pu.unwrap_many(xs, bad)
+    with pytest.raises(ValueError, match="lo must be"):
+        pu.unwrap_many(xs, gradient_lo=1.0)
+
+
+def test_last_iteration_leaves_no_held_startup(monkeypatch):
+    """max_outer_iters reached right after a fused acceptance: the next
+    unwrap on the same workspace starts clean (held_pending reset)."""
+    from paper_2401_09961_b200 import irls
+    monkeypatch.setattr(irls, "FUSED_START", "1")
+    x = _scene(7, 64, 64)
+    p = pu.IrlsParams(max_outer_iters=3)
+    a = pu.unwrap_many([x], None, None, p, dtype="fp32", concurrency=1)[0]
+    b = pu.unwrap_many([x], None, None, p, dtype="fp32", concurrency=1)[0]
+    np.testing.assert_array_equal(a.u, b.u)
+    assert len(a.trace) == 3
