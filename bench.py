@@ -271,6 +271,20 @@ def run_reference(args, rank, world):
         note = "; rows [0, 2048) of the input timed and scaled x8 by pixels"
     extra_setups = 63 if args.config == "c5" else 0
 
+    full = None
+    if args.ref_full == "on" or (args.ref_full == "auto" and args.config in REF_COUNTS):
+        # step 0: one COMPLETE reference unwrap (the port of irls.py:132-224 with
+        # the reference's dense-eigenbasis preconditioner), timed end to end
+        from oracle import phaseirls_port as port
+        t0 = time.perf_counter()
+        _st, recs, _g = port.unwrap(np.ascontiguousarray(x), poisson="dense")
+        t_full = time.perf_counter() - t0
+        n_outer, n_pcg = len(recs), int(sum(r.cg_iters for r in recs))
+        counts = f"iteration counts of the complete run ({n_outer} outer / {n_pcg} PCG)"
+        full = {"seconds": t_full, "mpix_s": total_pix / t_full / 1e6, "pcg_it_s": n_pcg / t_full,
+                "n_outer": n_outer, "n_pcg": n_pcg}
+        del _st, _g
+
     cache = {}
 
     def sample():
@@ -284,17 +298,26 @@ def run_reference(args, rank, world):
     steps = args.steps if args.steps_ref is None else args.steps_ref
     for _ in range(warmup):
         sample()
-    samples = [sample() for _ in range(max(1, steps))]
-    secs = statistics.median(s["seconds"] for s in samples)
+    # with a complete run, it is step 0 and the model fills the other steps
+    samples = [sample() for _ in range(max(1, steps - (1 if full else 0)))]
+    model_secs = statistics.median(s["seconds"] for s in samples)
+    secs = full["seconds"] if full else model_secs
     value = total_pix / secs / 1e6
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": len(samples), "warmup": warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
+        "steps": len(samples) + (1 if full else 0), "warmup": warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD[args.config], "n": n, "m": m, "cpu": model},
         "pcg_iters_per_s": n_pcg / secs,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": samples[0]["sample"] + f"; {counts}{note}"},
+                         "sample": (("one complete reference unwrap of the full input (oracle/phaseirls_port.py, "
+                                     "dense LAPACK eigenbasis preconditioner as preconditioner.py:64-100), timed "
+                                     f"end to end: {secs:.1f} s; the other steps: " if full else "")
+                                    + samples[0]["sample"] + f"; {counts}{note}")},
+        "reference_full_run": full,
+        "model": {"seconds": model_secs, "error_vs_full": (model_secs - full["seconds"]) / full["seconds"]
+                  if full else None, "samples": len(samples),
+                  "how": "set-up + 1 PCG iteration + 1 outer iteration timed, scaled to the iteration counts"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "detail": {k: v for k, v in samples[0].items() if k != "sample"},
     }
@@ -312,13 +335,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=("c1", "c2", "c3", "c4", "c5"), default="c3")
-    ap.add_argument("--dtype", choices=("fp32", "fp64"), default="fp32")
+    ap.add_argument("--dtype", choices=("fp32", "fp64"), default="fp64",
+                    help="headline arithmetic (fp64 = the reference's precision); the other mode is nested")
+    ap.add_argument("--no-nested", action="store_true", help="skip the nested run of the other dtype")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="only run N unwraps (for ncu launch lists); prints no JSON")
     ap.add_argument("--shard", choices=("auto", "images", "rows"), default="auto",
-                    help="N>1: independent images per rank, or one image row-sharded over the ranks "
-                         "(auto: rows for c4, images otherwise)")
+                    help="N>1: one image row-sharded over the ranks (auto for c1-c4: strong scaling), or "
+                         "independent images per rank (auto for c5: weak scaling)")
     ap.add_argument("--concurrency", type=int, default=8, help="c5: images in flight per GPU")
     ap.add_argument("--peer", action="store_true",
                     help="--shard rows: transpose fused into the row kernels over peer memory (default: all-to-all)")
@@ -326,27 +351,26 @@ def main():
                     help="--shard rows without torchrun: B bands in this process (loopback collectives)")
     ap.add_argument("--warmup-ref", type=int, default=None, help="reference arm (default: --warmup)")
     ap.add_argument("--steps-ref", type=int, default=None, help="reference arm (default: --steps)")
+    ap.add_argument("--ref-full", choices=("auto", "on", "off"), default="auto",
+                    help="reference arm: time one complete reference unwrap as step 0 (auto: c1-c3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.profile_steps == 0 else args.warmup
 
     rank, local_rank, world = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
-
     import torch
     import torch.distributed as dist
-    import paper_2401_09961_b200 as pu
     from paper_2401_09961_b200 import _native
-    from paper_2401_09961_b200.device import Workspace
-    from paper_2401_09961_b200.irls import unwrap_device
-    from paper_2401_09961_b200.batch import max_over_ranks, shard_indices
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     lib = _native.ensure()
-    shard = args.shard if args.shard != "auto" else ("rows" if args.config == "c4" and world > 1 else "images")
+    shard = args.shard
+    if shard == "auto":
+        shard = "rows" if (world > 1 or args.bands) and args.config != "c5" else "images"
     if shard == "rows":
         if args.config == "c5":
             raise SystemExit("--shard rows needs a single-image config (c1-c4)")
@@ -354,65 +378,115 @@ def main():
         if world > 1:
             dist.destroy_process_group()
         return rc
+    rc = main_images(args, rank, local_rank, world, dev, lib)
+    if world > 1:
+        dist.destroy_process_group()
+    return rc
 
-    # this rank's images: one C1-C3 image per rank, or its shard of the 64 C5 images
-    if args.config == "c5":
-        mine = shard_indices(64, rank, world)
-        xs = [pu.config_scene("c5", b)[1] for b in mine]
-    else:
-        xs = [pu.config_scene(args.config)[1]]
+
+def parity_block(config, xs, results, dtype):
+    """Reference-precision parity of this run's result against the committed
+    outputs of the unmodified reference on the same input
+    (tests/parity_configs.py; north_star: fp64 u within 1e-8, fp32 F within
+    1e-3, K-map mismatch reported).  None when no fixture covers `config`."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    try:
+        import parity_configs as pc
+    except ImportError:
+        return None
+    have = pc.available()
+    names = [config] if config != "c5" else [f"c5b{b}" for b in range(len(xs))]
+    out = []
+    for name, x, res in zip(names, xs, results):
+        if name not in have or res is None:
+            continue
+        r = pc.compare(name, x, res.u, res.vv, res.vh, res.trace)
+        out.append({k: r[k] for k in ("config", "u_rel_sub", "u_rel_lines", "u_norm_rel", "kmap_mismatch", "F",
+                                      "F_ref", "F_rel", "trace_equal", "outer", "pcg", "h_rel")})
+    if not out:
+        return None
+    worst = {
+        "u_rel": max(max(o["u_rel_sub"], o["u_rel_lines"]) for o in out),
+        "kmap_mismatch": max(o["kmap_mismatch"] for o in out),
+        "F_rel": max(o["F_rel"] for o in out),
+        "trace_equal": all(o["trace_equal"] for o in out),
+        "images": len(out),
+    }
+    bar = ({"u_rel": pc.FP64_U_REL, "ok": worst["u_rel"] <= pc.FP64_U_REL and worst["trace_equal"]}
+           if dtype == "fp64" else {"F_rel": pc.FP32_F_REL, "ok": worst["F_rel"] <= pc.FP32_F_REL})
+    return {"against": "outputs of the unmodified reference on the same input (tests/golden/configs)",
+            "dtype": dtype, "worst": worst, "bar": bar, "per_image": out if len(out) <= 4 else out[:4]}
+
+
+def measure_images(args, dtype, xs, rank, local_rank, world, dev, lib, with_clocks=True):
+    """One dtype mode on this rank's images: device-resident timed region,
+    instrumented per-kernel pass, end to end through the public API from
+    numpy, and parity of the e2e results.  Returns the measurement dict."""
+    import torch
+    import paper_2401_09961_b200 as pu
+    from paper_2401_09961_b200.device import Workspace, _ptr
+    from paper_2401_09961_b200.irls import unwrap_device
+    from paper_2401_09961_b200.batch import max_over_ranks
+
     n_img = len(xs)
-    x = xs[0]
-    n, m = x.shape
+    n, m = xs[0].shape
     model, params = pu.ModelParams(), pu.IrlsParams()
-    ws = Workspace.get(n, m, args.dtype, model.tau, model.delta, dev)
+    ws = Workspace.get(n, m, dtype, model.tau, model.delta, dev)
     x_devs = [torch.from_numpy(xi).to(dev) for xi in xs]
 
     def one_unwrap_sequential():
         for x_dev in x_devs:
-            run, trace = unwrap_device(x_dev, None, model, params, -np.pi, args.dtype, ws)
+            run, trace = unwrap_device(x_dev, None, model, params, -np.pi, dtype, ws)
         return run, trace
 
     def one_unwrap():
         if n_img == 1:
             return one_unwrap_sequential()
         # C5: the rank's images in flight concurrently (one workspace + stream each)
-        res = pu.unwrap_many(x_devs, None, model, params, -np.pi, dtype=args.dtype, concurrency=args.concurrency,
+        res = pu.unwrap_many(x_devs, None, model, params, -np.pi, dtype=dtype, concurrency=args.concurrency,
                              download=False)
         return res[-1]
 
-    if args.profile_steps:
-        for _ in range(args.profile_steps):
-            one_unwrap()
-        torch.cuda.synchronize()
-        return 0
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
 
     for _ in range(args.warmup):
         run, trace = one_unwrap()
     torch.cuda.synchronize()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
     # ---- timed region: device-resident input, CUDA graphs, no instrumentation ----
     ws.timing(False)
     launches0 = lib.pu_launch_count()
     traces = []
-    with ClockSampler(local_rank) as clocks:
-        barrier()
-        torch.cuda.synchronize()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        for _ in range(args.steps):
-            run, trace = one_unwrap()
-            traces.append(trace)
-        ev1.record()
-        torch.cuda.synchronize()
-        barrier()
+    clocks = ClockSampler(local_rank) if with_clocks else None
+    if clocks:
+        clocks.__enter__()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        run, trace = one_unwrap()
+        traces.append(trace)
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier()
+    if clocks:
+        clocks.__exit__(None, None, None)
     launches = lib.pu_launch_count() - launches0
     step_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, device=dev)
     value = world * n_img * n * m / (step_ms / 1e3) / 1e6
+
+    # objective of the device result (pu_eval_f) before anything else reuses the buffers
+    f_out = None
+    try:
+        cw = run.weight_planes()
+        ws.call("pu_eval_f", _ptr(run.state), _ptr(run.G[0]), _ptr(run.G[1]), _ptr(cw[0]), _ptr(cw[1]),
+                ws.sp(ws.S_F), ws.stream())
+        f_out = float(ws.read_block()[0][ws.S_F])
+    except Exception:
+        pass
 
     # ---- kernel timing pass: the same K steps again with a CUDA-event pair
     # around every launch on the launching stream (graphs off: event nodes
@@ -432,25 +506,18 @@ def main():
     kinds, its, ms = ws.read_timing()
     instrumented_ms = ev2.elapsed_time(ev3) / args.steps
 
-    # per-kernel statistics (skip launches that returned early after PCG exit)
-    e = 4 if args.dtype == "fp32" else 8
+    e = 4 if dtype == "fp32" else 8
     alg = algorithmic_bytes(n, m, e)
     hbm, peak_kind = peaks()
-    per_kind = {}
-    for kd in np.unique(kinds):
-        sel = ms[kinds == kd]
-        ran = sel[sel >= 0.25 * np.median(sel)] if sel.size else sel
-        name = Workspace.TIME_KINDS[kd] if kd < len(Workspace.TIME_KINDS) else str(kd)
-        per_kind[name] = {"launches": int(sel.size), "ran": int(ran.size), "total_ms": float(ran.sum()),
-                          "avg_ms": float(ran.mean()) if ran.size else 0.0}
+    per_kind = kernel_stats(kinds, ms, Workspace.TIME_KINDS)
     timed_total = sum(v["total_ms"] for v in per_kind.values())
     dom = max((k for k in per_kind if k in alg), key=lambda k: per_kind[k]["total_ms"])
     achieved = alg[dom] / (per_kind[dom]["avg_ms"] / 1e3) / 1e9 if per_kind[dom]["avg_ms"] > 0 else None
     n_pcg = sum(r.cg_iters for r in traces[-1].records)     # per image
     n_outer = len(traces[-1].records)
-    iter_ms = sum(per_kind[k]["total_ms"] for k in ("K1_p_Ap_pAp", "K2a_update_norms", "K2b_row_dct",
-                                                    "K3_coldct_spectral", "K4_row_idct", "reproject_update")
-                  if k in per_kind) / max(1, args.steps * n_img * n_pcg)
+    iter_kinds = ("K1_p_Ap_pAp", "K2a_update_norms", "K2b_row_dct", "K3_coldct_spectral", "K4_row_idct",
+                  "reproject_update")
+    iter_ms = sum(per_kind[k]["total_ms"] for k in iter_kinds if k in per_kind) / max(1, args.steps * n_pcg)
     # per-iteration time implied by the clean timed step: step time minus the
     # (event-timed) once-per-outer-iteration kernels, over the PCG iterations
     outer_kinds = ("pcg_start", "weights_hpair", "candidate", "hpair_states", "accept_center")
@@ -462,18 +529,22 @@ def main():
             init_ms += t
     init_ms /= args.steps
     pcg_ms_from_step = (step_ms - outer_ms - init_ms) / max(1, n_img * n_pcg)
+    traffic = ncu_traffic(dom, dtype, n)
     roofline = {
         "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
         "frac": achieved / hbm if achieved else None,
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "bytes_per_launch": alg[dom],
+        "bytes_how": "compulsory bytes of the fused kernel (DESIGN.md §4): " + {
+            "K1_p_Ap_pAp": "(u + 4s) e", "K2a_update_norms": "(5S + s) e", "K2b_row_dct": "2u e",
+            "K3_coldct_spectral": "2u e", "K4_row_idct": "3u e"}[dom],
         "avg_launch_ms": per_kind[dom]["avg_ms"], "share_of_kernel_time": per_kind[dom]["total_ms"] / timed_total,
-        "traffic": ncu_traffic(dom, args.dtype, n),
-        "note": ("achieved = algorithmic bytes / event-timed launch time; frac > 1 means part of the algorithmic "
-                 "operands (the direction p just written by K1/K4) is served from the 126 MB L2 - traffic is the "
-                 "ncu DRAM bytes of the same kernel"),
-        "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)",
-        "pcg_iteration": {"bytes": alg["iteration"], "ms": iter_ms,
-                          "how": "sum of the per-iteration kernels' event-timed durations",
+        "traffic": traffic,
+        "traffic_source": ("profiles/ncu_traffic.json (ncu --set full, dram__bytes_read.sum + "
+                           "dram__bytes_write.sum)") if traffic else None,
+        "pcg_iteration": {"bytes": alg["iteration"], "bytes_how": "(13u + 10s) e: K1..K4 as fused (z_s never "
+                                                                  "stored); SURVEY §8(d) (13u + 11s) e = "
+                                                                  f"{alg['iteration_survey']}",
+                          "ms": iter_ms, "how": "sum of the per-iteration kernels' event-timed durations",
                           "achieved_gbs": alg["iteration"] / (iter_ms / 1e3) / 1e9 if iter_ms else None,
                           "frac": (alg["iteration"] / (iter_ms / 1e3) / 1e9) / hbm if iter_ms else None,
                           "ms_from_step": pcg_ms_from_step,
@@ -481,73 +552,118 @@ def main():
                                              if pcg_ms_from_step else None)},
     }
 
-    # objective of the result (device eval_f) against the reference's F
-    f_out = None
-    try:
-        cw = run.weight_planes()
-        ws.call("pu_eval_f", pu.device._ptr(run.state), pu.device._ptr(run.G[0]), pu.device._ptr(run.G[1]),
-                pu.device._ptr(cw[0]), pu.device._ptr(cw[1]), ws.sp(ws.S_F), ws.stream())
-        f_out = float(ws.read_block()[0][ws.S_F])
-    except Exception:
-        pass
-
-    # ---- end to end through the public API: pinned host input -> host result ----
-    x_pins = [torch.from_numpy(xi).pin_memory() for xi in xs]
+    # ---- end to end through the public API: numpy fp64 input (pageable, as a
+    # caller holds it) -> host numpy result arrays ----
     e2e_ms = []
+    results = None
     for i in range(args.steps + 1):
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         if n_img == 1:
-            res = pu.unwrap(x_pins[0], dtype=args.dtype)
+            results = [pu.unwrap(xs[0], dtype=dtype)]
         else:
-            res = pu.unwrap_many(x_pins, dtype=args.dtype, concurrency=args.concurrency)[-1]
+            results = pu.unwrap_many(xs, dtype=dtype, concurrency=args.concurrency)
         t1 = time.perf_counter()
         if i > 0:
             e2e_ms.append((t1 - t0) * 1e3)
     e2e_step = max_over_ranks(statistics.mean(e2e_ms), device=dev)
     h2d = n_img * n * m * 8
     # the results travel in the compute dtype and are widened to fp64 on the host
-    d2h = n_img * (res.u.size + res.vv.size + res.vh.size) * (4 if args.dtype == "fp32" else 8)
+    res = results[-1]
+    d2h = n_img * (res.u.size + res.vv.size + res.vh.size) * e
+    return {
+        "value": value, "step_ms": step_ms, "instrumented_ms": instrumented_ms, "per_kind": per_kind,
+        "roofline": roofline, "n_pcg": n_pcg, "n_outer": n_outer, "F": f_out, "launches": int(launches),
+        "clocks": clocks.summary() if clocks else None, "ws": ws, "results": results,
+        "e2e": {"value": world * n_img * n * m / (e2e_step / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step,
+                "how": "pu.unwrap / pu.unwrap_many on the pageable numpy fp64 input(s), numpy fp64 results "
+                       "(host staging, H2D, solve, D2H and widening inside the timed region)"},
+    }
+
+
+def main_images(args, rank, local_rank, world, dev, lib):
+    """Images mode: one config image per rank (c1-c4), or the rank's shard of
+    the 64 C5 images; weak scaling with no data-path collective."""
+    import paper_2401_09961_b200 as pu
+    from paper_2401_09961_b200.batch import shard_indices
+
+    if args.config == "c5":
+        mine = shard_indices(64, rank, world)
+        xs = [pu.config_scene("c5", b)[1] for b in mine]
+    else:
+        xs = [pu.config_scene(args.config)[1]]
+    n_img = len(xs)
+    n, m = xs[0].shape
+    if args.profile_steps:  # launch lists for ncu: just the unwraps
+        import torch
+        from paper_2401_09961_b200.irls import unwrap_device
+        x_devs = [torch.from_numpy(xi).to(dev) for xi in xs]
+        for _ in range(args.profile_steps):
+            if n_img == 1:
+                unwrap_device(x_devs[0], None, pu.ModelParams(), pu.IrlsParams(), -np.pi, args.dtype)
+            else:
+                pu.unwrap_many(x_devs, dtype=args.dtype, concurrency=args.concurrency, download=False)
+        torch.cuda.synchronize()
+        return 0
+    head = measure_images(args, args.dtype, xs, rank, local_rank, world, dev, lib)
+    other = "fp32" if args.dtype == "fp64" else "fp64"
+    nested = None
+    if not args.no_nested and args.config != "c4":
+        sub = measure_images(args, other, xs, rank, local_rank, world, dev, lib, with_clocks=False)
+        nested = {"dtype": "f32" if other == "fp32" else "f64", "value": sub["value"], "unit": UNIT,
+                  "ms_per_step": sub["step_ms"], "pcg_iters_per_s": world * n_img * sub["n_pcg"] / (sub["step_ms"] / 1e3),
+                  "roofline": sub["roofline"], "kernels": sub["per_kind"], "e2e": sub["e2e"],
+                  "objective": {"F": sub["F"], "F_reference": REF_F.get(args.config)},
+                  "parity": parity_block(args.config, xs, sub["results"], other) if rank == 0 else None,
+                  "gpu_launches": sub["launches"],
+                  "note": ("north_star's fp32 mode (objective within 1e-3 of the fp64 reference)" if other == "fp32"
+                           else "fp64 (the reference's precision)")}
+        del sub
 
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config != "c5":
         model_name, cores = cpu_info()
-        smp = cpu_reference_sample(x, n_outer, n_pcg)
+        x = xs[0]
+        smp = cpu_reference_sample(x, head["n_outer"], head["n_pcg"])
         cpu_base = {"value": smp["mpix_s"], "unit": UNIT, "cores": cores, "kind": "port", "sample": smp["sample"],
                     "cpu": model_name, "pcg_iters_per_s": smp["pcg_it_s"], "seconds_per_unwrap": smp["seconds"]}
-        fast = cpu_reference_sample(x, n_outer, n_pcg, poisson="dct")
+        fast = cpu_reference_sample(x, head["n_outer"], head["n_pcg"], poisson="dct")
         cpu_base["fast_cpu_restatement"] = {"value": fast["mpix_s"], "unit": UNIT, "cores": cores,
                                             "seconds_per_unwrap": fast["seconds"], "sample": fast["sample"]}
 
     if rank == 0:
+        parity = parity_block(args.config, xs, head["results"], args.dtype)
+        f_out = head["F"]
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["step_ms"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: {WORKLOAD[args.config]}", "n": n, "m": m,
                        "per_rank": f"{n_img} independent image(s) per GPU per step",
-                       "l2": "inputs larger than L2 (~1.6 GB resident working set vs 126 MB L2)",
-                       "plan": ws.describe()},
-            "unwrap_s": step_ms / 1e3,
+                       "l2": "inputs larger than L2 (resident working set >= 1.6 GB vs 126 MB L2)"
+                             if n * m >= 2048 * 2048 else "working set partly L2-resident (small grid)",
+                       "plan": head["ws"].describe()},
+            "unwrap_s": head["step_ms"] / 1e3,
             "kernel_timing": {"how": "CUDA events around every launch on its stream, second pass of the same "
-                                     f"{args.steps} steps with graphs off", "ms_per_step": instrumented_ms},
-            "pcg_iters_per_step": n_pcg, "outer_iters_per_step": n_outer,
-            "pcg_iters_per_s": world * n_img * n_pcg / (step_ms / 1e3),
-            "roofline": roofline,
-            "kernels": per_kind,
+                                     f"{args.steps} steps with graphs off", "ms_per_step": head["instrumented_ms"]},
+            "pcg_iters_per_step": head["n_pcg"], "outer_iters_per_step": head["n_outer"],
+            "pcg_iters_per_s": world * n_img * head["n_pcg"] / (head["step_ms"] / 1e3),
+            "roofline": head["roofline"],
+            "kernels": head["per_kind"],
+            "parity": parity,
             "objective": {"F": f_out, "F_reference": REF_F.get(args.config),
                           "rel": (abs(f_out - REF_F[args.config]) / REF_F[args.config])
-                          if f_out is not None and args.config in REF_F else None},
+                          if f_out is not None and args.config in REF_F else None,
+                          "note": "F_reference is the survey's 3-decimal value; parity holds the full-precision one"},
             "cpu_baseline": cpu_base,
-            "e2e": {"value": world * n_img * n * m / (e2e_step / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step},
-            "clocks": clocks.summary(),
-            "gpu_launches": int(launches),
+            "e2e": head["e2e"],
+            "nested": nested,
+            "clocks": head["clocks"],
+            "gpu_launches": head["launches"],
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
     return 0
 
 

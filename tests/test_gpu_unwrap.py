@@ -276,7 +276,7 @@ def test_unwrap_many_device_results_survive_slot_reuse():
 
 def test_unwrap_many_checks_weight_shapes():
     xs = [_scene(s, 32, 30) for s in range(2)]
-    bad = pu.WeightField(np.ones((31, 30)), np.ones((32, 28)))
+    bad = pu.WeightField(np.ones((30, 30)), np.ones((31, 29)))  # consistent, but for a 31 x 30 grid
     with pytest.raises(ValueError, match="weight shapes"):
         pu.unwrap_many(xs, bad)
     with pytest.raises(ValueError, match="lo must be"):
