@@ -34,6 +34,8 @@ CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompi
 # PU_STATIC_LS_F32 / PU_STATIC_LS_F64 in csrc/pu_dct_launch.cuh.
 INSTANCES = ([("float", ls) for ls in (0, 512, 1024, 2048, 4096, 8192, 16384)]
              + [("double", ls) for ls in (0, 512, 1024, 2048, 4096, 8192)])
+# (dtype, half length) of the 2-CTA cluster transforms (csrc/pu_split.cuh)
+SPLIT_INSTANCES = [("double", 8192), ("float", 16384)]
 
 
 def nvcc():
@@ -103,6 +105,9 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     for t, ls in INSTANCES:
         work.append((os.path.join(CSRC, "pu_dct_inst.cu"), os.path.join(OBJDIR, f"pu_dct_{t}_{ls}.o"),
                      [f"-DPU_INST_T={t}", f"-DPU_INST_LS={ls}"]))
+    for t, lh in SPLIT_INSTANCES:
+        work.append((os.path.join(CSRC, "pu_split_inst.cu"), os.path.join(OBJDIR, f"pu_split_{t}_{lh}.o"),
+                     [f"-DPU_INST_T={t}", f"-DPU_INST_LH={lh}"]))
     jobs = jobs or max(1, min(len(work), os.cpu_count() or 1))
     logs = []
     with cf.ThreadPoolExecutor(max_workers=jobs) as ex:

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "pu_dct_launch.cuh"
+#include "pu_split.cuh"
 #include "pu_vec.cuh"
 
 namespace pu {
@@ -337,6 +338,11 @@ template <typename T>
 struct Impl : HandleBase {
   Grid g{};
   HostPlan<T> prow, pcol;  // row transforms (length m), column transforms (length n)
+  // lengths 2 LHS (fp64 16384, fp32 32768): a 2-CTA cluster per sequence
+  // (pu_split.cuh); prow_h / pcol_h hold the LHS-point static plans
+  static constexpr int LHS = sizeof(T) == 4 ? 16384 : 8192;
+  bool row_split = false, col_split = false;
+  HostPlan<T> prow_h, pcol_h;
   int cols_per_cta = 2, col_threads = 64;
   int col_nfull = 1 << 30, col_nhalf = 0;  // balanced column grid: full panels, then half panels
   size_t col_smem = 0;
@@ -361,6 +367,8 @@ struct Impl : HandleBase {
   ~Impl() override {
     prow.release();
     pcol.release();
+    prow_h.release();
+    pcol_h.release();
     if (rs.partials) cudaFree(rs.partials);
     if (rs.ticket) cudaFree(rs.ticket);
     if (pinned_done) cudaFreeHost(pinned_done);
@@ -402,9 +410,14 @@ struct Impl : HandleBase {
     }
     int rc;
     if ((rc = prow.build(m)) || (rc = pcol.build(n_glob))) return rc;
+    row_split = !prow.dev.bluestein && prow.dev.L == 2 * LHS && std::getenv("PU_NO_SPLIT") == nullptr;
+    col_split = !pcol.dev.bluestein && pcol.dev.L == 2 * LHS && std::getenv("PU_NO_SPLIT") == nullptr;
+    if (row_split && (rc = prow_h.build(LHS))) return rc;
+    if (col_split && (rc = pcol_h.build(LHS))) return rc;
     // row kernels (k_rows_pipe): one row pair per CTA, whole sequence in one group
-    if (pipe_bytes(2) > kSmemLimit) prow.dev.stage1 = 1;
-    if (prow.threads_for(1) > prow.max_threads() || pipe_bytes(prow.dev.stage1 ? 1 : 2) > kSmemLimit)
+    if (!row_split && pipe_bytes(2) > kSmemLimit) prow.dev.stage1 = 1;
+    if (!row_split &&
+        (prow.threads_for(1) > prow.max_threads() || pipe_bytes(prow.dev.stage1 ? 1 : 2) > kSmemLimit))
       return fail(PU_ERR_UNSUPPORTED, "row length " + std::to_string(m) + " exceeds the shared-memory FFT limit");
     // column kernels (k_cols_spec): panel of W = 2 cc columns
     // 2 sequences (W = 4 columns) per CTA, all in one thread group (<= 512
@@ -420,7 +433,8 @@ struct Impl : HandleBase {
                             pcol.smem_for(scc) <= kSmemLimit;
     int cc = col_static ? scc : PU_PANEL_COLS / 2;
     if (!col_static && pcol.smem_for(cc) > kSmemLimit) cc = 1;
-    if (pcol.threads_for(cc) > pcol.max_threads() || pcol.smem_for(cc) > kSmemLimit)
+    if (col_split) cc = 1;  // one column pair per cluster
+    if (!col_split && (pcol.threads_for(cc) > pcol.max_threads() || pcol.smem_for(cc) > kSmemLimit))
       return fail(PU_ERR_UNSUPPORTED, "column length " + std::to_string(n_glob) + " exceeds the shared-memory FFT limit");
     col_is_static = col_static;
     cols_per_cta = 2 * cc;
@@ -455,7 +469,8 @@ struct Impl : HandleBase {
     // that handles of different sizes sharing an instantiation never shrink it
     PU_CUDA(rops.set_attrs(kSmemLimit, kSmemLimit));
     PU_CUDA(cops.set_attrs(kSmemLimit, kSmemLimit));
-    {
+    if (row_split || col_split) PU_CUDA((SplitLaunch<T, LHS>::set_attrs()));
+    if (!col_split) {
       // k_cols_spec is one CTA per SM (shared memory); when the panels leave a
       // partial last wave, turn it into half panels spread over every SM
       // (4096 fp32: 444 panels of 8 columns + 136 of 4 instead of 3.46 waves)
@@ -476,7 +491,7 @@ struct Impl : HandleBase {
     // persistent pipelined row kernels: one row pair per iteration
     pipe_threads = prow.threads_for(1);
     pipe_smem = pipe_bytes(prow.dev.stage1 ? 1 : 2);
-    if (pipe_smem > kSmemLimit)
+    if (!row_split && pipe_smem > kSmemLimit)
       return fail(PU_ERR_UNSUPPORTED, "row length " + std::to_string(g.m) + " exceeds the row pipeline staging");
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -487,6 +502,23 @@ struct Impl : HandleBase {
     return PU_OK;
   }
 
+  // row transform (K2b forward / K4 inverse) and column pass (K3 / API) of
+  // the handle's plans: one-CTA kernels, or the 2-CTA cluster split
+  cudaError_t rows(bool inv, cudaStream_t st, const T* in, T* out, const PcgCtrl* ctrl, const T* pold, int first,
+                   Pack p) {
+    if (row_split)
+      return SplitLaunch<T, LHS>::rows(inv, (g.n + 1) / 2, st, g, prow.dev, prow_h.dev, in, out, ctrl, pold, first,
+                                       p);
+    return rops.rows_pipe(inv, pl_(st), g, prow.dev, in, out, ctrl, pold, first, p);
+  }
+  cudaError_t cols(int mode, cudaStream_t st, T* data, PcgCtrl* ctrl, int it, Push ps) {
+    if (col_split)
+      return SplitLaunch<T, LHS>::cols(mode, (gc.m + 1) / 2, st, gc, pcol.dev, pcol_h.dev, prow.dev.lam + col0, data,
+                                       ctrl, rs, S_K3, it, ps);
+    return cops.cols(mode, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, data, ctrl, rs, S_K3, it, ps,
+                     col_nfull);
+  }
+
   XLaunch cl(cudaStream_t st) const { return XLaunch{col_grid(), col_threads, col_smem, st}; }
   XLaunch pl_(cudaStream_t st) const { return XLaunch{pipe_grid, pipe_threads, pipe_smem, st}; }
 
@@ -494,9 +526,9 @@ struct Impl : HandleBase {
 
   // ---- preconditioner passes ----
   int sylvester(const T* r, T* z, T* spec, cudaStream_t st) {
-    PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, nullptr, nullptr, 0, Pack{}));
-    PU_DCT(cops.cols(MODE_API, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, nullptr, rs, S_K3, 0, Push{}, col_nfull));
-    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, z, nullptr, nullptr, 0, Pack{}));
+    PU_DCT(rows(false, st, r, spec, nullptr, nullptr, 0, Pack{}));
+    PU_DCT(cols(MODE_API, st, spec, nullptr, 0, Push{}));
+    PU_DCT(rows(true, st, spec, z, nullptr, nullptr, 0, Pack{}));
     return PU_OK;
   }
 
@@ -537,15 +569,15 @@ struct Impl : HandleBase {
     tm.end(st, e, TK_START, -1);
     // z = M r, rho = r.z (pcg.py:77-79); rho_s came with the start-up sums
     e = tm.begin(st);
-    PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl, nullptr, 0, Pack{}));
+    PU_DCT(rows(false, st, r, spec, ctrl, nullptr, 0, Pack{}));
     tm.end(st, e, TK_K2B, -1);
     e = tm.begin(st);
-    PU_DCT(cops.cols(MODE_INIT, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, ctrl, rs, S_K3, -1, Push{}, col_nfull));
+    PU_DCT(cols(MODE_INIT, st, spec, ctrl, -1, Push{}));
     tm.end(st, e, TK_K3, -1);
     // p of iteration k lives in pbuf[k & 1]; K4 writes its u block (p = z at k = 0)
     T* pbuf[2] = {p0, p1};
     e = tm.begin(st);
-    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, pbuf[0], ctrl, pbuf[1], 1, Pack{}));
+    PU_DCT(rows(true, st, spec, pbuf[0], ctrl, pbuf[1], 1, Pack{}));
     tm.end(st, e, TK_K4, -1);
     return PU_OK;
   }
@@ -585,13 +617,13 @@ struct Impl : HandleBase {
         tm.end(st, e, TK_K2, it);
       }
       e = tm.begin(st);
-      PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec, ctrl, nullptr, 0, Pack{}));
+      PU_DCT(rows(false, st, r, spec, ctrl, nullptr, 0, Pack{}));
       tm.end(st, e, TK_K2B, it);
       e = tm.begin(st);
-      PU_DCT(cops.cols(MODE_ITER, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec, ctrl, rs, S_K3, it, Push{}, col_nfull));
+      PU_DCT(cols(MODE_ITER, st, spec, ctrl, it, Push{}));
       tm.end(st, e, TK_K3, it);
       e = tm.begin(st);  // u block of p for iteration it + 1: beta p_u + z_u
-      PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec, pbuf[(it + 1) & 1], ctrl, pn, 0, Pack{}));
+      PU_DCT(rows(true, st, spec, pbuf[(it + 1) & 1], ctrl, pn, 0, Pack{}));
       tm.end(st, e, TK_K4, it);
     }
     return PU_OK;
@@ -626,7 +658,7 @@ struct Impl : HandleBase {
     const int vg = vec_grid();
     cudaEvent_t e = tm.begin(st);
     if (it < 0) {  // set-up: rho_s of r0 came with pu_pcg_begin; only the row transform
-      PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec_out, ctrl, nullptr, 0, pk));
+      PU_DCT(rows(false, st, r, spec_out, ctrl, nullptr, 0, pk));
       tm.end(st, e, TK_K2B, it);
       return PU_OK;
     }
@@ -637,7 +669,7 @@ struct Impl : HandleBase {
     PU_LAUNCH_CHECK();
     tm.end(st, e, TK_K2, it);
     e = tm.begin(st);
-    PU_DCT(rops.rows_pipe(false, pl_(st), g, prow.dev, r, spec_out, ctrl, nullptr, 0, pk));
+    PU_DCT(rows(false, st, r, spec_out, ctrl, nullptr, 0, pk));
     tm.end(st, e, TK_K2B, it);
     return PU_OK;
   }
@@ -653,8 +685,7 @@ struct Impl : HandleBase {
   // K3 on the (column block of the) spectrum, in place
   int pcg_columns(T* spec, PcgCtrl* ctrl, int it, cudaStream_t st) {
     cudaEvent_t e = tm.begin(st);
-    PU_DCT(cops.cols(it < 0 ? MODE_INIT : MODE_ITER, cl(st), gc, pcol.dev, prow.dev.lam + col0, cols_per_cta, spec,
-                     ctrl, rs, S_K3, it, push, col_nfull));
+    PU_DCT(cols(it < 0 ? MODE_INIT : MODE_ITER, st, spec, ctrl, it, push));
     tm.end(st, e, TK_K3, it);
     return PU_OK;
   }
@@ -664,7 +695,7 @@ struct Impl : HandleBase {
     cudaEvent_t e = tm.begin(st);
     Pack local = pk;  // the packed rows come from the local buffer (pushed there by K3 in peer mode)
     local.peers = nullptr;
-    PU_DCT(rops.rows_pipe(true, pl_(st), g, prow.dev, spec_in, pnew, ctrl, pold, first, local));
+    PU_DCT(rows(true, st, spec_in, pnew, ctrl, pold, first, local));
     tm.end(st, e, TK_K4, it);
     return PU_OK;
   }
@@ -768,13 +799,14 @@ int pu_describe(const pu_handle* h, char* buf, int cap) {
   auto fmt = [&](auto& I) {
     std::snprintf(buf, cap,
                   "{\"n\":%d,\"m\":%d,\"ld\":%lld,\"dtype\":\"%s\",\"row_fft\":{\"n\":%d,\"L\":%d,\"bluestein\":%d,"
-                  "\"stages\":%d},\"col_fft\":{\"n\":%d,\"L\":%d,\"bluestein\":%d,\"stages\":%d},"
+                  "\"stages\":%d,\"split\":%d},\"col_fft\":{\"n\":%d,\"L\":%d,\"bluestein\":%d,\"stages\":%d,"
+                  "\"split\":%d},"
                   "\"row_pipe_grid\":%d,\"row_threads\":%d,\"row_smem\":%zu,\"cols_per_cta\":%d,"
                   "\"col_grid\":%d,\"col_half_panels\":%d,\"col_threads\":%d,\"col_smem\":%zu,\"ew_grid\":%d,"
                   "\"ew_threads\":%d}",
                   I.g.n, I.g.m, I.g.ld, h->dtype == PU_F32 ? "f32" : "f64", I.prow.dev.n, I.prow.dev.L,
-                  I.prow.dev.bluestein, I.prow.dev.nst, I.pcol.dev.n, I.pcol.dev.L, I.pcol.dev.bluestein,
-                  I.pcol.dev.nst, I.pipe_grid, I.pipe_threads, I.pipe_smem, I.cols_per_cta, I.col_grid(), I.col_nhalf, I.col_threads,
+                  I.prow.dev.bluestein, I.prow.dev.nst, (int)I.row_split, I.pcol.dev.n, I.pcol.dev.L,
+                  I.pcol.dev.bluestein, I.pcol.dev.nst, (int)I.col_split, I.pipe_grid, I.pipe_threads, I.pipe_smem, I.cols_per_cta, I.col_grid(), I.col_nhalf, I.col_threads,
                   I.col_smem, I.ew_grid, I.ew_threads);
   };
   if (h->dtype == PU_F32) fmt(*h->f); else fmt(*h->d);

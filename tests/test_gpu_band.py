@@ -86,3 +86,14 @@ def test_band_layout_errors():
         pu.band.BandLayout(3, 8, 4)
     with pytest.raises(ValueError):
         pu.band.BandLayout(64, 8, 4)  # 8 columns cannot give 4 blocks of >= 8
+
+
+@pytest.mark.parametrize("peer", [False, True])
+def test_bands_cluster_split_rows_fp64(peer):
+    """fp64 rows of 16384 (cluster-split row transforms, packed / pushed
+    spectrum) in 2 bands against the single-grid solve."""
+    x = _scene(10, 16384, noise=0.6, seed=11)
+    single = pu.unwrap(x, dtype="fp64", params=pu.IrlsParams(max_outer_iters=6))
+    res = pu.unwrap_rows(x, dtype="fp64", bands=2, peer=peer, params=pu.IrlsParams(max_outer_iters=6))
+    assert [r.cg_iters for r in res.trace.records] == [r.cg_iters for r in single.trace.records]
+    assert rel(res.u, single.u) <= 1e-9

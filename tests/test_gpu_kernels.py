@@ -106,9 +106,32 @@ def test_sylvester_long_rows(rng, shape, dtypes):
         assert rel(got, want) <= (1e-11 if dt == "fp64" else 5e-5), dt
 
 
-def test_fp64_row_limit():
-    with pytest.raises(NotImplementedError):
-        pu.sylvester_solve(np.zeros((2, 16384)), 1e-2, dtype="fp64")
+@pytest.mark.parametrize("shape,dtypes", [((2, 16384), ("fp64",)), ((7, 16384), ("fp64",)),
+                                          ((16384, 4), ("fp64",)), ((16384, 7), ("fp64",)),
+                                          ((16384, 16384 // 64), ("fp64",)),
+                                          ((3, 32768), ("fp32",)), ((32768, 5), ("fp32",))])
+def test_sylvester_cluster_split(rng, shape, dtypes):
+    """Lengths whose packed sequence exceeds one CTA's shared memory (fp64
+    16384, fp32 32768): a 2-CTA cluster per sequence exchanging halves
+    through distributed shared memory (pu_split.cuh).  Odd counts exercise
+    the lone last row / column of a pair."""
+    n, m = shape
+    r = rng.standard_normal((n, m))
+    want = port.DctPoisson(n, m)(r, 1e-2)
+    for dt in dtypes:
+        got = pu.sylvester_solve(r, 1e-2, dtype=dt)
+        assert rel(got, want) <= (1e-11 if dt == "fp64" else 5e-5), dt
+
+
+def test_fp64_long_axis_unwrap_matches_oracle():
+    """End-to-end fp64 unwrap on a grid with a 16384-long axis (cluster-split
+    row transforms) against the oracle with the exact DCT preconditioner."""
+    x = pu.add_phase_noise(pu.wrap_scene(pu.generate_scene(pu.SceneSpec("gaussian-bumps", 12, 16384, 30.0, 40.0,
+                                                                       5))), 0.5, 55)
+    ref_state, ref_recs, _ = port.unwrap(x, poisson="dct")
+    res = pu.unwrap(x, dtype="fp64")
+    assert [r.cg_iters for r in res.trace.records] == [r.cg_iters for r in ref_recs]
+    assert rel(res.u, ref_state.u) <= 1e-8
 
 
 def test_apply_preconditioner(rng):
