@@ -336,11 +336,11 @@ class BandUnwrap:
     def __init__(self, bands, comm, graphs=None):
         import os
         self.bands, self.comm = bands, comm
-        # one CUDA graph per (budget, buffer parity) replays a whole outer
-        # iteration -- kernels and loopback copies; NCCL collectives only on
-        # request (PU_BAND_GRAPHS=1) until graph capture has run on a multi-GPU box
+        # captured CUDA graphs replay the outer iteration -- kernels, loopback
+        # copies and NCCL collectives alike (PU_BAND_GRAPHS=0: eager launches)
         if graphs is None:
-            graphs = isinstance(comm, LoopbackComm) or os.environ.get("PU_BAND_GRAPHS") == "1"
+            capturable = isinstance(comm, LoopbackComm) or comm.dist.get_backend(comm.group) == "nccl"
+            graphs = capturable and os.environ.get("PU_BAND_GRAPHS", "1") != "0"
         self.graphs = bool(graphs)
         self._graphs = {}
         self.replayed_kernels = 0  # library kernels run by graph replays (the capture counted the first)
@@ -394,16 +394,41 @@ class BandUnwrap:
         self.comm.halo(self.bands, [(lambda b: b.D, 0, "down")])
 
     # ---- one outer iteration ------------------------------------------------------
+    GRAPH_CHUNK = 64  # PCG iterations per captured graph
+
     def step(self, k, m_cg, params: IrlsParams, lip, poll=16):
-        """irls.py:191-215 for iteration k (graph replay when enabled)."""
-        if not self.graphs or m_cg > 64:
+        """irls.py:191-215 for iteration k.
+
+        With graphs (the default): the start-up, z0 and the first 64 PCG
+        iterations replay as one captured CUDA graph (kernels and collectives
+        alike), every further 64 iterations as another, and the H pair +
+        acceptance as a third; the host checks the device exit flag once per
+        64-iteration chunk and only when the budget is longer than that."""
+        if not self.graphs:
             return self._step(k, m_cg, params, lip, poll)
-        torch = _torch()
         for b in self.bands:
-            b.ensure_norms(max(m_cg, 64))  # stable pointer across budgets
-        key = (m_cg, k & 1, self.bands[0].cur, float(lip), float(params.cg_rel_tol),
-               tuple(b.norms.data_ptr() for b in self.bands),
-               tuple(b.W.data_ptr() if b.use_w else 0 for b in self.bands))
+            b.ensure_norms(max(m_cg, self.GRAPH_CHUNK))  # stable pointer across budgets
+        base = (k & 1, self.bands[0].cur, float(lip), float(params.cg_rel_tol),
+                tuple(b.norms.data_ptr() for b in self.bands),
+                tuple(b.W.data_ptr() if b.use_w else 0 for b in self.bands))
+        first = min(m_cg, self.GRAPH_CHUNK)
+
+        def head():
+            self._head(k, m_cg, params, lip)
+            self._iters(0, first)
+
+        self._replay(("head", m_cg, first) + base, head)
+        it = first
+        while it < m_cg:
+            if self._done():
+                break
+            nxt = min(m_cg, it + self.GRAPH_CHUNK)
+            self._replay(("iters", it, nxt) + base, lambda a=it, z=nxt: self._iters(a, z))
+            it = nxt
+        self._replay(("tail",) + base, lambda: self._tail(k), flips=True)
+
+    def _replay(self, key, fn, flips=False):
+        torch = _torch()
         entry = self._graphs.get(key)
         if entry is None:
             cur = [b.cur for b in self.bands]
@@ -411,23 +436,37 @@ class BandUnwrap:
             n0 = lib.pu_launch_count()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=torch.cuda.Stream(device=self.bands[0].device)):
-                self._step(k, m_cg, params, lip, poll=None)
+                fn()
             for b, c in zip(self.bands, cur):  # capture does not run the work
                 b.cur = c
             entry = self._graphs[key] = (g, lib.pu_launch_count() - n0)
         else:
             self.replayed_kernels += entry[1]
         entry[0].replay()
-        for b in self.bands:
-            b.cur = 1 - b.cur
+        if flips:
+            for b in self.bands:
+                b.cur = 1 - b.cur
 
     def _step(self, k, m_cg, params: IrlsParams, lip, poll=16):
+        """Eager launches (no graphs); the host polls the exit flag every
+        `poll` PCG iterations so a converged budget stops enqueueing."""
+        self._head(k, m_cg, params, lip)
+        it = 0
+        while it < m_cg:
+            nxt = min(m_cg, it + (poll or m_cg))
+            if it > 0 and self._done():
+                break
+            self._iters(it, nxt)
+            it = nxt
+        self._tail(k)
+
+    def _head(self, k, m_cg, params: IrlsParams, lip):
+        """pcg.py:59-79: start-up (+ the candidate step), z0 = M r0, p0 = z0."""
         P = BandState.p
         tol = float(params.cg_rel_tol)
         for b in self.bands:
             b.ensure_norms(m_cg)
         cur = lambda b: b.S[b.cur]  # noqa: E731
-        nxt = lambda b: b.S[1 - b.cur]  # noqa: E731
         for b in self.bands:
             cv, ch = self._c(b)
             w = b.Wt[k & 1]
@@ -435,7 +474,6 @@ class BandUnwrap:
                    _ptr(b.norms), int(m_cg), tol, P(b.G, 0), P(b.G, 1), cv, ch, P(w, 0), P(w, 1), float(lip),
                    P(b.C), b.stream())
         self._reduce(nat.SITE_START, nat.SITE_START, _mask(nat.SITE_START), 1, -1, rel_tol=tol, max_iters=m_cg)
-        # z0 = M r0, rho0; p0 = z0 (pcg.py:77-79)
         for b in self.bands:
             b.call("pu_pcg_residual_rows", None, P(b.D, 0), P(b.D, 1), P(cur(b)), P(b.R), _ptr(b.ctrl),
                    _ptr(b.norms), b.send(), -1, 0, b.stream())
@@ -443,9 +481,13 @@ class BandUnwrap:
         for b in self.bands:
             b.call("pu_pcg_rows_inv", b.send(), P(b.P[0]), P(b.P[1]), 1, _ptr(b.ctrl), -1, b.stream())
         self._dir_halo(0)
-        for it in range(m_cg):
-            if poll and it > 0 and it % poll == 0 and self._done():
-                break
+
+    def _iters(self, it0, it1):
+        """pcg.py:81-108 for iterations [it0, it1) (kernels return at once
+        after the device-side exit)."""
+        P = BandState.p
+        cur = lambda b: b.S[b.cur]  # noqa: E731
+        for it in range(it0, it1):
             for b in self.bands:
                 pn, po = b.P[it & 1], b.P[(it + 1) & 1]
                 b.call("pu_pcg_direction", P(b.R), P(po), P(pn), P(b.D, 0), P(b.D, 1), _ptr(b.ctrl), it,
@@ -465,7 +507,13 @@ class BandUnwrap:
                 b.call("pu_pcg_rows_inv", b.send(), P(b.P[(it + 1) & 1]), P(b.P[it & 1]), 0,
                        _ptr(b.ctrl), it, b.stream())
             self._dir_halo((it + 1) & 1)
-        # H pair (irls.py:202-205) on the proposal (= state, solved in place) and the candidate
+
+    def _tail(self, k):
+        """H pair (irls.py:202-205) on the proposal (= state, solved in place)
+        and the candidate, then the acceptance and the weights of k + 1."""
+        P = BandState.p
+        cur = lambda b: b.S[b.cur]  # noqa: E731
+        nxt = lambda b: b.S[1 - b.cur]  # noqa: E731
         self.comm.halo(self.bands, [(cur, 0, "up"), (lambda b: b.C, 0, "up")])
         for b in self.bands:
             cv, ch = self._c(b)
