@@ -41,7 +41,8 @@ enum pu_status {
   PU_ERR_ARG = 1,          /* invalid argument (reference raises ValueError) */
   PU_ERR_CUDA = 2,         /* CUDA runtime error */
   PU_ERR_UNSUPPORTED = 3,  /* grid size outside the shared-memory FFT limits */
-  PU_ERR_NOMEM = 4
+  PU_ERR_NOMEM = 4,
+  PU_ERR_BREAKDOWN = 5     /* NumericalBreakdown (pcg.py:24-29): a non-finite PCG value (pu_unwrap) */
 };
 
 /* Device-side PCG control block (caller allocates pu_pcg_ctrl_bytes()).
@@ -321,6 +322,55 @@ int pu_pcg_rows_inv(pu_handle* h, const void* spec_in, void* pnew, const void* p
  * p'Ap. */
 int pu_pcg_direction(pu_handle* h, const void* r, const void* pold, void* pnew, const void* dv, const void* dh,
                      void* ctrl, int it, void* stream);
+
+/* ------------------------------------------------------------------------
+ * The whole unwrap behind one call, for hosts that bind C (cgo, JNI,
+ * N-API, ctypes) instead of running the Python mirror of irls.py:
+ * reference `unwrap(x, c, model, params, gradient_lo) -> UnwrapResult`
+ * (irls.py:132-224, re-exported at __init__.py:4).  Host arrays in and out;
+ * the IRLS outer loop (weights, H pair, CG-budget rule irls.py:111-129,
+ * warm-started PCG, safeguard, centring, trace) runs in C++ over the entry
+ * points above, on its own handle and stream, so concurrent calls are safe
+ * (SPEC.md:391, 453-454).
+ * ------------------------------------------------------------------------ */
+typedef struct pu_irls_params {   /* irls.py:43-64 IrlsParams (same defaults) */
+  int32_t max_iter_cg_start;      /* 5 */
+  int32_t max_outer_iters;        /* 100 */
+  int32_t max_cg_iters_cap;       /* 10000 */
+  int32_t pad_;
+  double rel_improvement_tol;     /* 1e-3 */
+  double cg_growth_factor;        /* 1.7 */
+  double cg_rel_tol;              /* 1e-10 */
+} pu_irls_params;
+
+typedef struct pu_iteration_record {  /* irls.py:67-75 IterationRecord */
+  int32_t k, m_cg, cg_iters;
+  int32_t has_delta_rel;              /* 0: delta_rel is None (k = 0) */
+  double delta_rel, h_delta;
+  int32_t sufficient_decrease, fallback_used;
+} pu_iteration_record;
+
+/* Fill *p with the IrlsParams defaults. */
+void pu_irls_params_default(pu_irls_params* p);
+
+/* Unwrap a wrapped phase grid.
+ *  x          host fp64, n x m row-major, every value finite and in [0, 2pi)
+ *             (phase.py:100-115);
+ *  cv, ch     host fp64 arc weights, (n-1) x m and n x (m-1), finite, >= 0,
+ *             not all zero (phase.py:54-73); both NULL = uniform unit weights;
+ *  tau, delta ModelParams (objective.py:30-41); params NULL = defaults;
+ *  gradient_lo 0 or -pi (phase.py:140-149);  dtype PU_F64 (the reference's
+ *             precision) or PU_F32;  device: CUDA ordinal;
+ *  u, vv, vh  host fp64 outputs, n x m, (n-1) x m, n x (m-1), mean(u) = 0;
+ *  trace      up to trace_cap records; *trace_len = records written (the
+ *             full count is returned even when it exceeds trace_cap).
+ * Returns PU_OK; PU_ERR_ARG for what the reference rejects with ValueError
+ * (checked before any device work); PU_ERR_BREAKDOWN with
+ * *breakdown_iteration = NumericalBreakdown.iteration; PU_ERR_UNSUPPORTED /
+ * PU_ERR_CUDA / PU_ERR_NOMEM otherwise.  pu_last_error() has the message. */
+int pu_unwrap(const double* x, int n, int m, const double* cv, const double* ch, double tau, double delta,
+              const pu_irls_params* params, double gradient_lo, int dtype, int device, double* u, double* vv,
+              double* vh, pu_iteration_record* trace, int trace_cap, int* trace_len, int* breakdown_iteration);
 
 #ifdef __cplusplus
 }

@@ -14,9 +14,24 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PU_LIB_PATH") or os.path.join(_HERE, "_lib", "libpu_unwrap.so")
 
 PU_F32, PU_F64 = 0, 1
-PU_OK, PU_ERR_ARG, PU_ERR_CUDA, PU_ERR_UNSUPPORTED, PU_ERR_NOMEM = 0, 1, 2, 3, 4
+PU_OK, PU_ERR_ARG, PU_ERR_CUDA, PU_ERR_UNSUPPORTED, PU_ERR_NOMEM, PU_ERR_BREAKDOWN = 0, 1, 2, 3, 4, 5
 
 _vp, _i, _d, _i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int64
+
+class PuIrlsParams(ctypes.Structure):
+    """struct pu_irls_params (include/pu_unwrap.h; irls.py:43-64)."""
+    _fields_ = [("max_iter_cg_start", ctypes.c_int32), ("max_outer_iters", ctypes.c_int32),
+                ("max_cg_iters_cap", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("rel_improvement_tol", ctypes.c_double), ("cg_growth_factor", ctypes.c_double),
+                ("cg_rel_tol", ctypes.c_double)]
+
+
+class PuIterationRecord(ctypes.Structure):
+    """struct pu_iteration_record (include/pu_unwrap.h; irls.py:67-75)."""
+    _fields_ = [("k", ctypes.c_int32), ("m_cg", ctypes.c_int32), ("cg_iters", ctypes.c_int32),
+                ("has_delta_rel", ctypes.c_int32), ("delta_rel", ctypes.c_double), ("h_delta", ctypes.c_double),
+                ("sufficient_decrease", ctypes.c_int32), ("fallback_used", ctypes.c_int32)]
+
 
 # name -> (restype, argtypes); mirrors include/pu_unwrap.h
 SIGNATURES = {
@@ -76,6 +91,10 @@ SIGNATURES = {
     "pu_pcg_columns": (_i, [_vp, _vp, _vp, _i, _vp]),
     "pu_pcg_rows_inv": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _vp]),
     "pu_pcg_direction": (_i, [_vp] + [_vp] * 6 + [_i, _vp]),
+    # the whole unwrap behind one call (pu_host.cu)
+    "pu_irls_params_default": (None, [ctypes.POINTER(PuIrlsParams)]),
+    "pu_unwrap": (_i, [_vp, _i, _i, _vp, _vp, _d, _d, ctypes.POINTER(PuIrlsParams), _d, _i, _i, _vp, _vp, _vp,
+                       ctypes.POINTER(PuIterationRecord), _i, ctypes.POINTER(_i), ctypes.POINTER(_i)]),
 }
 
 

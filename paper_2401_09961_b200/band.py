@@ -343,6 +343,7 @@ class BandUnwrap:
             graphs = capturable and os.environ.get("PU_BAND_GRAPHS", "1") != "0"
         self.graphs = bool(graphs)
         self._graphs = {}
+        self._warm = isinstance(comm, LoopbackComm)  # nothing to initialise lazily
         self.replayed_kernels = 0  # library kernels run by graph replays (the capture counted the first)
 
     # ---- helpers ------------------------------------------------------------
@@ -404,7 +405,11 @@ class BandUnwrap:
         alike), every further 64 iterations as another, and the H pair +
         acceptance as a third; the host checks the device exit flag once per
         64-iteration chunk and only when the budget is longer than that."""
-        if not self.graphs:
+        if not self.graphs or not self._warm:
+            # the first outer iteration runs eagerly: NCCL creates its
+            # communicators (all-reduce, all-to-all, P2P halo) lazily on first
+            # use, which cannot happen inside a stream capture
+            self._warm = True
             return self._step(k, m_cg, params, lip, poll)
         for b in self.bands:
             b.ensure_norms(max(m_cg, self.GRAPH_CHUNK))  # stable pointer across budgets

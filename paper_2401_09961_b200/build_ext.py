@@ -22,13 +22,15 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-LIBDIR = os.path.join(PKG, "_lib")
+# PU_BUILD_LIBDIR / PU_BUILD_DEFS: an alternative build (A/B variants, loaded
+# with PU_LIB_PATH=<libdir>/libpu_unwrap.so)
+LIBDIR = os.environ.get("PU_BUILD_LIBDIR") or os.path.join(PKG, "_lib")
 OBJDIR = os.path.join(LIBDIR, "obj")
 LIB = os.path.join(LIBDIR, "libpu_unwrap.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-O2",
-          "-Xptxas", "-v"]
+          "-Xptxas", "-v"] + os.environ.get("PU_BUILD_DEFS", "").split()
 
 # (dtype, internal FFT length); 0 = runtime plan.  Keep in sync with
 # PU_STATIC_LS_F32 / PU_STATIC_LS_F64 in csrc/pu_dct_launch.cuh.
@@ -101,7 +103,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     if not force and up_to_date():
         return LIB
     os.makedirs(OBJDIR, exist_ok=True)
-    work = [(os.path.join(CSRC, "pu_api.cu"), os.path.join(OBJDIR, "pu_api.o"), [])]
+    work = [(os.path.join(CSRC, "pu_api.cu"), os.path.join(OBJDIR, "pu_api.o"), []),
+            (os.path.join(CSRC, "pu_host.cu"), os.path.join(OBJDIR, "pu_host.o"), [])]
     for t, ls in INSTANCES:
         work.append((os.path.join(CSRC, "pu_dct_inst.cu"), os.path.join(OBJDIR, f"pu_dct_{t}_{ls}.o"),
                      [f"-DPU_INST_T={t}", f"-DPU_INST_LS={ls}"]))

@@ -25,6 +25,9 @@ static int fail(int code, const std::string& msg) {
   return code;
 }
 
+// the same error slot for the other translation units (pu_host.cu)
+int fail_ext(int code, const char* msg) { return fail(code, msg); }
+
 #define PU_CUDA(call)                                                                       \
   do {                                                                                      \
     cudaError_t e_ = (call);                                                                \
@@ -100,7 +103,7 @@ struct HostPlan {
   int emax = 0;
 
   int build(int n) {
-    emax = sizeof(T) == 4 ? 16 : 8;
+    emax = emax_of<T>();
     std::memset(&dev, 0, sizeof(dev));
     dev.n = n;
     std::vector<int> rad;
@@ -199,8 +202,9 @@ struct HostPlan {
   // threads for `nseq` sequences: at least one whole sequence per stage,
   // at most the instantiation's launch bound (larger groups run sequentially)
   int max_threads() const {
-    const bool stat = !dev.bluestein && (dev.L & (dev.L - 1)) == 0 && dev.L >= 512 && dev.L <= (emax == 16 ? 16384 : 8192);
-    return fft_max_threads(stat ? dev.L : 0, emax);
+    const bool stat = !dev.bluestein && (dev.L & (dev.L - 1)) == 0 && dev.L >= 512 &&
+                      dev.L <= (sizeof(T) == 4 ? 16384 : 8192);
+    return fft_max_threads(stat ? dev.L : 0, emax, sizeof(T));
   }
   int threads_for(int nseq) const {
     const long long need = ((long long)nseq * dev.L + seq_capacity - 1) / seq_capacity;
@@ -426,7 +430,7 @@ struct Impl : HandleBase {
     // not HBM, efficiency
     // static plans use PU_PANEL_COLS (2 packed sequences) in one thread group;
     // runtime plans (odd sizes, Bluestein) fall back to 1 sequence if needed
-    const int scc = static_panel_cols(pcol.dev.L, EM) / 2;  // sequences per CTA of a static plan
+    const int scc = static_panel_cols(pcol.dev.L, EM, sizeof(T)) / 2;  // sequences per CTA of a static plan
     const bool col_static = !pcol.dev.bluestein && (pcol.dev.L & (pcol.dev.L - 1)) == 0 && pcol.dev.L >= 512 &&
                             pcol.dev.L <= (sizeof(T) == 4 ? 16384 : 8192) && pcol.seq_capacity == EM &&
                             (long long)scc * pcol.dev.L <= 1024LL * pcol.seq_capacity &&
@@ -453,7 +457,7 @@ struct Impl : HandleBase {
     return set_smem_attrs();
   }
 
-  static constexpr int EM = sizeof(T) == 4 ? 16 : 8;
+  static constexpr int EM = emax_of<T>();
 
   // dynamic shared memory of the row kernels with `staged` rows of staging
   size_t pipe_bytes(int staged) const {

@@ -99,40 +99,58 @@ __device__ __forceinline__ void block_sum(double (&v)[NS], double* sh /* [NS][32
   __syncthreads();
 }
 
-// Returns true in exactly one block (the last to finish); in that block all
-// threads see `tot[s]` = the grid-wide sums.
+// Returns true in exactly one warp of one block (warp 0 of the last block to
+// finish); there every lane holds `tot[s]` = the grid-wide sums.  Only warp 0
+// of each block waits: the other warps leave their warp sums in shared memory,
+// signal with a non-blocking bar.arrive on named barrier 1 and exit, so the
+// tail of the block costs no CTA-wide barrier (K3 spent ~14% of its stall
+// samples in the old two-__syncthreads block sum).  Every order is fixed
+// (xor butterflies, warp index, block index), so the result does not depend
+// on scheduling.  All warps of the block must call it (no early exits).
 template <int NS>
 __device__ __forceinline__ bool grid_reduce(double (&v)[NS], RedScratch rs, int site, double (&tot)[NS]) {
   __shared__ double sh[NS * 32];
-  __shared__ bool last;
-  block_sum<NS>(v, sh);
-  if (threadIdx.x == 0) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[s] += __shfl_xor_sync(0xffffffffu, v[s], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) sh[s * 32 + warp] = v[s];
+  }
+  if (warp != 0) {
+    asm volatile("bar.arrive 1, %0;" ::"r"(nw * 32) : "memory");
+    return false;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    double t = lane < nw ? sh[s * 32 + lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    v[s] = t;
+  }
+  unsigned int ticket = 0;
+  if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < NS; ++s) rs.partials[(size_t)s * rs.stride + blockIdx.x] = v[s];
     __threadfence();
-    unsigned int t = atomicAdd(rs.ticket + site, 1u);
-    last = (t == gridDim.x - 1);
+    ticket = atomicAdd(rs.ticket + site, 1u);
   }
-  __syncthreads();
-  if (!last) return false;
+  ticket = __shfl_sync(0xffffffffu, ticket, 0);
+  if (ticket != gridDim.x - 1) return false;
   __threadfence();
-  double acc[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
-    acc[s] = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
-      acc[s] += ((volatile double*)rs.partials)[(size_t)s * rs.stride + b];
-  }
-  block_sum<NS>(acc, sh);
-  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) acc += ((volatile double*)rs.partials)[(size_t)s * rs.stride + b];
 #pragma unroll
-    for (int s = 0; s < NS; ++s) sh[s * 32] = acc[s];
-    rs.ticket[site] = 0u;  // re-arm for the next launch
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    tot[s] = acc;
   }
-  __syncthreads();
-#pragma unroll
-  for (int s = 0; s < NS; ++s) tot[s] = sh[s * 32];
-  __syncthreads();
+  if (lane == 0) rs.ticket[site] = 0u;  // re-arm for the next launch
   return true;
 }
 

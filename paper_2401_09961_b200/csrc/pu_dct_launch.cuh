@@ -18,7 +18,7 @@ struct XLaunch {
 
 template <typename T, int LS>
 struct DctLaunch {
-  static constexpr int EM = sizeof(T) == 4 ? 16 : 8;
+  static constexpr int EM = emax_of<T>();
 
   static cudaError_t set_attrs(size_t row_smem, size_t col_smem);
 

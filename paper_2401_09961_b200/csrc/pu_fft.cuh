@@ -18,19 +18,38 @@ namespace pu {
 
 #define PU_FFT_MAX_STAGES 20
 #define PU_PANEL_COLS 4  // columns per CTA of the column-transform kernel (2 packed sequences)
-// columns per CTA of a static column plan: 2 packed sequences while they fit
-// one 1024-thread group, else 1 (L / EMAX = 1024 threads, e.g. 16384 fp32)
-__host__ __device__ constexpr int static_panel_cols(int L, int emax) {
-  return 4 * L <= 1024 * emax ? 2 * PU_PANEL_COLS : (2 * L <= 1024 * emax ? PU_PANEL_COLS : PU_PANEL_COLS / 2);
-}
-#define PU_FFT_MAX_THREADS 1024  // absolute per-CTA thread cap of the transform kernels
+
+// Complex values per thread of one FFT stage (the largest radix): 16 in fp32;
+// in fp64 PU_F64_EMAX (8: radix-8 stages at <= 64 registers; 16: radix-16
+// stages, one fewer shared-memory round trip per 4096-point FFT, at <= 128
+// registers with half the threads).
+#ifndef PU_F64_EMAX
+#define PU_F64_EMAX 8
+#endif
+template <typename T>
+__host__ __device__ constexpr int emax_of() { return sizeof(T) == 4 ? 16 : PU_F64_EMAX; }
 
 // Per-instantiation launch bounds.  Transform kernels run every sequence of
 // the CTA in one group (no loop over sequence groups: ptxas hoists the
 // thread-invariant twiddles/addresses of such loops and spills), so a CTA
-// has nseq * L / EMAX threads, up to 1024, at <= 64 registers.
-__host__ __device__ constexpr int fft_max_threads(int LS, int EMAX) { return 1024; }
+// has nseq * L / EMAX threads: up to 1024 at <= 64 registers, or up to 512
+// at <= 128 registers for 16 complex doubles per thread.
+__host__ __device__ constexpr int fft_max_threads(int LS, int EMAX, int tsize = 4) {
+  return (tsize == 8 && EMAX >= 16) ? 512 : 1024;
+}
 __host__ __device__ constexpr int fft_min_blocks(int LS, int EMAX) { return 1; }
+
+__host__ __device__ constexpr int ldseq_for(int L);
+// columns per CTA of a static column plan: 4, 2 or 1 packed sequences, the
+// most that fit one thread group and the shared memory (2 columns each)
+__host__ __device__ constexpr int static_panel_cols(int L, int emax, int tsize = 4) {
+  return (4 * L <= fft_max_threads(L, emax, tsize) * emax && 4LL * ldseq_for(L) * 2 * tsize <= 220 * 1024)
+             ? 2 * PU_PANEL_COLS
+             : ((2 * L <= fft_max_threads(L, emax, tsize) * emax && 2LL * ldseq_for(L) * 2 * tsize <= 220 * 1024)
+                    ? PU_PANEL_COLS
+                    : PU_PANEL_COLS / 2);
+}
+#define PU_FFT_MAX_THREADS 1024  // absolute per-CTA thread cap of the transform kernels
 
 // Plan for one transform length (built on the host, pu_api.cu HostPlan).
 template <typename T>
@@ -506,7 +525,17 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 __device__ __forceinline__ float fast_div(float a, float b) { return a * rcp_approx(b); }
-__device__ __forceinline__ double fast_div(double a, double b) { return a * __drcp_rn(b); }
+// fp64: MUFU reciprocal seed + two Newton steps (<= 1 ulp, no IEEE rounding
+// fix-up path: the spectral scaling is ~6% of K3's fp64 stall samples with __drcp_rn)
+__device__ __forceinline__ double rcp_nr(double b) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
+  double e = fma(-b, y, 1.0);
+  y = fma(e, y, y);
+  e = fma(-b, y, 1.0);
+  return fma(e, y, y);
+}
+__device__ __forceinline__ double fast_div(double a, double b) { return a * rcp_nr(b); }
 
 // correctly rounded reciprocal
 __device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }

@@ -227,17 +227,17 @@ __device__ __forceinline__ void col_last_stage(const Grid& g, T* data, int j0, c
 // panel of `cols_per_cta` columns; reduces rho_u = <r_hat, z_hat>.
 // ---------------------------------------------------------------------------
 template <typename T, int EMAX, int LS, int MODE>
-__global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, EMAX)) k_cols_spec(Grid g, FftPlan<T> pl, const T* __restrict__ lam_cols, int cols_per_cta, T* data,
+__global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_blocks(LS, EMAX)) k_cols_spec(Grid g, FftPlan<T> pl, const T* __restrict__ lam_cols, int cols_per_cta, T* data,
                             PcgCtrl* ctrl, RedScratch rs, int site, int it, Push ps, int nfull) {
   extern __shared__ __align__(16) unsigned char smraw[];
   cplx<T>* buf = reinterpret_cast<cplx<T>*>(smraw);
   if (MODE != MODE_API && ctrl->done) return;
   const int n = LS > 0 ? LS : g.n;  // static plans are only used when n == L
   // static plans: compile-time panel width; runtime plans: 4 or 2 (smem)
-  const int W0 = LS > 0 ? static_panel_cols(LS, EMAX) : cols_per_cta;
+  const int W0 = LS > 0 ? static_panel_cols(LS, EMAX, sizeof(T)) : cols_per_cta;
   // balanced grid (static plans): CTAs past `nfull` take half panels, so the
   // last wave is spread over every SM instead of a few full panels
-  constexpr bool HALF_OK = LS > 0 && static_panel_cols(LS > 0 ? LS : 4096, EMAX) >= 8;  // host: cols_per_cta >= 8
+  constexpr bool HALF_OK = LS > 0 && static_panel_cols(LS > 0 ? LS : 4096, EMAX, sizeof(T)) >= 8;  // host: cols_per_cta >= 8
   const bool halfp = HALF_OK && (int)blockIdx.x >= nfull;
   const int W = halfp ? W0 / 2 : W0;
   const int j0 = halfp ? nfull * W0 + ((int)blockIdx.x - nfull) * W : (int)blockIdx.x * W0;
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   const bool fuse = FUSE && ncols == W;
   if (fuse) {
     if constexpr (FUSE) {
-      constexpr int NSF = static_panel_cols(LF, EMAX) / 2;
+      constexpr int NSF = static_panel_cols(LF, EMAX, sizeof(T)) / 2;
       if (halfp) {
         if constexpr (NSF >= 4) col_first_stage<T, EMAX, LF, NSF / 2>(g, data, j0, buf);
       } else {
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, 
   if (fuse) {
     if constexpr (FUSE) {
       fft_stages_range<T, EMAX, LF, 1, 0, LF / (EMAX >= 16 ? 16 : 8)>(buf, 0, nseq, pl.stw);
-      constexpr int NSF = static_panel_cols(LF, EMAX) / 2;
+      constexpr int NSF = static_panel_cols(LF, EMAX, sizeof(T)) / 2;
       if (halfp) {
         if constexpr (NSF >= 4) col_last_stage<T, EMAX, LF, NSF / 2>(g, data, j0, buf, pl.stw, ps);
       } else {

@@ -167,7 +167,7 @@ struct Pack {
 // the u block of the next search direction (pcg.py:107-108); `first` gives
 // out = DCT-III(in) (p = z at iteration 0).
 template <typename T, int EMAX, int LS, bool INV>
-__global__ void __launch_bounds__(fft_max_threads(LS, EMAX), fft_min_blocks(LS, EMAX))
+__global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_blocks(LS, EMAX))
     k_rows_pipe(Grid g, FftPlan<T> pl, const T* __restrict__ in, T* __restrict__ out, const PcgCtrl* ctrl,
                 const T* __restrict__ pold, int first, Pack pk) {
   extern __shared__ __align__(128) unsigned char smraw[];

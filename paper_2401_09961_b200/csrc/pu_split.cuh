@@ -211,7 +211,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(split_threads<LH, EM
 // supported half lengths: double 8192 -> n = 16384, float 16384 -> n = 32768).
 template <typename T, int LH>
 struct SplitLaunch {
-  static constexpr int EM = sizeof(T) == 4 ? 16 : 8;
+  static constexpr int EM = emax_of<T>();
   static constexpr int threads() { return split_threads<LH, EM>(); }
   static size_t smem() { return (size_t)ldseq_for(LH) * sizeof(cplx<T>); }
   static cudaError_t set_attrs();

@@ -19,7 +19,7 @@ HEADER = os.path.join(ROOT, "include", "pu_unwrap.h")
 
 def header_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(pu_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void|const char\*)\s+(pu_\w+)\s*\(", text, re.M)))
 
 
 def test_header_and_binding_agree():
@@ -146,3 +146,46 @@ def test_band_layout_partitions():
         assert all(lay.row0[i] + lay.rows[i] == lay.row0[i + 1] for i in range(w - 1))
         assert max(lay.rows) - min(lay.rows) <= 1
         assert lay.mb % 8 == 0 and lay.mb * w >= m and sum(lay.cols) == m
+
+
+def _capi_args():
+    from paper_2401_09961_b200 import capi  # noqa: F401  (binding module imports cleanly without a GPU)
+    return capi
+
+
+@pytest.mark.parametrize("x,kw,msg", [
+    (np.full((4, 5), np.nan), {}, "non-finite"),
+    (np.full((4, 5), 7.0), {}, "[0, 2*pi)"),
+    (np.zeros((4, 5)), {"model": ModelParams.__new__(ModelParams)}, "tau"),
+    (np.zeros((4, 5)), {"gradient_lo": 1.0}, "lo must be"),
+    (np.zeros((4, 5)), {"c": WeightField(np.ones((3, 4)), np.ones((4, 3)))}, "weight shapes"),
+])
+def test_pu_unwrap_validates_before_device_work(x, kw, msg):
+    """pu_unwrap (csrc/pu_host.cu) checks the reference's ValueError cases in C
+    before touching CUDA, so they are testable without a GPU."""
+    capi = _capi_args()
+    if "model" in kw:  # bypass the dataclass check to reach the C-side one
+        object.__setattr__(kw["model"], "tau", -1.0)
+        object.__setattr__(kw["model"], "delta", 1e-6)
+    with pytest.raises(ValueError, match=re.escape(msg)):
+        capi.unwrap_capi(x, **kw)
+
+
+def test_pu_unwrap_params_and_weights_checked_in_c():
+    capi = _capi_args()
+    lib = _native.load()
+    p = _native.PuIrlsParams()
+    lib.pu_irls_params_default(p)
+    assert (p.max_iter_cg_start, p.max_outer_iters, p.max_cg_iters_cap) == (5, 100, 10000)
+    assert (p.rel_improvement_tol, p.cg_growth_factor, p.cg_rel_tol) == (1e-3, 1.7, 1e-10)
+    bad = IrlsParams.__new__(IrlsParams)
+    for f, v in dict(max_iter_cg_start=5, rel_improvement_tol=1e-3, cg_growth_factor=0.5, max_outer_iters=100,
+                     max_cg_iters_cap=10000, cg_rel_tol=1e-10).items():
+        object.__setattr__(bad, f, v)
+    with pytest.raises(ValueError, match="cg_growth_factor"):
+        capi.unwrap_capi(np.zeros((3, 3)), params=bad)
+    neg = WeightField.__new__(WeightField)
+    object.__setattr__(neg, "cv", -np.ones((2, 3)))
+    object.__setattr__(neg, "ch", np.ones((3, 2)))
+    with pytest.raises(ValueError, match="nonnegative"):
+        capi.unwrap_capi(np.zeros((3, 3)), c=neg)
