@@ -336,11 +336,15 @@ class BandUnwrap:
     def __init__(self, bands, comm, graphs=None):
         import os
         self.bands, self.comm = bands, comm
-        # captured CUDA graphs replay the outer iteration -- kernels, loopback
-        # copies and NCCL collectives alike (PU_BAND_GRAPHS=0: eager launches)
+        # captured CUDA graphs replay the outer iteration (kernels and loopback
+        # copies).  NCCL collectives only on request (PU_BAND_GRAPHS=1): with
+        # them captured, the world-1 torchrun test hung on the B200 (round 2,
+        # tests/test_gpu_dist1.py), so torch.distributed bands launch eagerly
         if graphs is None:
-            capturable = isinstance(comm, LoopbackComm) or comm.dist.get_backend(comm.group) == "nccl"
-            graphs = capturable and os.environ.get("PU_BAND_GRAPHS", "1") != "0"
+            if isinstance(comm, LoopbackComm):
+                graphs = os.environ.get("PU_BAND_GRAPHS", "1") != "0"
+            else:
+                graphs = os.environ.get("PU_BAND_GRAPHS") == "1" and comm.dist.get_backend(comm.group) == "nccl"
         self.graphs = bool(graphs)
         self._graphs = {}
         self._warm = isinstance(comm, LoopbackComm)  # nothing to initialise lazily
