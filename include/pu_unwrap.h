@@ -89,6 +89,14 @@ int pu_copy(pu_handle* h, const void* src, void* dst, int nplanes, void* stream)
 int pu_wrapped_gradients(pu_handle* h, const double* x, int64_t ldx, void* gv, void* gh, double lo,
                          void* stream);
 
+/* pu_wrapped_gradients + the input check of phase.py:100-115 from the same
+ * loads (whole grids): check[0] = number of non-finite x, check[1] = number
+ * of finite x outside [0, 2pi) (device fp64).  The caller raises the
+ * reference's ValueError when either is non-zero (the Python host reads them
+ * with the first scalar snapshot, so no extra synchronisation). */
+int pu_wrapped_gradients_checked(pu_handle* h, const double* x, int64_t ldx, void* gv, void* gh, double lo,
+                                 double* check, void* stream);
+
 /* irls.py:167 initial state x = (0, -gv, -gh). */
 int pu_init_state(pu_handle* h, const void* gv, const void* gh, void* x, void* stream);
 

@@ -49,6 +49,7 @@ SIGNATURES = {
     "pu_unpack_native": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
     "pu_fill": (_i, [_vp, _vp, _i, _d, _vp]),
     "pu_copy": (_i, [_vp, _vp, _vp, _i, _vp]),
+    "pu_wrapped_gradients_checked": (_i, [_vp, _vp, _i64, _vp, _vp, _d, _vp, _vp]),
     "pu_init_state": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "pu_wrapped_gradients": (_i, [_vp, _vp, _i64, _vp, _vp, _d, _vp]),
     "pu_build_rhs": (_i, [_vp, _vp, _vp, _vp, _vp]),

@@ -870,6 +870,19 @@ int pu_wrapped_gradients(pu_handle* h, const double* x, int64_t ldx, void* gv, v
   return PU_OK;
 }
 
+int pu_wrapped_gradients_checked(pu_handle* h, const double* x, int64_t ldx, void* gv, void* gh, double lo,
+                                 double* check, void* stream) {
+  if (!(lo == 0.0 || lo == -3.141592653589793)) return fail(PU_ERR_ARG, "lo must be 0 or -pi");
+  if (!check) return fail(PU_ERR_ARG, "check must not be NULL");
+  PU_DISPATCH(h, {
+    if (I.band) return fail(PU_ERR_ARG, "pu_wrapped_gradients_checked runs on whole grids");
+    k_grad_check<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, x, ldx, MP(gv), MP(gh), lo, I.rs, S_CHK,
+                                                               check);
+    PU_LAUNCH_CHECK();
+  });
+  return PU_OK;
+}
+
 int pu_init_state(pu_handle* h, const void* gv, const void* gh, void* x, void* stream) {
   PU_DISPATCH(h, {
     k_init_state<T><<<I.ew_grid, I.ew_threads, 0, ST(stream)>>>(I.g, CP(gv), CP(gh), MP(x));

@@ -11,8 +11,42 @@
 #include <stdint.h>
 
 #include "pu_unwrap.h"
+#ifdef PU_DEBUG_CHECKS
+#include <cstdio>
+#endif
 
 namespace pu {
+
+// ---------------------------------------------------------------------------
+// Debug build checks (-DPU_DEBUG_CHECKS, build_ext PU_BUILD_DEFS): device
+// asserts on shared-memory addresses (inside the CTA's allocation, read from
+// %total_smem_size) and on the global indices of the transform and reduction
+// kernels.  compute-sanitizer is closed on the GPU pool of this project, so
+// the GPU test suite runs once against this build instead.
+// Compiled out of the production library.
+// ---------------------------------------------------------------------------
+#ifdef PU_DEBUG_CHECKS
+#define PU_ASSERT(c)                                                                            \
+  do {                                                                                          \
+    if (!(c)) {                                                                                 \
+      printf("PU_ASSERT failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x, #c);                                                             \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+template <typename P>
+__device__ __forceinline__ P* sm_chk(P* p) {
+  unsigned tot;
+  asm("mov.u32 %0, %%total_smem_size;" : "=r"(tot));
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  PU_ASSERT(a + sizeof(P) <= tot);
+  return p;
+}
+#else
+#define PU_ASSERT(c) ((void)0)
+template <typename P>
+__device__ __forceinline__ P* sm_chk(P* p) { return p; }
+#endif
 
 struct Grid {
   int n;            // rows (N)
@@ -133,6 +167,7 @@ __device__ __forceinline__ bool grid_reduce(double (&v)[NS], RedScratch rs, int 
     v[s] = t;
   }
   unsigned int ticket = 0;
+  PU_ASSERT((int)blockIdx.x < rs.stride && site >= 0 && site < 32);
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < NS; ++s) rs.partials[(size_t)s * rs.stride + blockIdx.x] = v[s];

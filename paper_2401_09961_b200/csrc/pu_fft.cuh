@@ -235,7 +235,10 @@ __device__ __forceinline__ void fft_stage(cplx<T>* buf, int L, int seq0, int nse
       const int j = b - s * nb;
       const cplx<T>* sb = buf + (seq0 + s) * ldseq;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[q][r] = sb[spad(j + r * nb)];
+      for (int r = 0; r < R; ++r) {
+        PU_ASSERT(spad(j + r * nb) < ldseq);
+        v[q][r] = *sm_chk(&sb[spad(j + r * nb)]);
+      }
       if constexpr (FIRST) {
         obase[q] = (seq0 + s) * ldseq + j * R;
       } else {
@@ -256,7 +259,10 @@ __device__ __forceinline__ void fft_stage(cplx<T>* buf, int L, int seq0, int nse
       const int s0 = (obase[q] / ldseq) * ldseq;
       const int i0 = obase[q] - s0;
 #pragma unroll
-      for (int r = 0; r < R; ++r) buf[s0 + spad(i0 + r * (FIRST ? 1 : Ns))] = v[q][r];
+      for (int r = 0; r < R; ++r) {
+        PU_ASSERT(spad(i0 + r * (FIRST ? 1 : Ns)) < ldseq);
+        *sm_chk(&buf[s0 + spad(i0 + r * (FIRST ? 1 : Ns))]) = v[q][r];
+      }
     }
   }
   __syncthreads();
@@ -333,10 +339,16 @@ __device__ __forceinline__ void fft_stage_s(cplx<T>* buf, int seq0, int nseq, co
         // spad(j + r NB) = spad(j) + r (NB + NB/16): one base register, immediate offsets
         const cplx<T>* src = buf + base + spad(j);
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[q][r] = src[r * (NB + NB / 16)];
+        for (int r = 0; r < R; ++r) {
+          PU_ASSERT(spad(j) + r * (NB + NB / 16) < LD);
+          v[q][r] = *sm_chk(&src[r * (NB + NB / 16)]);
+        }
       } else {
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[q][r] = buf[base + spad(j + r * NB)];
+        for (int r = 0; r < R; ++r) {
+          PU_ASSERT(spad(j + r * NB) < LD);
+          v[q][r] = *sm_chk(&buf[base + spad(j + r * NB)]);
+        }
       }
       if constexpr (NS > 1) {
         // twiddles W_{NS R}^{r k}: one table load (w = W^k), powers by a
@@ -368,14 +380,23 @@ __device__ __forceinline__ void fft_stage_s(cplx<T>* buf, int seq0, int nseq, co
       if constexpr (NS % 16 == 0) {
         cplx<T>* dst = buf + base + spad(i0);
 #pragma unroll
-        for (int r = 0; r < R; ++r) dst[r * (NS + NS / 16)] = v[q][r];
+        for (int r = 0; r < R; ++r) {
+          PU_ASSERT(spad(i0) + r * (NS + NS / 16) < LD);
+          *sm_chk(&dst[r * (NS + NS / 16)]) = v[q][r];
+        }
       } else if constexpr (NS == 1 && R == 16) {
         cplx<T>* dst = buf + base + spad(i0);  // i0 = 16 j: spad(16 j + r) = 17 j + r
 #pragma unroll
-        for (int r = 0; r < R; ++r) dst[r] = v[q][r];
+        for (int r = 0; r < R; ++r) {
+          PU_ASSERT(spad(i0) + r < LD);
+          *sm_chk(&dst[r]) = v[q][r];
+        }
       } else {
 #pragma unroll
-        for (int r = 0; r < R; ++r) buf[base + spad(i0 + r * NS)] = v[q][r];
+        for (int r = 0; r < R; ++r) {
+          PU_ASSERT(spad(i0 + r * NS) < LD);
+          *sm_chk(&buf[base + spad(i0 + r * NS)]) = v[q][r];
+        }
       }
     }
   }

@@ -11,6 +11,8 @@
 namespace pu {
 
 enum Site { S_DOT = 0, S_WH, S_EVH, S_HPAIR, S_ACC, S_EVF, S_START, S_K1, S_K2, S_K3, S_UPD, S_K2B, S_MET, S_NSITES };
+// ticket of the input check (whole grids only: no band totals row)
+enum { S_CHK = S_NSITES };
 enum { MODE_API = 0, MODE_INIT = 1, MODE_ITER = 2 };
 
 #define PU_TINY_CURVATURE 1e-300

@@ -104,6 +104,28 @@ __global__ void k_grad(Grid g, const double* __restrict__ x, long long ldx, T* g
   }
 }
 
+// k_grad + the input check of phase.py:100-115 from the same loads:
+// out[0] = number of non-finite x, out[1] = number of finite x outside
+// [0, 2 pi).  The host raises ValueError on the first scalar read.
+template <typename T>
+__global__ void k_grad_check(Grid g, const double* __restrict__ x, long long ldx, T* gv, T* gh, double lo,
+                             RedScratch rs, int site, double* out) {
+  double acc[2] = {0.0, 0.0};
+  PU_FOR_CELLS(g, i, j) {
+    const long long o = (long long)i * g.ld + j;
+    const double xij = x[(long long)i * ldx + j];
+    if (!isfinite(xij)) acc[0] += 1.0;
+    else if (xij < 0.0 || xij >= PU_TWO_PI) acc[1] += 1.0;
+    gv[o] = dn_ok(g, i) ? (T)wrap_lo(__dsub_rn(x[(long long)(i + 1) * ldx + j], xij), lo) : (T)0;
+    gh[o] = (j < g.m - 1) ? (T)wrap_lo(__dsub_rn(x[(long long)i * ldx + j + 1], xij), lo) : (T)0;
+  }
+  double tot[2];
+  if (grid_reduce<2>(acc, rs, site, tot) && threadIdx.x == 0) {
+    out[0] = tot[0];
+    out[1] = tot[1];
+  }
+}
+
 // irls.py:167 — initial state (u, vv, vh) = (0, -gv, -gh)
 template <typename T>
 __global__ void k_init_state(Grid g, const T* __restrict__ gv, const T* __restrict__ gh, T* x) {

@@ -49,6 +49,7 @@ __device__ __forceinline__ void panel_load(const Grid& g, const FftPlan<T>& pl, 
         const int e = base + u * blockDim.x + threadIdx.x;
         if (e < items) {
           const int i = e / vpr, v = e - i * vpr;
+          PU_ASSERT(i < g.n && j0 + (v + 1) * VN <= g.ld);
           r[u] = __ldg(reinterpret_cast<const V*>(data + (long long)i * g.ld + j0 + v * VN));
         }
       }
@@ -58,11 +59,12 @@ __device__ __forceinline__ void panel_load(const Grid& g, const FftPlan<T>& pl, 
         if (e < items) {
           const int i = e / vpr, v = e - i * vpr;
           const int p = spad(mperm(i, n));
+          PU_ASSERT(p < pl.ldseq);
           if constexpr (VN == 4) {
-            buf[(2 * v) * pl.ldseq + p] = mk<T>(r[u].x, r[u].y);
-            buf[(2 * v + 1) * pl.ldseq + p] = mk<T>(r[u].z, r[u].w);
+            *sm_chk(&buf[(2 * v) * pl.ldseq + p]) = mk<T>(r[u].x, r[u].y);
+            *sm_chk(&buf[(2 * v + 1) * pl.ldseq + p]) = mk<T>(r[u].z, r[u].w);
           } else {
-            buf[v * pl.ldseq + p] = mk<T>(r[u].x, r[u].y);
+            *sm_chk(&buf[v * pl.ldseq + p]) = mk<T>(r[u].x, r[u].y);
           }
         }
       }
@@ -70,8 +72,9 @@ __device__ __forceinline__ void panel_load(const Grid& g, const FftPlan<T>& pl, 
   } else {
     for (int e = threadIdx.x; e < n * 2 * nseq; e += blockDim.x) {
       const int i = e / (2 * nseq), c = e - i * (2 * nseq);
+      PU_ASSERT(i < g.n && (c >= ncols || j0 + c < g.ld));
       const T val = (c < ncols) ? data[(long long)i * g.ld + j0 + c] : (T)0;
-      T* slot = reinterpret_cast<T*>(buf + (c >> 1) * pl.ldseq + spad(mperm(i, n)));
+      T* slot = reinterpret_cast<T*>(sm_chk(buf + (c >> 1) * pl.ldseq + spad(mperm(i, n))));
       slot[c & 1] = val;
     }
   }
@@ -121,6 +124,7 @@ __device__ __forceinline__ void panel_store(const Grid& g, const FftPlan<T>& pl,
         const cplx<T> a = buf[v * pl.ldseq + p];
         o.x = a.x; o.y = -a.y;
       }
+      PU_ASSERT(i < g.n && j0 + (v + 1) * VN <= g.ld && p < pl.ldseq);
       T* row = ps.backs ? push_row<T>(ps, i) : data + (long long)i * g.ld;
       *reinterpret_cast<V*>(row + j0 + v * VN) = o;
     }
@@ -168,6 +172,8 @@ __device__ __forceinline__ void col_first_stage(const Grid& g, const T* __restri
     if (b >= NSEQ * NB) break;  // CTAs may be rounded up
     const T* pa = data + (long long)(2 * j) * ld + j0 + 2 * s;
     const T* pb = data + (long long)(2 * L - 1 - 2 * j) * ld + j0 + 2 * s;
+    PU_ASSERT(2 * j + 2 * (R / 2 - 1) * NB < g.n && 2 * L - 1 - 2 * j - 2 * (R - 1) * NB >= 0 &&
+              2 * L - 1 - 2 * j < g.n && j0 + 2 * s + 2 <= ld);
 #pragma unroll
     for (int r = 0; r < R / 2; ++r) v[q][r] = __ldg(reinterpret_cast<const cplx<T>*>(pa + r * step));
 #pragma unroll
@@ -180,7 +186,10 @@ __device__ __forceinline__ void col_first_stage(const Grid& g, const T* __restri
     Dft<T, R>::run(v[q]);
     cplx<T>* dst = buf + s * LD + spad(j * R);  // spad(j R + r) = spad(j R) + r for R | 16
 #pragma unroll
-    for (int r = 0; r < R; ++r) dst[r] = v[q][r];
+    for (int r = 0; r < R; ++r) {
+      PU_ASSERT(spad(j * R) + r < LD);
+      *sm_chk(&dst[r]) = v[q][r];
+    }
   }
   __syncthreads();
 }
@@ -197,7 +206,10 @@ __device__ __forceinline__ void col_last_stage(const Grid& g, T* data, int j0, c
     const cplx<T>* src = buf + s * LD + spad(j);
     cplx<T> v[R], w[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = src[r * (NS + NS / 16)];
+    for (int r = 0; r < R; ++r) {
+      PU_ASSERT(spad(j) + r * (NS + NS / 16) < LD);
+      v[r] = *sm_chk(&src[r * (NS + NS / 16)]);
+    }
     w[1] = __ldg(stw + OFF + j);
 #pragma unroll
     for (int r = 2; r < R; ++r) w[r] = cmul<T>(w[r / 2], w[r - r / 2]);
@@ -212,6 +224,8 @@ __device__ __forceinline__ void col_last_stage(const Grid& g, T* data, int j0, c
       }
     } else {
       const long long ld = g.ld, step = 2LL * NS * ld;
+      PU_ASSERT(2 * j + 2 * (R / 2 - 1) * NS < g.n && 2 * L - 1 - 2 * j < g.n &&
+                2 * L - 1 - 2 * j - 2 * (R - 1) * NS >= 0 && j0 + 2 * s + 2 <= ld);
       T* pa = data + (long long)(2 * j) * ld + j0 + 2 * s;
       T* pb = data + (long long)(2 * L - 1 - 2 * j) * ld + j0 + 2 * s;
 #pragma unroll
@@ -268,7 +282,8 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_
     const int s = e / half, k = e - s * half;
     const int nk = k == 0 ? 0 : n - k;
     cplx<T>* sb = buf + s * pl.ldseq;
-    const PairOut<T> q = dct2_post<T>(sb[spad(k)], sb[spad(nk)], k, nk, pl);
+    PU_ASSERT(spad(k) < pl.ldseq && spad(nk) < pl.ldseq);
+    const PairOut<T> q = dct2_post<T>(*sm_chk(&sb[spad(k)]), *sm_chk(&sb[spad(nk)]), k, nk, pl);
     const int ja = j0 + 2 * s, jb = ja + 1;
     const bool hasb = jb < g.m;
     const T lk = __ldg(pl.lam + k), lnk = __ldg(pl.lam + nk);

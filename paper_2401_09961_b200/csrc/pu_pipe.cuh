@@ -166,6 +166,15 @@ struct Pack {
 // INV with `pold` != nullptr (PCG K4): out = beta * pold + DCT-III(in), i.e.
 // the u block of the next search direction (pcg.py:107-108); `first` gives
 // out = DCT-III(in) (p = z at iteration 0).
+// debug check: staging rows + FFT buffer inside the CTA's shared memory
+template <typename T>
+__device__ __forceinline__ bool row_pair_smem_ok(unsigned char* smraw, bool one, bool ffuse, unsigned RB, int ldseq) {
+  const size_t need = 128 + (ffuse ? 0 : (one ? 1 : 2) * (size_t)RB) + (size_t)ldseq * sizeof(cplx<T>);
+  const size_t need_f = 128 + (size_t)(one ? 1 : 2) * RB;
+  sm_chk(smraw + (need > need_f ? need : need_f) - 1);
+  return true;
+}
+
 template <typename T, int EMAX, int LS, bool INV>
 __global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_blocks(LS, EMAX))
     k_rows_pipe(Grid g, FftPlan<T> pl, const T* __restrict__ in, T* __restrict__ out, const PcgCtrl* ctrl,
@@ -189,6 +198,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_
     fence_mbar_init();
   }
   __syncthreads();
+  PU_ASSERT(row_pair_smem_ok<T>(smraw, one, ffuse, RB, pl.ldseq));
   auto fetch = [&](T* dst, int row) {  // one thread; RB bytes
     if (pin) {
       for (int q = 0; q < pk.nq; ++q) {
@@ -197,6 +207,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_
         bulk_g2s(dst + q * pk.mb, src, pk.mb * (unsigned)sizeof(T), mbar);
       }
     } else {
+      PU_ASSERT(row < g.n && RB <= g.ld * sizeof(T));
       bulk_g2s(dst, in + (long long)row * g.ld, RB, mbar);
     }
   };

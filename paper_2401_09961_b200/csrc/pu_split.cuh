@@ -49,7 +49,8 @@ __device__ __forceinline__ void split_dif_load(int q, const FftPlan<T>& pl, cplx
     cplx<T> y;
     if (q == 0) y = cadd<T>(x0, x1);
     else y = cmul<T>(csub<T>(x0, x1), __ldg(pl.tw + j));
-    buf[spad(j)] = y;
+    PU_ASSERT(spad(j) < ldseq_for(LH));
+    *sm_chk(&buf[spad(j)]) = y;
   }
 }
 
@@ -65,7 +66,8 @@ __device__ __forceinline__ void split_dit_store(int q, const FftPlan<T>& pl, cpl
   const cplx<T>* other = cl.map_shared_rank(buf, q ^ 1);
   const int n = 2 * LH;
   for (int t = threadIdx.x; t < LH; t += blockDim.x) {
-    const cplx<T> mine = buf[spad(t)], theirs = other[spad(t)];
+    PU_ASSERT(spad(t) < ldseq_for(LH));
+    const cplx<T> mine = *sm_chk(&buf[spad(t)]), theirs = other[spad(t)];
     const cplx<T> e = q == 0 ? mine : theirs;
     const cplx<T> o = cmul<T>(q == 0 ? theirs : mine, __ldg(pl.tw + t));
     const cplx<T> x = q == 0 ? cadd<T>(e, o) : csub<T>(e, o);

@@ -76,7 +76,7 @@ class Workspace:
 
     # scalar slots (fp64) in the device scalar block
     (S_HOLD, S_HNEW, S_HPROP, S_HCAND, S_MEAN, S_TAKE, S_HACC, S_HNEXT, S_F, S_L1, S_DOT,
-     S_EVH) = range(12)
+     S_EVH, S_CHK_NF, S_CHK_RANGE) = range(14)
     NSCAL = 16
 
     @classmethod

@@ -104,8 +104,10 @@ class DeviceUnwrap:
             self._keep = [ws.pack(c.cv, self.W[0]), ws.pack(c.ch, self.W[1])]
         x64 = x_dev if x_dev.dtype == torch.float64 else x_dev.to(torch.float64)
         self._x = x64.contiguous()
-        ws.call("pu_wrapped_gradients", _ptr(self._x), int(self._x.shape[1]), _ptr(self.G[0]), _ptr(self.G[1]),
-                float(lo), st)
+        # gradients + the input check of phase.py:100-115 from the same loads;
+        # the counts are read with the first scalar snapshot (check_input)
+        ws.call("pu_wrapped_gradients_checked", _ptr(self._x), int(self._x.shape[1]), _ptr(self.G[0]),
+                _ptr(self.G[1]), float(lo), ws.sp(ws.S_CHK_NF), st)
         if _rhs_in_kernel(ws):
             self.B = None
         else:
@@ -213,6 +215,15 @@ class DetachedUnwrap:
         return ones
 
 
+def check_input(scal, ws):
+    """phase.py:108-114 from the counts pu_wrapped_gradients_checked left in
+    the scalar block: the reference's ValueError, raised before any result."""
+    if scal[ws.S_CHK_NF] != 0.0:
+        raise ValueError("phase grid contains non-finite values")
+    if scal[ws.S_CHK_RANGE] != 0.0:
+        raise ValueError("wrapped phase values must lie in [0, 2*pi)")
+
+
 def _record(k, m_cg, delta_rel, scal, ctrl, ws):
     raise_if_breakdown(ctrl)
     sufficient = bool(scal[ws.S_TAKE] != 0.0)
@@ -281,6 +292,8 @@ class _LoopJob:
             return True
         ws, params = self.ws, self.params
         scal, ctrl = ws.read_snapshot()
+        if self.k == 1:
+            check_input(scal, ws)  # the input check rides on the first snapshot
         self.trace.append(_record(*self.pending, scal, ctrl, ws))
         self.pending = None
         k = self.k
@@ -351,7 +364,7 @@ def unwrap_many(xs, c: WeightField | None = None, model: ModelParams | None = No
         s.wait_stream(caller)
         with torch.cuda.stream(s):
             x_dev = xi.to(device=dev, dtype=torch.float64) if isinstance(xi, torch.Tensor) else ws.upload_grid(xi)
-            _validate_device(x_dev)
+            _check_shape(x_dev)
             active[slot] = (i, _LoopJob(ws, x_dev, c, model, params, gradient_lo, concurrent=slots > 1))
 
     for slot in range(slots):
@@ -390,16 +403,11 @@ def _check_call(c, n, m, gradient_lo):
         raise ValueError(f"lo must be 0 or -pi, got {gradient_lo!r}")
 
 
-def _validate_device(x_dev):
-    """phase.py:100-115 on a device grid (one small synchronising read)."""
-    torch = _torch()
+def _check_shape(x_dev):
+    """phase.py:104-106; the value checks (phase.py:108-114) run inside the
+    gradient kernel and are read with the first scalar snapshot."""
     if x_dev.dim() != 2 or x_dev.shape[0] < 1 or x_dev.shape[1] < 1:
         raise ValueError(f"phase grid must be 2-D and non-empty, got shape {tuple(x_dev.shape)}")
-    chk = torch.stack([x_dev.min(), x_dev.max(), torch.isfinite(x_dev).all().to(torch.float64)]).cpu()
-    if chk[2] != 1.0:
-        raise ValueError("phase grid contains non-finite values")
-    if float(chk[0]) < 0.0 or float(chk[1]) >= 2.0 * np.pi:
-        raise ValueError("wrapped phase values must lie in [0, 2*pi)")
 
 
 def unwrap(x, c: WeightField | None = None, model: ModelParams | None = None, params: IrlsParams | None = None,
@@ -426,7 +434,7 @@ def unwrap(x, c: WeightField | None = None, model: ModelParams | None = None, pa
         ws_in = Workspace.get(int(arr.shape[0]), int(arr.shape[1]), dtype, (model or ModelParams()).tau,
                               (model or ModelParams()).delta, dev)
         x_dev = ws_in.upload_grid(arr if isinstance(arr, torch.Tensor) else arr)
-    _validate_device(x_dev)  # phase.py:100-115 on the device: finite, within [0, 2pi)
+    _check_shape(x_dev)  # values: checked by the gradient kernel (check_input)
     n, m = int(x_dev.shape[0]), int(x_dev.shape[1])
     model = model or ModelParams()
     params = params or IrlsParams()
