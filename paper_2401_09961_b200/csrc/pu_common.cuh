@@ -26,20 +26,21 @@ namespace pu {
 // Compiled out of the production library.
 // ---------------------------------------------------------------------------
 #ifdef PU_DEBUG_CHECKS
-#define PU_ASSERT(c)                                                                            \
-  do {                                                                                          \
-    if (!(c)) {                                                                                 \
-      printf("PU_ASSERT failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x, \
-             (int)threadIdx.x, #c);                                                             \
-      __trap();                                                                                 \
-    }                                                                                           \
+// trap (no printf: a printf per inlined site multiplied the compile time)
+#define PU_ASSERT(c)     \
+  do {                   \
+    if (!(c)) __trap();  \
   } while (0)
+// a dynamic-shared-memory address [p, p + 1) lies inside this CTA's
+// dynamic allocation (base of the extern array .. + %dynamic_smem_size)
 template <typename P>
 __device__ __forceinline__ P* sm_chk(P* p) {
-  unsigned tot;
-  asm("mov.u32 %0, %%total_smem_size;" : "=r"(tot));
+  extern __shared__ __align__(16) unsigned char pu_dyn_smem_[];
+  unsigned dyn;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+  const unsigned base = (unsigned)__cvta_generic_to_shared(pu_dyn_smem_);
   const unsigned a = (unsigned)__cvta_generic_to_shared(p);
-  PU_ASSERT(a + sizeof(P) <= tot);
+  if (a < base || a + sizeof(P) > base + dyn) __trap();
   return p;
 }
 #else

@@ -239,22 +239,23 @@ __device__ __forceinline__ void col_last_stage(const Grid& g, T* data, int j0, c
 // ---------------------------------------------------------------------------
 // K3 / API: column DCT-II, spectral division, column DCT-III, in place on a
 // panel of `cols_per_cta` columns; reduces rho_u = <r_hat, z_hat>.
+// cols_panel is one panel (index pidx) and returns this thread's share of
+// rho_u; k_cols_spec runs one panel per CTA, the persistent small-grid PCG
+// kernel (pu_persist.cuh) loops over panels.
 // ---------------------------------------------------------------------------
-template <typename T, int EMAX, int LS, int MODE>
-__global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_blocks(LS, EMAX)) k_cols_spec(Grid g, FftPlan<T> pl, const T* __restrict__ lam_cols, int cols_per_cta, T* data,
-                            PcgCtrl* ctrl, RedScratch rs, int site, int it, Push ps, int nfull) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  cplx<T>* buf = reinterpret_cast<cplx<T>*>(smraw);
-  if (MODE != MODE_API && ctrl->done) return;
+template <typename T, int EMAX, int LS>
+__device__ __forceinline__ T cols_panel(const Grid& g, const FftPlan<T>& pl, const T* __restrict__ lam_cols,
+                                        int cols_per_cta, T* data, const Push& ps, int nfull, int pidx,
+                                        cplx<T>* buf) {
   const int n = LS > 0 ? LS : g.n;  // static plans are only used when n == L
   // static plans: compile-time panel width; runtime plans: 4 or 2 (smem)
   const int W0 = LS > 0 ? static_panel_cols(LS, EMAX, sizeof(T)) : cols_per_cta;
   // balanced grid (static plans): CTAs past `nfull` take half panels, so the
   // last wave is spread over every SM instead of a few full panels
   constexpr bool HALF_OK = LS > 0 && static_panel_cols(LS > 0 ? LS : 4096, EMAX, sizeof(T)) >= 8;  // host: cols_per_cta >= 8
-  const bool halfp = HALF_OK && (int)blockIdx.x >= nfull;
+  const bool halfp = HALF_OK && pidx >= nfull;
   const int W = halfp ? W0 / 2 : W0;
-  const int j0 = halfp ? nfull * W0 + ((int)blockIdx.x - nfull) * W : (int)blockIdx.x * W0;
+  const int j0 = halfp ? nfull * W0 + (pidx - nfull) * W : pidx * W0;
   const int ncols = min(W, g.m - j0);
   const int nseq = (ncols + 1) >> 1;
   constexpr bool FUSE = LS > 0 && col_fused_ok<(LS > 0 ? LS : 4096), EMAX>();
@@ -321,6 +322,16 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_
     fft_n<T, EMAX, LS>(buf, nseq, pl);
     panel_store<T>(g, pl, data, j0, W, ncols, nseq, buf, n, ps);
   }
+  return accT;
+}
+
+template <typename T, int EMAX, int LS, int MODE>
+__global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_blocks(LS, EMAX)) k_cols_spec(Grid g, FftPlan<T> pl, const T* __restrict__ lam_cols, int cols_per_cta, T* data,
+                            PcgCtrl* ctrl, RedScratch rs, int site, int it, Push ps, int nfull) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  cplx<T>* buf = reinterpret_cast<cplx<T>*>(smraw);
+  if (MODE != MODE_API && ctrl->done) return;
+  const T accT = cols_panel<T, EMAX, LS>(g, pl, lam_cols, cols_per_cta, data, ps, nfull, (int)blockIdx.x, buf);
   if (MODE != MODE_API) {
     double acc[1] = {(double)accT};
     double tot[1];

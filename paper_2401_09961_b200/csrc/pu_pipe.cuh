@@ -175,12 +175,15 @@ __device__ __forceinline__ bool row_pair_smem_ok(unsigned char* smraw, bool one,
   return true;
 }
 
+// One row pair s of K2b (forward) / K4 (inverse); the mbarrier at smraw is
+// initialised by the caller and `ph` is its current phase parity (advanced
+// here by the phases this pair consumed).  k_rows_pipe runs one pair per CTA;
+// the persistent small-grid PCG kernel (pu_persist.cuh) loops over pairs.
 template <typename T, int EMAX, int LS, bool INV>
-__global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_blocks(LS, EMAX))
-    k_rows_pipe(Grid g, FftPlan<T> pl, const T* __restrict__ in, T* __restrict__ out, const PcgCtrl* ctrl,
-                const T* __restrict__ pold, int first, Pack pk) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  if (ctrl && ctrl->done) return;
+__device__ __forceinline__ void rows_pair(const Grid& g, const FftPlan<T>& pl, const T* __restrict__ in,
+                                          T* __restrict__ out, const PcgCtrl* ctrl, const T* __restrict__ pold,
+                                          int first, const Pack& pk, int s, unsigned char* smraw, unsigned& ph) {
+  int waits = 0;  // mbarrier phases completed by this row pair
   const int n = LS > 0 ? LS : g.m;  // static plans only when n == L
   const int S = (g.n + 1) >> 1;     // row pairs
   const unsigned RBrow = stage_row_bytes(n, sizeof(T));  // one plain row
@@ -193,11 +196,6 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_
   const bool ffuse = FFUSE && !one;  // launched with rows_fused_smem (DctLaunch::rows_pipe)
   T* sb = one ? sa : reinterpret_cast<T*>(smraw + 128 + RB);
   cplx<T>* buf0 = reinterpret_cast<cplx<T>*>(smraw + 128 + (ffuse ? 0 : (one ? 1 : 2) * RB));
-  if (threadIdx.x == 0) {
-    mbar_init(mbar, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
   PU_ASSERT(row_pair_smem_ok<T>(smraw, one, ffuse, RB, pl.ldseq));
   auto fetch = [&](T* dst, int row) {  // one thread; RB bytes
     if (pin) {
@@ -231,10 +229,11 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_
       mbar_expect_tx(mbar, RB);
       fetch(sa, ia + 1);
     }
-    mbar_wait(mbar, 1);
+    mbar_wait(mbar, ph ^ 1);
+    ++waits;
   };
-  const int s = blockIdx.x;
   if (threadIdx.x == 0 && s < S) {
+    fence_proxy_async();  // the staging may have been read by the previous pair (persistent loop)
     issue(s);
     if (INV && ffuse && pold != nullptr && !first) {
       // fused K4 reads the old direction from global memory in its output
@@ -246,7 +245,8 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_
   const int half = n / 2 + 1;
   if (s < S) {
     cplx<T>* buf = buf0;
-    mbar_wait(mbar, 0);
+    mbar_wait(mbar, ph);
+    ++waits;
     const int ia = 2 * s;
     const bool hasb = ia + 1 < g.n;
     if (one) {
@@ -360,7 +360,10 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_
     } else {
       const int cpr = (n + 3) >> 2;
       const T beta = axpy ? (T)ctrl->beta : (T)0;
-      if (axpy && !one && !ffuse) mbar_wait(mbar, 1);
+      if (axpy && !one && !ffuse) {
+        mbar_wait(mbar, ph ^ 1);
+        ++waits;
+      }
       for (int e = threadIdx.x; e < 2 * cpr; e += blockDim.x) {
         const int rr = e >= cpr, j0 = (e - rr * cpr) * 4;
         if (rr && !hasb) continue;
@@ -385,6 +388,22 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_
       }
     }
   }
+  ph ^= (unsigned)(waits & 1);
+}
+
+template <typename T, int EMAX, int LS, bool INV>
+__global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_blocks(LS, EMAX))
+    k_rows_pipe(Grid g, FftPlan<T> pl, const T* __restrict__ in, T* __restrict__ out, const PcgCtrl* ctrl,
+                const T* __restrict__ pold, int first, Pack pk) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  if (ctrl && ctrl->done) return;
+  if (threadIdx.x == 0) {
+    mbar_init(reinterpret_cast<uint64_t*>(smraw), 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  unsigned ph = 0;
+  rows_pair<T, EMAX, LS, INV>(g, pl, in, out, ctrl, pold, first, pk, (int)blockIdx.x, smraw, ph);
 }
 
 }  // namespace pu

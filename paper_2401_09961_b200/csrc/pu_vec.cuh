@@ -121,10 +121,9 @@ __global__ void k_ghost_pslack(Grid g, const T* __restrict__ r, const T* __restr
 // forward differences only (pcg.py:82-89, 102-108).
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(256, PU_MINB(T, 4)) k_pcg_p_v(Grid g, const T* __restrict__ r, const T* __restrict__ pold,
-                                                    T* __restrict__ pnew, const T* __restrict__ dv,
-                                                    const T* __restrict__ dh, PcgCtrl* ctrl, RedScratch rs, int site,
-                                                    int it) {
+__device__ __forceinline__ void pcg_p_body(const Grid& g, const T* __restrict__ r, const T* __restrict__ pold,
+                                           T* __restrict__ pnew, const T* __restrict__ dv, const T* __restrict__ dh,
+                                           PcgCtrl* ctrl, const RedScratch& rs, int site, int it) {
   if (ctrl->done) return;
   const bool first = it == 0;
   const T beta = (T)ctrl->beta;
@@ -165,15 +164,23 @@ __global__ void __launch_bounds__(256, PU_MINB(T, 4)) k_pcg_p_v(Grid g, const T*
   if (red_final<1>(acc, rs, site, tot) && threadIdx.x == 0) fin_k1(ctrl, tot, it);
 }
 
+template <typename T>
+__global__ void __launch_bounds__(256, PU_MINB(T, 4)) k_pcg_p_v(Grid g, const T* __restrict__ r, const T* __restrict__ pold,
+                                                    T* __restrict__ pnew, const T* __restrict__ dv,
+                                                    const T* __restrict__ dh, PcgCtrl* ctrl, RedScratch rs, int site,
+                                                    int it) {
+  pcg_p_body<T>(g, r, pold, pnew, dv, dh, ctrl, rs, site, it);
+}
+
 // ---------------------------------------------------------------------------
 // K2a: residual update + slack preconditioner + norms.
 // UPDATE: x += alpha p, r -= alpha A p.  SUBMEAN: r_u -= ctrl->mean_ru.
 // MODE_ITER finaliser: ||r|| exits (pcg.py:94-100); MODE_INIT: rho_s only.
 // ---------------------------------------------------------------------------
 template <typename T, bool UPDATE, bool SUBMEAN, int MODE>
-__global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_pcg_r_v(Grid g, const T* __restrict__ p, const T* __restrict__ dv,
-                                                 const T* __restrict__ dh, T* __restrict__ x, T* __restrict__ r,
-                                                 PcgCtrl* ctrl, double* res_norms, RedScratch rs, int site, int it) {
+__device__ __forceinline__ void pcg_r_body(const Grid& g, const T* __restrict__ p, const T* __restrict__ dv,
+                                           const T* __restrict__ dh, T* __restrict__ x, T* __restrict__ r,
+                                           PcgCtrl* ctrl, double* res_norms, const RedScratch& rs, int site, int it) {
   if (ctrl->done) return;
   const long long P = g.plane, ld = g.ld;
   const T alpha = (T)ctrl->alpha, nalpha = (T)(-ctrl->alpha);
@@ -235,12 +242,19 @@ __global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_pcg_r_v(Grid g, const T*
   if (red_final<2>(acc, rs, site, tot) && threadIdx.x == 0) fin_k2(g, ctrl, res_norms, tot, it, MODE);
 }
 
+template <typename T, bool UPDATE, bool SUBMEAN, int MODE>
+__global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_pcg_r_v(Grid g, const T* __restrict__ p, const T* __restrict__ dv,
+                                                 const T* __restrict__ dh, T* __restrict__ x, T* __restrict__ r,
+                                                 PcgCtrl* ctrl, double* res_norms, RedScratch rs, int site, int it) {
+  pcg_r_body<T, UPDATE, SUBMEAN, MODE>(g, p, dv, dh, x, r, ctrl, res_norms, rs, site, it);
+}
+
 // update + sum(r_u) for the every-50 re-projection (the mean is subtracted by
 // k_pcg_r_v<false, true, ...> next)
 template <typename T>
-__global__ void __launch_bounds__(256) k_pcg_upd_sum_v(Grid g, const T* __restrict__ p, const T* __restrict__ dv,
-                                                       const T* __restrict__ dh, T* __restrict__ x,
-                                                       T* __restrict__ r, PcgCtrl* ctrl, RedScratch rs, int site) {
+__device__ __forceinline__ void pcg_upd_sum_body(const Grid& g, const T* __restrict__ p, const T* __restrict__ dv,
+                                                 const T* __restrict__ dh, T* __restrict__ x, T* __restrict__ r,
+                                                 PcgCtrl* ctrl, const RedScratch& rs, int site) {
   if (ctrl->done) return;
   const long long P = g.plane, ld = g.ld;
   const T alpha = (T)ctrl->alpha, nalpha = (T)(-ctrl->alpha);
@@ -277,6 +291,13 @@ __global__ void __launch_bounds__(256) k_pcg_upd_sum_v(Grid g, const T* __restri
   }
   double tot[1];
   if (red_final<1>(acc, rs, site, tot) && threadIdx.x == 0) fin_upd(g, ctrl, tot);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_pcg_upd_sum_v(Grid g, const T* __restrict__ p, const T* __restrict__ dv,
+                                                       const T* __restrict__ dh, T* __restrict__ x,
+                                                       T* __restrict__ r, PcgCtrl* ctrl, RedScratch rs, int site) {
+  pcg_upd_sum_body<T>(g, p, dv, dh, x, r, ctrl, rs, site);
 }
 
 // setup: x = x0 (skipped when x aliases x0), r = b - A x0, ||b||, ||r0||
@@ -830,7 +851,7 @@ __global__ void __launch_bounds__(256, 2) k_accept_start_v(
 }
 
 // pu_irls_begin_z0: fin_start from the start-up sums held by k_accept_start_v
-__global__ void k_fin_start_held(PcgCtrl* ctrl, double* res_norms, const double* held, double rel_tol,
+static __global__ void k_fin_start_held(PcgCtrl* ctrl, double* res_norms, const double* held, double rel_tol,
                                  int max_iters) {
   if (threadIdx.x == 0 && blockIdx.x == 0) fin_start(ctrl, res_norms, held, rel_tol, max_iters);
 }
