@@ -172,8 +172,9 @@ __device__ __forceinline__ void col_first_stage(const Grid& g, const T* __restri
     if (b >= NSEQ * NB) break;  // CTAs may be rounded up
     const T* pa = data + (long long)(2 * j) * ld + j0 + 2 * s;
     const T* pb = data + (long long)(2 * L - 1 - 2 * j) * ld + j0 + 2 * s;
+    // rows touched: 2 j + 2 r NB (r < R/2) and 2L - 1 - 2 j - 2 r NB (R/2 <= r < R)
     PU_ASSERT(2 * j + 2 * (R / 2 - 1) * NB < g.n && 2 * L - 1 - 2 * j - 2 * (R - 1) * NB >= 0 &&
-              2 * L - 1 - 2 * j < g.n && j0 + 2 * s + 2 <= ld);
+              2 * L - 1 - 2 * j - R * NB < g.n && j0 + 2 * s + 2 <= ld);
 #pragma unroll
     for (int r = 0; r < R / 2; ++r) v[q][r] = __ldg(reinterpret_cast<const cplx<T>*>(pa + r * step));
 #pragma unroll
@@ -224,7 +225,7 @@ __device__ __forceinline__ void col_last_stage(const Grid& g, T* data, int j0, c
       }
     } else {
       const long long ld = g.ld, step = 2LL * NS * ld;
-      PU_ASSERT(2 * j + 2 * (R / 2 - 1) * NS < g.n && 2 * L - 1 - 2 * j < g.n &&
+      PU_ASSERT(2 * j + 2 * (R / 2 - 1) * NS < g.n && 2 * L - 1 - 2 * j - R * NS < g.n &&
                 2 * L - 1 - 2 * j - 2 * (R - 1) * NS >= 0 && j0 + 2 * s + 2 <= ld);
       T* pa = data + (long long)(2 * j) * ld + j0 + 2 * s;
       T* pb = data + (long long)(2 * L - 1 - 2 * j) * ld + j0 + 2 * s;

@@ -33,6 +33,7 @@ def main():
     p = pu.IrlsParams(max_outer_iters=3)
     for dt in ("fp64", "fp32"):
         pu.unwrap(scene(64, 512, 1), params=p, dtype=dt)        # static plans (512 rows / 64 columns runtime)
+        pu.unwrap(scene(512, 512, 11), params=p, dtype=dt)      # static 512-point columns (fused first/last stage)
         pu.unwrap(scene(37, 53, 2), params=p, dtype=dt)         # runtime mixed-radix plans
         pu.unwrap(scene(11, 29, 3), params=p, dtype=dt)         # Bluestein (11, 29 prime)
         pu.unwrap_rows(scene(40, 48, 4), params=p, dtype=dt, bands=3)               # bands, packed transpose
