@@ -317,12 +317,26 @@ __host__ __device__ constexpr int first_radix_rt(int L, int emax) {
 template <int L, int EMAX>
 __host__ __device__ constexpr int first_radix() { return first_radix_rt(L, EMAX); }
 
-template <typename T, int R, int EMAX, int L, int NS, int OFF>
+// GRP: stage barriers per sequence (named barrier 2 + s over the NB threads
+// that own sequence s; needs Q == 1 and NB a multiple of 32) instead of
+// CTA-wide, so the sequences of a column panel progress independently.
+template <bool GRP>
+__device__ __forceinline__ void stage_sync(int nb, int nseq) {
+  if constexpr (GRP) {
+    const int s = threadIdx.x / nb;
+    if (s < nseq) asm volatile("bar.sync %0, %1;" ::"r"(2 + s), "r"(nb) : "memory");
+  } else {
+    __syncthreads();
+  }
+}
+
+template <typename T, int R, int EMAX, int L, int NS, int OFF, bool GRP = false>
 __device__ __forceinline__ void fft_stage_s(cplx<T>* buf, int seq0, int nseq, const cplx<T>* __restrict__ stw) {
   constexpr int Q = EMAX / R;
   constexpr int NB = L / R;
   constexpr int LD = ldseq_for(L);
   static_assert(Q >= 1 && NB * R == L, "bad static stage");
+  static_assert(!GRP || (Q == 1 && NB % 32 == 0), "grouped stages need one butterfly per thread");
   const int total = nseq * NB;
   cplx<T> v[Q][R];
   int ob[Q], sbase[Q];
@@ -371,7 +385,7 @@ __device__ __forceinline__ void fft_stage_s(cplx<T>* buf, int seq0, int nseq, co
       Dft<T, R>::run(v[q]);
     }
   }
-  __syncthreads();
+  stage_sync<GRP>(NB, nseq);
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
     if (ob[q] >= 0) {
@@ -400,7 +414,7 @@ __device__ __forceinline__ void fft_stage_s(cplx<T>* buf, int seq0, int nseq, co
       }
     }
   }
-  __syncthreads();
+  stage_sync<GRP>(NB, nseq);
 }
 
 // Stage s >= 1 of the static plan reads W_{NS R}^k, k < NS, from its block at
@@ -416,13 +430,21 @@ __device__ __forceinline__ void fft_stages_s(cplx<T>* buf, int seq0, int nseq, c
 
 // Stages NS in [NS, STOP) of the static plan (the column kernel runs the
 // first / last stage itself, straight from / to global memory).
-template <typename T, int EMAX, int L, int NS, int OFF, int STOP>
+template <typename T, int EMAX, int L, int NS, int OFF, int STOP, bool GRP = false>
 __device__ __forceinline__ void fft_stages_range(cplx<T>* buf, int seq0, int nseq, const cplx<T>* stw) {
   if constexpr (NS < STOP) {
     constexpr int R = (NS == 1) ? first_radix<L, EMAX>() : (EMAX >= 16 ? 16 : 8);
-    fft_stage_s<T, R, EMAX, L, NS, OFF>(buf, seq0, nseq, stw);
-    fft_stages_range<T, EMAX, L, NS * R, (NS == 1 ? OFF : OFF + NS), STOP>(buf, seq0, nseq, stw);
+    fft_stage_s<T, R, EMAX, L, NS, OFF, GRP>(buf, seq0, nseq, stw);
+    fft_stages_range<T, EMAX, L, NS * R, (NS == 1 ? OFF : OFF + NS), STOP, GRP>(buf, seq0, nseq, stw);
   }
+}
+
+// every stage of the static plan of L has one butterfly per thread and NB a
+// multiple of 32 (grouped barriers possible)
+template <int L, int EMAX>
+__host__ __device__ constexpr bool grp_ok() {
+  return EMAX / first_radix<L, EMAX>() == 1 && (L / first_radix<L, EMAX>()) % 32 == 0 &&
+         (L / (EMAX >= 16 ? 16 : 8)) % 32 == 0;
 }
 
 // offset of stage NS's twiddle block in pl.stw (mirrors fft_stages_s)

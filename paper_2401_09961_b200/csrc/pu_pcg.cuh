@@ -262,6 +262,15 @@ __device__ __forceinline__ T cols_panel(const Grid& g, const FftPlan<T>& pl, con
   constexpr bool FUSE = LS > 0 && col_fused_ok<(LS > 0 ? LS : 4096), EMAX>();
   constexpr int LF = LS > 0 ? LS : 4096;  // (LS == 0: FUSE is false, LF unused)
   const bool fuse = FUSE && ncols == W;
+  // K3 group mode (PU_K3_GROUPS): after the CTA-wide first stage, every
+  // sequence's stages, post-processing and inverse stages synchronise only
+  // its own NB threads (named barriers), the last stage is CTA-wide again
+#ifdef PU_K3_GROUPS
+  constexpr bool GRP = FUSE && grp_ok<LF, EMAX>();
+#else
+  constexpr bool GRP = false;
+#endif
+  constexpr int NBG = LF / EMAX;  // threads per sequence in group mode
   if (fuse) {
     if constexpr (FUSE) {
       constexpr int NSF = static_panel_cols(LF, EMAX, sizeof(T)) / 2;
@@ -270,7 +279,7 @@ __device__ __forceinline__ T cols_panel(const Grid& g, const FftPlan<T>& pl, con
       } else {
         col_first_stage<T, EMAX, LF, NSF>(g, data, j0, buf);
       }
-      fft_stages_range<T, EMAX, LF, first_radix<LF, EMAX>(), 0, LF>(buf, 0, nseq, pl.stw);
+      fft_stages_range<T, EMAX, LF, first_radix<LF, EMAX>(), 0, LF, GRP>(buf, 0, nseq, pl.stw);
     }
   } else {
     panel_load<T>(g, pl, data, j0, W, ncols, nseq, buf, n);
@@ -280,7 +289,12 @@ __device__ __forceinline__ T cols_panel(const Grid& g, const FftPlan<T>& pl, con
   T accT = (T)0;  // per-thread partial of rho_u in T (a few dozen terms), fp64 across threads
   const int half = n / 2 + 1;
   const double tau = g.tau;
-  for (int e = threadIdx.x; e < nseq * half; e += blockDim.x) {
+  const bool grp = GRP && fuse;
+  // group mode: sequence s = threadIdx.x / NBG, its NBG threads stride over k
+  const int e0 = grp ? (int)threadIdx.x % NBG + ((int)threadIdx.x / NBG) * half : (int)threadIdx.x;
+  const int e1 = grp ? ((int)threadIdx.x / NBG < nseq ? ((int)threadIdx.x / NBG + 1) * half : 0) : nseq * half;
+  const int es = grp ? NBG : (int)blockDim.x;
+  for (int e = e0; e < e1; e += es) {
     const int s = e / half, k = e - s * half;
     const int nk = k == 0 ? 0 : n - k;
     cplx<T>* sb = buf + s * pl.ldseq;
@@ -308,10 +322,12 @@ __device__ __forceinline__ T cols_panel(const Grid& g, const FftPlan<T>& pl, con
     sb[spad(k)] = ck;
     if (nk != k) sb[spad(nk)] = cnk;
   }
-  __syncthreads();
+  if (grp) stage_sync<GRP>(NBG, nseq);
+  else __syncthreads();
   if (fuse) {
     if constexpr (FUSE) {
-      fft_stages_range<T, EMAX, LF, 1, 0, LF / (EMAX >= 16 ? 16 : 8)>(buf, 0, nseq, pl.stw);
+      fft_stages_range<T, EMAX, LF, 1, 0, LF / (EMAX >= 16 ? 16 : 8), GRP>(buf, 0, nseq, pl.stw);
+      if constexpr (GRP) __syncthreads();  // the last stage reads across sequences
       constexpr int NSF = static_panel_cols(LF, EMAX, sizeof(T)) / 2;
       if (halfp) {
         if constexpr (NSF >= 4) col_last_stage<T, EMAX, LF, NSF / 2>(g, data, j0, buf, pl.stw, ps);

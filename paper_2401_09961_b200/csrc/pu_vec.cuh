@@ -21,6 +21,14 @@
 // resident CTAs per SM the element-wise kernels are compiled for: the fp32
 // budget in fp32; 2 (128 registers) in fp64, where the fp32 budgets spill
 #define PU_MINB(T, N) (sizeof(T) == 4 ? (N) : 2)
+// fp64 once-per-outer-iteration kernels (H pair, acceptance, start-up): 2
+// CTAs/SM (128 registers, ~150-200 B of spills) by default; PU_OUTER64_MINB=1
+// builds them at 1 CTA/SM without spills (A/B, the way k_accept_start_v
+// won: 0.70 vs 0.865 ms)
+#ifndef PU_OUTER64_MINB
+#define PU_OUTER64_MINB 2
+#endif
+#define PU_MINB_OUTER(T, N) (sizeof(T) == 4 ? (N) : PU_OUTER64_MINB)
 
 namespace pu {
 
@@ -313,7 +321,7 @@ struct CandArgs {
 };
 
 template <typename T, bool CAND, bool RHSG = false>
-__global__ void __launch_bounds__(256, 2) k_pcg_start_v(Grid g, const T* __restrict__ b, const T* x0, T* x,
+__global__ void __launch_bounds__(256, PU_MINB_OUTER(T, 2)) k_pcg_start_v(Grid g, const T* __restrict__ b, const T* x0, T* x,
                                                         T* __restrict__ r, const T* __restrict__ dv,
                                                         const T* __restrict__ dh, PcgCtrl* ctrl, double* res_norms,
                                                         double rel_tol, int max_iters, RedScratch rs, int site,
@@ -463,7 +471,7 @@ __device__ __forceinline__ T slack4(T c, T v, T w, T d2) {
 
 // w = sqrt((c v)^2 + delta^2), d = c^2 / w; H(x, w_prev), H(x, w)
 template <typename T>
-__global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_weights_hpair_v(Grid g, const T* __restrict__ x, const T* __restrict__ cv,
+__global__ void __launch_bounds__(256, PU_MINB_OUTER(T, 3)) k_weights_hpair_v(Grid g, const T* __restrict__ x, const T* __restrict__ cv,
                                                          const T* __restrict__ ch, const T* __restrict__ gv,
                                                          const T* __restrict__ gh, const T* __restrict__ wpv,
                                                          const T* __restrict__ wph, T* __restrict__ wv,
@@ -515,7 +523,7 @@ __global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_weights_hpair_v(Grid g, 
 
 // H(xa, w), H(xb, w), mean u of the accepted one, acceptance flag
 template <typename T>
-__global__ void __launch_bounds__(256, PU_MINB(T, 2)) k_hpair_states_v(Grid g, const T* __restrict__ xa, const T* __restrict__ xb,
+__global__ void __launch_bounds__(256, PU_MINB_OUTER(T, 2)) k_hpair_states_v(Grid g, const T* __restrict__ xa, const T* __restrict__ xb,
                                                         const T* __restrict__ wv, const T* __restrict__ wh,
                                                         const T* __restrict__ gv, const T* __restrict__ gh,
                                                         const T* __restrict__ cv, const T* __restrict__ ch,
@@ -647,7 +655,7 @@ __global__ void __launch_bounds__(256, PU_MINB(T, 3)) k_accept_v(Grid g, const T
 // out[0] = H(dst, w_k) (the trace value and the next h_old), out[1] =
 // H(dst, w_next) (the next h_new).  cv/ch == nullptr: unit weights.
 template <typename T>
-__global__ void __launch_bounds__(256, PU_MINB(T, 2)) k_accept_weights_v(Grid g, const T* __restrict__ xa,
+__global__ void __launch_bounds__(256, PU_MINB_OUTER(T, 2)) k_accept_weights_v(Grid g, const T* __restrict__ xa,
                                                              const T* __restrict__ xb, const double* sel,
                                                              T* __restrict__ dst, const T* __restrict__ gv,
                                                              const T* __restrict__ gh, const T* __restrict__ cv,
@@ -717,11 +725,12 @@ __global__ void __launch_bounds__(256, PU_MINB(T, 2)) k_accept_weights_v(Grid g,
 // per-cell arithmetic and per-thread accumulation order as the two kernels
 // (same grid), so every value and sum is bit-identical to them.
 // (fp32: 2 CTAs/SM, 104 B of spills, 0.268 ms at C3; 1 CTA/SM at 196
-// registers without spills: 0.333 ms.  fp64 is not used: 0.865 ms spilling
-// vs 0.80 for the two kernels; 1 CTA/SM would win (0.70) but its FMA
-// contraction differs from the two-kernel build in the last bits.)
+// registers without spills: 0.333 ms.  fp64: 2 CTAs/SM spill, 0.865 ms vs
+// 0.80 for the two kernels; 1 CTA/SM, 0.70 ms, is the fp64 build.  Its FMA
+// contraction differs from the two-kernel build in the last bits, so fp64
+// results agree with the unfused path to ~1e-15, not bitwise.)
 template <typename T>
-__global__ void __launch_bounds__(256, 2) k_accept_start_v(
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) k_accept_start_v(
     Grid g, const T* __restrict__ xa, const T* __restrict__ xb, const double* sel, T* __restrict__ dst,
     const T* __restrict__ gv, const T* __restrict__ gh, const T* __restrict__ cv, const T* __restrict__ ch,
     const T* __restrict__ wkv, const T* __restrict__ wkh, T* __restrict__ wnv, T* __restrict__ wnh,

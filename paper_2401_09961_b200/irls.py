@@ -21,10 +21,10 @@ from .pcg import raise_if_breakdown
 from .phase import WeightField, validate_wrapped
 
 # pu_accept_weights_start: acceptance of k and the start-up of k + 1 in one
-# pass.  Used in fp32 on grids of >= 2048^2 cells: the fp64 build of the fused
-# kernel spills (measured slower than two kernels), and on small grids the
-# start-up is what keeps the GPU busy while the host applies the budget rule
-# (C1 512^2: 10.3 -> 10.6 ms fused; C3 fp32: 120.1 -> 116.5 ms).
+# pass.  Used on grids of >= 2048^2 cells (C3 fp32: 120.1 -> 116.5 ms; fp64:
+# the 1-CTA/SM build, 0.70 vs 0.80 ms per outer iteration); on small grids
+# the separate start-up is what keeps the GPU busy while the host applies the
+# budget rule (C1 512^2: 10.3 -> 10.6 ms fused).
 # PU_FUSED_START=0 / 1 forces it off / on (A/B timing).
 FUSED_START = os.environ.get("PU_FUSED_START", "auto")
 FUSED_START_MIN_CELLS = 2048 * 2048
@@ -49,7 +49,7 @@ def _fuse_start(ws, concurrent=False):
     579 -> 561 ms fused)."""
     if FUSED_START in ("0", "1"):
         return FUSED_START == "1"
-    return ws.tdtype == _torch().float32 and (concurrent or ws.n * ws.m >= FUSED_START_MIN_CELLS)
+    return concurrent or ws.n * ws.m >= FUSED_START_MIN_CELLS
 
 
 def _torch():

@@ -168,7 +168,8 @@ def test_release_workspaces_and_replan():
 def test_fused_accept_start_bit_identical(monkeypatch, golden_unwrap, golden_meta, name, dtype):
     """pu_accept_weights_start (acceptance of k + start-up of k + 1 in one
     pass) against pu_accept_weights + pu_irls_begin: identical trace and
-    bit-identical state, on ragged grids, edges and user arc weights."""
+    state (bitwise in fp32, to round-off in fp64), on ragged grids, edges and
+    user arc weights."""
     from paper_2401_09961_b200 import irls
     x, cv, ch, tau, delta, prm, lo = case_inputs(golden_unwrap, golden_meta, name)
     params = pu.IrlsParams(**prm.__dict__)
@@ -177,10 +178,19 @@ def test_fused_accept_start_bit_identical(monkeypatch, golden_unwrap, golden_met
         monkeypatch.setattr(irls, "FUSED_START", mode)
         out[mode] = pu.unwrap(x, _weights(cv, ch), pu.ModelParams(tau, delta), params, lo, dtype=dtype)
     a, b = out["0"], out["1"]
-    assert [(r.m_cg, r.cg_iters, r.h_delta, r.sufficient_decrease) for r in a.trace.records] == \
-        [(r.m_cg, r.cg_iters, r.h_delta, r.sufficient_decrease) for r in b.trace.records]
-    for f in ("u", "vv", "vh"):
-        np.testing.assert_array_equal(getattr(a, f), getattr(b, f))
+    assert [(r.m_cg, r.cg_iters, r.sufficient_decrease) for r in a.trace.records] == \
+        [(r.m_cg, r.cg_iters, r.sufficient_decrease) for r in b.trace.records]
+    if dtype == "fp32":
+        assert [r.h_delta for r in a.trace.records] == [r.h_delta for r in b.trace.records]
+        for f in ("u", "vv", "vh"):
+            np.testing.assert_array_equal(getattr(a, f), getattr(b, f))
+    else:
+        # the fp64 fused kernel is a 1-CTA/SM build whose FMA contraction
+        # differs from the two-kernel build in the last bits
+        np.testing.assert_allclose([r.h_delta for r in a.trace.records], [r.h_delta for r in b.trace.records],
+                                   rtol=1e-12)
+        for f in ("u", "vv", "vh"):
+            assert rel(getattr(a, f), getattr(b, f)) <= 1e-12 or np.max(np.abs(getattr(a, f) - getattr(b, f))) <= 1e-13
 
 
 @pytest.mark.parametrize("dtype", ["fp32", "fp64"])
@@ -201,15 +211,15 @@ def test_rhs_in_kernel_bit_identical(monkeypatch, golden_unwrap, golden_meta, dt
 
 
 def test_fused_accept_start_auto_rule():
-    """The fused start-up is used in fp32 from 2048^2 cells (the default
-    bench workload) or when unwraps run concurrently, and not in fp64 or on
-    small single grids."""
+    """The fused start-up is used from 2048^2 cells (the default bench
+    workload) or when unwraps run concurrently, and not on small single
+    grids."""
     from paper_2401_09961_b200 import irls
     from paper_2401_09961_b200.device import Workspace
     import torch
     dev = torch.device("cuda", 0)
     assert irls._fuse_start(Workspace.get(2048, 2048, "fp32", 1e-2, 1e-6, dev))
-    assert not irls._fuse_start(Workspace.get(2048, 2048, "fp64", 1e-2, 1e-6, dev))
+    assert irls._fuse_start(Workspace.get(2048, 2048, "fp64", 1e-2, 1e-6, dev))
     assert not irls._fuse_start(Workspace.get(512, 512, "fp32", 1e-2, 1e-6, dev))
     assert irls._fuse_start(Workspace.get(512, 512, "fp32", 1e-2, 1e-6, dev), concurrent=True)
     pu.release_workspaces()
