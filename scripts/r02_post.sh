@@ -28,3 +28,20 @@ fi
 # 3. production build: full GPU suite with the parity report
 PU_PARITY_REPORT=gpurun_out/post_parity.jsonl timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/post_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/post_pytest.log
 tail -n 3 gpurun_out/post_grp_tests.log gpurun_out/post_o1_tests.log gpurun_out/post_chk_cases.log gpurun_out/post_chk_pytest.log gpurun_out/post_pytest.log; cat gpurun_out/post_ab.txt
+# 3b. row-sharded path through the bench (2 loopback bands, fp64) and C5 concurrency
+timeout 600 python bench.py --bands 2 --steps 3 --warmup 3 > gpurun_out/post_bands2.json 2> gpurun_out/post_bands2.err
+for c in 8 16; do
+  for dt in fp32 fp64; do
+    timeout 900 python bench.py --config c5 --concurrency $c --dtype $dt --steps 3 --warmup 3 --no-cpu-baseline --no-nested > gpurun_out/post_c5_${c}_${dt}.json 2>> gpurun_out/post_c5.err
+  done
+done
+# 4. ncu: launch list of one fp64 C3 unwrap, and --set full of the PCG / outer kernels in fp64
+CMD="python bench.py --profile-steps 1 --config c3 --dtype fp64"
+$CMD > gpurun_out/post_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/post_launches_fp64.csv $CMD > gpurun_out/post_ncu_launches.log 2>&1
+$CMD > gpurun_out/post_plain2.log 2>&1 && \
+ncu --set full --import-source on --clock-control none -k regex:'k_pcg_(p|r)_v' \
+    --launch-skip 20 --launch-count 4 -o gpurun_out/ncu_r02_pcg_fp64 -f $CMD > gpurun_out/post_ncu_full.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:'k_(accept_start|hpair_states)_v' \
+    --launch-skip 4 --launch-count 4 -o gpurun_out/ncu_r02_outer_fp64 -f $CMD > gpurun_out/post_ncu_full2.log 2>&1
+echo "ncu rc=$?"

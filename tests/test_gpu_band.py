@@ -97,3 +97,16 @@ def test_bands_cluster_split_rows_fp64(peer):
     res = pu.unwrap_rows(x, dtype="fp64", bands=2, peer=peer, params=pu.IrlsParams(max_outer_iters=6))
     assert [r.cg_iters for r in res.trace.records] == [r.cg_iters for r in single.trace.records]
     assert rel(res.u, single.u) <= 1e-9
+
+
+def test_band_graph_chunks_past_64_iterations():
+    """Loopback bands replay captured graphs of 64 PCG iterations per chunk;
+    a 100-iteration budget crosses a chunk boundary (and the every-50
+    re-projection) with an exit poll between the chunks."""
+    x = _scene(64, 72, noise=1.0, seed=13)
+    prm = pu.IrlsParams(max_iter_cg_start=100, max_cg_iters_cap=200, cg_rel_tol=1e-14, max_outer_iters=3)
+    single = pu.unwrap(x, params=prm, dtype="fp64")
+    res = pu.unwrap_rows(x, params=prm, dtype="fp64", bands=2)
+    assert [r.cg_iters for r in res.trace.records] == [r.cg_iters for r in single.trace.records]
+    assert max(r.cg_iters for r in res.trace.records) > 64
+    assert rel(res.u, single.u) <= 1e-9
