@@ -24,7 +24,7 @@ pytestmark = pytest.mark.gpu
 pu = pytest.importorskip("paper_2401_09961_b200")
 
 META = pc.available()
-SINGLE = [c for c in ("c1", "c2", "c3") if c in META]
+SINGLE = [c for c in ("c1", "c2", "c3", "c4") if c in META]
 C5 = sorted(c for c in META if c.startswith("c5b"))
 REPORT = os.environ.get("PU_PARITY_REPORT")  # optional JSON-lines output (profiles/)
 
