@@ -136,12 +136,14 @@ extern "C" int pu_unwrap(const double* x, int n, int m, const double* cv, const 
   char* base = nullptr;
   // planes: state x2, cand, rhs, grad, w x2, d, r, p0, p1, spec, weights
   const bool uniform = cv == nullptr;
-  const int nplanes = 3 + 3 + 3 + 3 + 2 + 2 + 2 + 2 + 3 + 3 + 3 + 1 + (uniform ? 0 : 2);
+  const int nplanes = 3 + 3 + 3 + 3 + 3 + 2 + 2 + 2 + 2 + 3 + 3 + 3 + 1 + (uniform ? 0 : 2);
   PU_CK(R.alloc(reinterpret_cast<void**>(&base), plane * nplanes), "cudaMalloc planes");
   char* at = base;
   auto take = [&](int k) { char* q = at; at += plane * k; return q; };
   void* S[2] = {take(3), take(3)};
-  void* cand = take(3);
+  // the candidate of iteration k lives in Cs[k & 1]: the fused acceptance of
+  // k reads it while writing the candidate of k + 1
+  void* Cs[2] = {take(3), take(3)};
   void* rhs = take(3);
   char* G = take(2);
   char* W[2] = {take(2), take(2)};
@@ -196,11 +198,6 @@ extern "C" int pu_unwrap(const double* x, int n, int m, const double* cv, const 
   PU_OK_OR(pu_weights_hpair(R.h, S[0], cvp, chp, gv, gh, nullptr, nullptr, W[0], W[0] + plane, dv, dh, blk + S_HOLD,
                             R.st));
 
-  auto read_block = [&]() -> int {
-    PU_CK(cudaMemcpyAsync(R.pin, blk, NSCAL * 8 + ctrl_bytes, cudaMemcpyDeviceToHost, R.st), "read scalars");
-    PU_CK(cudaStreamSynchronize(R.st), "cudaStreamSynchronize");
-    return PU_OK;
-  };
   int count = 0;
   auto record = [&](int k, int m_cg, bool has_delta, double delta_rel) -> int {
     if (hc->breakdown >= 0) {  // pcg.py:24-29 -> NumericalBreakdown(iteration)
@@ -227,60 +224,85 @@ extern "C" int pu_unwrap(const double* x, int n, int m, const double* cv, const 
     return PU_OK;
   };
 
-  // irls.py:172-222
-  std::vector<int> hist{p.max_iter_cg_start};
+  // irls.py:172-222, as the Python host runs it (irls._LoopJob): iteration k
+  // is finished, its scalars are snapshot asynchronously, and the
+  // budget-free first half of k + 1 (pu_irls_begin: candidate step, PCG
+  // start-up, z0) is enqueued before the host waits for the snapshot.  From
+  // 2048^2 cells the acceptance of k also runs the start-up of k + 1 in the
+  // same pass (pu_accept_weights_start; then pu_irls_begin_z0).
+  const bool fused = (long long)n * m >= 2048LL * 2048LL;  // irls._fuse_start on a single unwrap
+  cudaEvent_t snap = nullptr;
+  PU_CK(cudaEventCreateWithFlags(&snap, cudaEventDisableTiming), "cudaEventCreate");
+  struct EvGuard { cudaEvent_t e; ~EvGuard() { if (e) cudaEventDestroy(e); } } evg{snap};
   int cur = 0;
-  int pend_k = -1, pend_m = 0;
-  bool pend_has = false;
-  double pend_delta = 0.0;
-  for (int k = 0; k < p.max_outer_iters; ++k) {
-    int m_cg = hist[0];
-    bool has_delta = false;
-    double delta_rel = 0.0;
-    if (k >= 1) {
-      PU_OK_OR(read_block());
-      PU_OK_OR(record(pend_k, pend_m, pend_has, pend_delta));
-      pend_k = -1;
-      // H(state_k, w_{k-1}) is the accepted value of k-1; H(state_k, w_k) its refresh
-      const double h_old = hs[S_HACC], h_new = hs[S_HNEXT];
-      if (h_old == 0.0) {
-        delta_rel = 0.0;
-      } else {
-        if (!(h_old > 0)) return bad("reference objective value must be positive");  // irls.py:111-115
-        delta_rel = (h_old - h_new) / h_old;
-      }
-      has_delta = true;
-      const int m_prev = hist[k - 1];
-      const int m_prev2 = k >= 2 ? hist[k - 2] : m_prev;
-      // irls.py:118-129: keep while improving, stop after a fruitless grow, else grow
-      if (delta_rel > p.rel_improvement_tol) {
-        m_cg = m_prev;
-      } else if (m_prev != m_prev2 || m_prev >= p.max_cg_iters_cap) {
-        break;
-      } else {
-        m_cg = (int)std::min<double>(std::ceil(p.cg_growth_factor * m_prev), (double)p.max_cg_iters_cap);
-      }
-      hist.push_back(m_cg);
+  bool prestarted = false;
+  auto begin = [&](int k) -> int {
+    char* w = W[k & 1];
+    if (prestarted) {
+      prestarted = false;
+      return pu_irls_begin_z0(R.h, dv, dh, p.cg_rel_tol, r, p0, p1, spec, ctrl, norms, R.st);
     }
-    void* st_cur = S[cur];
-    void* st_nxt = S[1 - cur];
+    return pu_irls_begin(R.h, S[cur], b, gv, gh, cvp, chp, w, w + plane, dv, dh, lip, p.cg_rel_tol, Cs[k & 1], r, p0,
+                         p1, spec, ctrl, norms, R.st);
+  };
+  auto finish = [&](int k, int m_cg) -> int {
     char* w = W[k & 1];
     char* wn = W[(k + 1) & 1];
-    PU_OK_OR(pu_irls_begin(R.h, st_cur, b, gv, gh, cvp, chp, w, w + plane, dv, dh, lip, p.cg_rel_tol, cand, r, p0, p1,
-                           spec, ctrl, norms, R.st));
-    PU_OK_OR(pu_irls_iterate(R.h, st_cur, gv, gh, cvp, chp, w, w + plane, dv, dh, m_cg, cand, r, p0, p1, spec, ctrl,
-                             norms, blk + S_HPROP, R.st));
-    PU_OK_OR(pu_accept_weights(R.h, st_cur, cand, blk + S_MEAN, st_nxt, gv, gh, cvp, chp, w, w + plane, wn,
-                               wn + plane, dv, dh, blk + S_HACC, R.st));
+    PU_OK_OR(pu_irls_iterate(R.h, S[cur], gv, gh, cvp, chp, w, w + plane, dv, dh, m_cg, Cs[k & 1], r, p0, p1, spec,
+                             ctrl, norms, blk + S_HPROP, R.st));
+    if (fused && k + 1 < p.max_outer_iters) {
+      PU_OK_OR(pu_accept_weights_start(R.h, S[cur], Cs[k & 1], blk + S_MEAN, S[1 - cur], gv, gh, cvp, chp, w,
+                                       w + plane, wn, wn + plane, dv, dh, blk + S_HACC, lip, r, Cs[(k + 1) & 1],
+                                       R.st));
+      prestarted = true;
+    } else {
+      PU_OK_OR(pu_accept_weights(R.h, S[cur], Cs[k & 1], blk + S_MEAN, S[1 - cur], gv, gh, cvp, chp, w, w + plane,
+                                 wn, wn + plane, dv, dh, blk + S_HACC, R.st));
+    }
     cur = 1 - cur;
+    return PU_OK;
+  };
+  auto enqueue = [&](int k, int m_cg) -> int {
+    if (k == 0) PU_OK_OR(begin(0));
+    PU_OK_OR(finish(k, m_cg));
+    PU_CK(cudaMemcpyAsync(R.pin, blk, NSCAL * 8 + ctrl_bytes, cudaMemcpyDeviceToHost, R.st), "snapshot");
+    PU_CK(cudaEventRecord(snap, R.st), "cudaEventRecord");
+    if (k + 1 < p.max_outer_iters) PU_OK_OR(begin(k + 1));  // speculative: needs no budget
+    return PU_OK;
+  };
+  std::vector<int> hist{p.max_iter_cg_start};
+  PU_OK_OR(enqueue(0, hist[0]));
+  int pend_k = 0, pend_m = hist[0];
+  bool pend_has = false;
+  double pend_delta = 0.0;
+  for (int k = 1;; ++k) {
+    PU_CK(cudaEventSynchronize(snap), "cudaEventSynchronize");
+    PU_OK_OR(record(pend_k, pend_m, pend_has, pend_delta));
+    if (k >= p.max_outer_iters) break;
+    // H(state_k, w_{k-1}) is the accepted value of k-1; H(state_k, w_k) its refresh
+    const double h_old = hs[S_HACC], h_new = hs[S_HNEXT];
+    double delta_rel = 0.0;
+    if (h_old != 0.0) {
+      if (!(h_old > 0)) return bad("reference objective value must be positive");  // irls.py:111-115
+      delta_rel = (h_old - h_new) / h_old;
+    }
+    const int m_prev = hist[k - 1];
+    const int m_prev2 = k >= 2 ? hist[k - 2] : m_prev;
+    int m_cg;
+    // irls.py:118-129: keep while improving, stop after a fruitless grow, else grow
+    if (delta_rel > p.rel_improvement_tol) {
+      m_cg = m_prev;
+    } else if (m_prev != m_prev2 || m_prev >= p.max_cg_iters_cap) {
+      break;
+    } else {
+      m_cg = (int)std::min<double>(std::ceil(p.cg_growth_factor * m_prev), (double)p.max_cg_iters_cap);
+    }
+    hist.push_back(m_cg);
+    PU_OK_OR(enqueue(k, m_cg));
     pend_k = k;
     pend_m = m_cg;
-    pend_has = has_delta;
+    pend_has = true;
     pend_delta = delta_rel;
-  }
-  if (pend_k >= 0) {
-    PU_OK_OR(read_block());
-    PU_OK_OR(record(pend_k, pend_m, pend_has, pend_delta));
   }
   if (trace_len) *trace_len = count;
 
