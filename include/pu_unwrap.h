@@ -380,6 +380,24 @@ int pu_unwrap(const double* x, int n, int m, const double* cv, const double* ch,
               const pu_irls_params* params, double gradient_lo, int dtype, int device, double* u, double* vv,
               double* vh, pu_iteration_record* trace, int trace_cap, int* trace_len, int* breakdown_iteration);
 
+/* ------------------------------------------------------------------------
+ * GPU synthetic scenes (reference synth.py:43-109):
+ * the per-pixel work of the reference's scene recipes, for large benchmark
+ * inputs.  Parameters (bump centres/widths/peaks, fault seam) are drawn on
+ * the host from the reference's Philox stream (synth_gpu.py).  Plateau,
+ * fault mask and wrapping are exact; bumps agree with the host generator to
+ * ~1e-15 (device exp); the phase noise is a device Philox-4x32 / Box-Muller
+ * stream (statistically equivalent, not numpy's realisation).  Device fp64
+ * arrays, row pitch ld.
+ * ------------------------------------------------------------------------ */
+/* out = sum_b params[4b+3] exp(-((i - params[4b])^2 + (j - params[4b+1])^2) / (2 params[4b+2]^2)) */
+int pu_synth_bumps(double* out, int rows, int cols, int64_t ld, const double* params, int count, void* stream);
+/* out += lin[i] * amplitude * (j >= seam[i])  (plateau-discontinuity, tapered fault) */
+int pu_synth_fault(double* out, int rows, int cols, int64_t ld, const int64_t* seam, const double* lin,
+                   double amplitude, void* stream);
+/* x = wrap_to_principal(x + sigma * N(0,1), 0) (sigma = 0: wrap only) */
+int pu_synth_wrap_noise(double* x, int rows, int cols, int64_t ld, double sigma, uint64_t seed, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -92,6 +92,10 @@ SIGNATURES = {
     "pu_pcg_columns": (_i, [_vp, _vp, _vp, _i, _vp]),
     "pu_pcg_rows_inv": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _vp]),
     "pu_pcg_direction": (_i, [_vp] + [_vp] * 6 + [_i, _vp]),
+    # GPU synthetic scenes (pu_synth.cu)
+    "pu_synth_bumps": (_i, [_vp, _i, _i, _i64, _vp, _i, _vp]),
+    "pu_synth_fault": (_i, [_vp, _i, _i, _i64, _vp, _vp, _d, _vp]),
+    "pu_synth_wrap_noise": (_i, [_vp, _i, _i, _i64, _d, ctypes.c_uint64, _vp]),
     # the whole unwrap behind one call (pu_host.cu)
     "pu_irls_params_default": (None, [ctypes.POINTER(PuIrlsParams)]),
     "pu_unwrap": (_i, [_vp, _i, _i, _vp, _vp, _d, _d, ctypes.POINTER(PuIrlsParams), _d, _i, _i, _vp, _vp, _vp,

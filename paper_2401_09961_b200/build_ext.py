@@ -104,7 +104,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
         return LIB
     os.makedirs(OBJDIR, exist_ok=True)
     work = [(os.path.join(CSRC, "pu_api.cu"), os.path.join(OBJDIR, "pu_api.o"), []),
-            (os.path.join(CSRC, "pu_host.cu"), os.path.join(OBJDIR, "pu_host.o"), [])]
+            (os.path.join(CSRC, "pu_host.cu"), os.path.join(OBJDIR, "pu_host.o"), []),
+            (os.path.join(CSRC, "pu_synth.cu"), os.path.join(OBJDIR, "pu_synth.o"), [])]
     for t, ls in INSTANCES:
         work.append((os.path.join(CSRC, "pu_dct_inst.cu"), os.path.join(OBJDIR, f"pu_dct_{t}_{ls}.o"),
                      [f"-DPU_INST_T={t}", f"-DPU_INST_LS={ls}"]))
