@@ -414,8 +414,9 @@ struct Impl : HandleBase {
     }
     int rc;
     if ((rc = prow.build(m)) || (rc = pcol.build(n_glob))) return rc;
-    row_split = !prow.dev.bluestein && prow.dev.L == 2 * LHS && std::getenv("PU_NO_SPLIT") == nullptr;
-    col_split = !pcol.dev.bluestein && pcol.dev.L == 2 * LHS && std::getenv("PU_NO_SPLIT") == nullptr;
+    // (Bluestein plans: internal length L = 2 LHS, i.e. non-smooth n in (LHS/2, LHS])
+    row_split = prow.dev.L == 2 * LHS && std::getenv("PU_NO_SPLIT") == nullptr;
+    col_split = pcol.dev.L == 2 * LHS && std::getenv("PU_NO_SPLIT") == nullptr;
     if (row_split && (rc = prow_h.build(LHS))) return rc;
     if (col_split && (rc = pcol_h.build(LHS))) return rc;
     // row kernels (k_rows_pipe): one row pair per CTA, whole sequence in one group

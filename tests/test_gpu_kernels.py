@@ -123,6 +123,21 @@ def test_sylvester_cluster_split(rng, shape, dtypes):
         assert rel(got, want) <= (1e-11 if dt == "fp64" else 5e-5), dt
 
 
+@pytest.mark.parametrize("shape,dtypes", [((3, 4099), ("fp64",)), ((4099, 4), ("fp64",)), ((4099, 5), ("fp64",)),
+                                          ((6001, 3), ("fp64",)), ((2, 8191), ("fp64",)),
+                                          ((3, 8209), ("fp32",)), ((8209, 4), ("fp32",)), ((2, 16381), ("fp32",))])
+def test_sylvester_cluster_split_bluestein(rng, shape, dtypes):
+    """Non-smooth lengths past half the one-CTA limit (fp64 4097..8192,
+    fp32 8193..16384): Bluestein on the internal length 2 LH, split over the
+    2-CTA cluster (pu_split.cuh split_bluestein)."""
+    n, m = shape
+    r = rng.standard_normal((n, m))
+    want = port.DctPoisson(n, m)(r, 1e-2)
+    for dt in dtypes:
+        got = pu.sylvester_solve(r, 1e-2, dtype=dt)
+        assert rel(got, want) <= (1e-10 if dt == "fp64" else 1e-4), dt
+
+
 def test_fp64_long_axis_unwrap_matches_oracle():
     """End-to-end fp64 unwrap on a grid with a 16384-long axis (cluster-split
     row transforms) against the oracle with the exact DCT preconditioner."""
