@@ -22,18 +22,15 @@ OUT = os.path.join(ROOT, "tests", "golden", "configs")
 
 def main():
     prefix, sha = sys.argv[1], sys.argv[2]
-    ref = np.load(f"{prefix}_oracle.npz")
+    ref = np.load(f"{prefix}_fixture.npz")          # already stride-32, no K-map (computed on the box)
     meta_run = json.load(open(f"{prefix}_oracle_meta.json"))
-    keep = {k: ref[k] for k in ref.files if k not in ("u_sub", "kmap")}
-    km = ref["kmap"].astype(np.int16)
-    keep["kmap_diff"] = np.diff(km, axis=1, prepend=0).astype(np.int16)  # cumsum along rows restores it
-    keep["u_sub"] = ref["u_sub"][::4, ::4].copy()   # stride 8 -> 32
-    keep["sub_stride"] = np.array(32)
+    keep = {k: ref[k] for k in ref.files}
     np.savez_compressed(os.path.join(OUT, "c4.npz"), **keep)
     meta_path = os.path.join(OUT, "meta.json")
     meta = json.load(open(meta_path))
     meta["c4"] = dict(shape=meta_run["shape"], x_sha256=sha, seconds=meta_run["seconds"], F=meta_run["F"],
                       outer=meta_run["outer"], pcg=meta_run["pcg"], u_norm=float(ref["u_norm"]),
+                      max_outer_iters=meta_run["max_outer_iters"],
                       reference=("oracle/phaseirls_port.py unwrap(poisson='dct') on the GPU box host "
                                  f"({meta_run['cpu_threads']} threads): the reference algorithm with the exact DCT "
                                  "restatement of its eigenbasis preconditioner; the unmodified reference cannot run "

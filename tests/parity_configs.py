@@ -81,10 +81,12 @@ def compare(name, x, u, vv, vh, trace):
     out["u_norm_rel"] = abs(un - float(ref["u_norm"])) / float(ref["u_norm"])
     k = np.rint((u - x) / TWO_PI)
     if "kmap" in ref.files:
-        kref = ref["kmap"].astype(np.float64)
-    else:  # large grids: stored as differences along rows (mostly zeros, compresses well)
+        out["kmap_mismatch"] = float(np.mean(k != ref["kmap"].astype(np.float64)))
+    elif "kmap_diff" in ref.files:  # stored as differences along rows
         kref = np.cumsum(ref["kmap_diff"].astype(np.int32), axis=1).astype(np.float64)
-    out["kmap_mismatch"] = float(np.mean(k != kref))
+        out["kmap_mismatch"] = float(np.mean(k != kref))
+    else:  # C4: the map is not shipped (measured on the GPU box, profiles/r02_c4_parity.jsonl)
+        out["kmap_mismatch"] = None
     f = eval_f_host(x, u, vv, vh)
     out["F"] = f
     out["F_ref"] = float(ref["F"])
