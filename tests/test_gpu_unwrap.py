@@ -124,7 +124,9 @@ def test_monotone_descent_and_safeguard():
 
 def test_unwrap_many_matches_sequential():
     """Concurrent unwraps (one workspace + stream each, host round-robin) give
-    exactly the results of one-at-a-time unwraps."""
+    the results of one-at-a-time unwraps: bitwise in fp32; in fp64 to
+    round-off, because concurrent unwraps use the fused acceptance + start-up
+    (its fp64 1-CTA/SM build contracts FMAs differently in the last bits)."""
     xs = [pu.add_phase_noise(pu.wrap_scene(pu.generate_scene(pu.SceneSpec("gaussian-bumps", 40, 36, 8.0, 5.0, s))),
                              0.6, 50 + s) for s in range(5)]
     for dtype in ("fp64", "fp32"):
@@ -132,8 +134,11 @@ def test_unwrap_many_matches_sequential():
         many = pu.unwrap_many(xs, dtype=dtype, concurrency=3)
         for a, b in zip(seq, many):
             assert [r.cg_iters for r in a.trace.records] == [r.cg_iters for r in b.trace.records]
-            np.testing.assert_array_equal(a.u, b.u)
-            np.testing.assert_array_equal(a.vh, b.vh)
+            if dtype == "fp32":
+                np.testing.assert_array_equal(a.u, b.u)
+                np.testing.assert_array_equal(a.vh, b.vh)
+            else:
+                assert rel(a.u, b.u) <= 1e-12 and rel(a.vh, b.vh) <= 1e-11
 
 
 @pytest.mark.parametrize("shape", [(257, 385), (1000, 3), (3, 1000), (513, 1023), (127, 2048)])
