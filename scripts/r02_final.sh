@@ -1,6 +1,8 @@
 #!/bin/bash
 # round-2 final measurements: the driver's default bench line, the reference arm, every BASELINE config
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
+PU_PARITY_REPORT=gpurun_out/fin_parity.jsonl timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/fin_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/fin_pytest.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/fin_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/fin_smoke.log
 timeout 1200 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/fin_default.json 2> gpurun_out/fin_default.err
 for cfg in c1 c2; do
   timeout 900 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/fin_$cfg.json 2> gpurun_out/fin_$cfg.err
