@@ -138,7 +138,9 @@ def test_unwrap_many_matches_sequential():
                 np.testing.assert_array_equal(a.u, b.u)
                 np.testing.assert_array_equal(a.vh, b.vh)
             else:
-                assert rel(a.u, b.u) <= 1e-12 and rel(a.vh, b.vh) <= 1e-11
+                for f in ("u", "vv", "vh"):  # (slacks of a residue-free scene are ~1e-17: absolute floor)
+                    ga, gb = getattr(a, f), getattr(b, f)
+                    assert rel(ga, gb) <= 1e-12 or np.max(np.abs(ga - gb)) <= 1e-13, f
 
 
 @pytest.mark.parametrize("shape", [(257, 385), (1000, 3), (3, 1000), (513, 1023), (127, 2048)])
