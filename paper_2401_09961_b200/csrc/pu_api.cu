@@ -347,6 +347,11 @@ struct Impl : HandleBase {
   static constexpr int LHS = sizeof(T) == 4 ? 16384 : 8192;
   bool row_split = false, col_split = false;
   HostPlan<T> prow_h, pcol_h;
+  // programmatic dependent launch of the PCG-iteration kernels (PU_PDL=1/2;
+  // g.pdl / gc.pdl carry the mode into the kernels); pdl_now is set while
+  // pcg_iterate enqueues
+  int pdl_mode = 0;
+  bool pdl_now = false;
   int cols_per_cta = 2, col_threads = 64;
   int col_nfull = 1 << 30, col_nhalf = 0;  // balanced column grid: full panels, then half panels
   size_t col_smem = 0;
@@ -405,6 +410,12 @@ struct Impl : HandleBase {
       const double grow = 16.0 * (double)n_glob * (double)m * (std::isfinite(lam_min) ? tau / lam_min + 1.0 : 1.0);
       g.tail_rn2_max = tmax / grow;
     }
+    if (!band) {
+      const char* e = std::getenv("PU_PDL");
+      pdl_mode = e ? std::atoi(e) : 0;
+      if (pdl_mode < 0 || pdl_mode > 2) pdl_mode = 0;
+    }
+    g.pdl = pdl_mode;
     gc = g;
     if (band) {
       gc.n = n_glob; gc.m = b->cols; gc.ld = b->mb; gc.plane = (long long)n_glob * b->mb;
@@ -524,8 +535,8 @@ struct Impl : HandleBase {
                      col_nfull);
   }
 
-  XLaunch cl(cudaStream_t st) const { return XLaunch{col_grid(), col_threads, col_smem, st}; }
-  XLaunch pl_(cudaStream_t st) const { return XLaunch{pipe_grid, pipe_threads, pipe_smem, st}; }
+  XLaunch cl(cudaStream_t st) const { return XLaunch{col_grid(), col_threads, col_smem, st, pdl_now}; }
+  XLaunch pl_(cudaStream_t st) const { return XLaunch{pipe_grid, pipe_threads, pipe_smem, st, pdl_now}; }
 
   int col_grid() const { return col_nhalf ? col_nfull + col_nhalf : (gc.m + cols_per_cta - 1) / cols_per_cta; }
 
@@ -591,6 +602,10 @@ struct Impl : HandleBase {
   int pcg_iterate(T* x, const T* dv, const T* dh, T* r, T* p0, T* p1, T* spec, int max_iters, PcgCtrl* ctrl,
                   double* norms, cudaStream_t st) {
     const int vg = vec_grid();
+    // PDL only without per-launch timing events (an event between two
+    // kernels breaks the programmatic edge)
+    const bool pdl = pdl_mode > 0 && !tm.on;
+    struct PdlScope { bool& f; PdlScope(bool& f_, bool v) : f(f_) { f = v; } ~PdlScope() { f = false; } } scope(pdl_now, pdl);
     cudaEvent_t e;
     T* pbuf[2] = {p0, p1};
     const int chunk = 64;
@@ -603,8 +618,7 @@ struct Impl : HandleBase {
       T* pn = pbuf[it & 1];
       const T* po = pbuf[(it + 1) & 1];
       e = tm.begin(st);
-      k_pcg_p_v<T><<<vg, 256, 0, st>>>(g, r, po, pn, dv, dh, ctrl, rs, S_K1, it);
-      PU_LAUNCH_CHECK();
+      PU_DCT(launch_k(k_pcg_p_v<T>, vg, 256, 0, st, pdl, g, r, po, pn, dv, dh, ctrl, rs, (int)S_K1, it));
       tm.end(st, e, TK_K1, it);
       if ((it + 1) % 50 == 0) {
         e = tm.begin(st);
@@ -617,8 +631,8 @@ struct Impl : HandleBase {
         tm.end(st, e, TK_K2, it);
       } else {
         e = tm.begin(st);
-        k_pcg_r_v<T, true, false, MODE_ITER><<<vg, 256, 0, st>>>(g, pn, dv, dh, x, r, ctrl, norms, rs, S_K2, it);
-        PU_LAUNCH_CHECK();
+        PU_DCT(launch_k(k_pcg_r_v<T, true, false, MODE_ITER>, vg, 256, 0, st, pdl, g, (const T*)pn, dv, dh, x, r,
+                        ctrl, norms, rs, (int)S_K2, it));
         tm.end(st, e, TK_K2, it);
       }
       e = tm.begin(st);

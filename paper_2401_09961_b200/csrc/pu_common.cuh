@@ -66,7 +66,20 @@ struct Grid {
   // largest ||r||^2 for which the preconditioned product r.z of the PCG tail
   // is provably finite in T (see fin_k2); set by the host
   double tail_rn2_max;
+  // programmatic dependent launch of the PCG-iteration kernels (PU_PDL):
+  // 0 off, 1 wait at entry, 2 wait at entry + trigger the next launch before
+  // the kernel's tail (reduction / final stores)
+  int pdl;
 };
+
+// griddepcontrol: no-ops unless the kernel was launched with the
+// programmatic-stream-serialization attribute
+__device__ __forceinline__ void pdl_enter(const Grid& g) {
+  if (g.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger(const Grid& g) {
+  if (g.pdl == 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // vertical neighbours of row i within the global grid (ghost rows count)
 __host__ __device__ __forceinline__ bool dn_ok(const Grid& g, int i) { return i < g.n - 1 || g.bot; }

@@ -5,6 +5,8 @@
 // for every other length.
 #pragma once
 
+#include <utility>
+
 #include "pu_pipe.cuh"
 
 namespace pu {
@@ -14,7 +16,28 @@ struct XLaunch {
   int threads;
   size_t smem;
   cudaStream_t st;
+  bool pdl = false;  // programmatic dependent launch (Grid::pdl)
 };
+
+// <<<grid, block, smem, st>>>, or with the programmatic-stream-serialization
+// attribute: the kernel may be scheduled while the previous one in the stream
+// drains, and waits for it in griddepcontrol.wait (pdl_enter)
+template <typename... P, typename... A>
+cudaError_t launch_k(void (*kernel)(P...), int grid, int block, size_t smem, cudaStream_t st, bool pdl, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  if (pdl) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+}
 
 template <typename T, int LS>
 struct DctLaunch {
@@ -52,11 +75,11 @@ template <typename T, int LS>
 cudaError_t DctLaunch<T, LS>::rows_pipe(bool inv, const XLaunch& c, const Grid& g, const FftPlan<T>& pl, const T* in,
                                         T* out, const PcgCtrl* ctrl, const T* pold, int first, Pack pk) {
   const size_t smem = rows_fused(pl) ? rows_fused_smem(c.smem, sizeof(T), pl.ldseq) : c.smem;
-  if (inv)
-    k_rows_pipe<T, EM, LS, true><<<c.grid, c.threads, smem, c.st>>>(g, pl, in, out, ctrl, pold, first, pk);
-  else
-    k_rows_pipe<T, EM, LS, false><<<c.grid, c.threads, smem, c.st>>>(g, pl, in, out, ctrl, nullptr, 0, pk);
-  return cudaGetLastError();
+  const PcgCtrl* cc = ctrl;
+  const T* po = inv ? pold : nullptr;
+  const int fi = inv ? first : 0;
+  if (inv) return launch_k(k_rows_pipe<T, EM, LS, true>, c.grid, c.threads, smem, c.st, c.pdl, g, pl, in, out, cc, po, fi, pk);
+  return launch_k(k_rows_pipe<T, EM, LS, false>, c.grid, c.threads, smem, c.st, c.pdl, g, pl, in, out, cc, po, fi, pk);
 }
 
 template <typename T, int LS>
@@ -89,7 +112,8 @@ cudaError_t DctLaunch<T, LS>::cols(int mode, const XLaunch& c, const Grid& g, co
   else if (mode == MODE_INIT)
     k_cols_spec<T, EM, LS, MODE_INIT><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it, ps, nfull);
   else
-    k_cols_spec<T, EM, LS, MODE_ITER><<<c.grid, c.threads, c.smem, c.st>>>(g, pl, lam_cols, cpc, data, ctrl, rs, site, it, ps, nfull);
+    return launch_k(k_cols_spec<T, EM, LS, MODE_ITER>, c.grid, c.threads, c.smem, c.st, c.pdl, g, pl, lam_cols, cpc,
+                    data, ctrl, rs, site, it, ps, nfull);
   return cudaGetLastError();
 }
 #endif  // PU_DCT_DEFINE

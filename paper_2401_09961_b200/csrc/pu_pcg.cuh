@@ -347,8 +347,10 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_
                             PcgCtrl* ctrl, RedScratch rs, int site, int it, Push ps, int nfull) {
   extern __shared__ __align__(16) unsigned char smraw[];
   cplx<T>* buf = reinterpret_cast<cplx<T>*>(smraw);
+  pdl_enter(g);
   if (MODE != MODE_API && ctrl->done) return;
   const T accT = cols_panel<T, EMAX, LS>(g, pl, lam_cols, cols_per_cta, data, ps, nfull, (int)blockIdx.x, buf);
+  pdl_trigger(g);
   if (MODE != MODE_API) {
     double acc[1] = {(double)accT};
     double tot[1];

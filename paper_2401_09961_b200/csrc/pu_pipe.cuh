@@ -396,6 +396,7 @@ __global__ void __launch_bounds__(fft_max_threads(LS, EMAX, sizeof(T)), fft_min_
     k_rows_pipe(Grid g, FftPlan<T> pl, const T* __restrict__ in, T* __restrict__ out, const PcgCtrl* ctrl,
                 const T* __restrict__ pold, int first, Pack pk) {
   extern __shared__ __align__(128) unsigned char smraw[];
+  pdl_enter(g);
   if (ctrl && ctrl->done) return;
   if (threadIdx.x == 0) {
     mbar_init(reinterpret_cast<uint64_t*>(smraw), 1);

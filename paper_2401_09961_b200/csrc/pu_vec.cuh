@@ -132,6 +132,7 @@ template <typename T>
 __device__ __forceinline__ void pcg_p_body(const Grid& g, const T* __restrict__ r, const T* __restrict__ pold,
                                            T* __restrict__ pnew, const T* __restrict__ dv, const T* __restrict__ dh,
                                            PcgCtrl* ctrl, const RedScratch& rs, int site, int it) {
+  pdl_enter(g);
   if (ctrl->done) return;
   const bool first = it == 0;
   const T beta = (T)ctrl->beta;
@@ -168,6 +169,7 @@ __device__ __forceinline__ void pcg_p_body(const Grid& g, const T* __restrict__ 
     }
     acc[0] += (double)part;
   }
+  pdl_trigger(g);
   double tot[1];
   if (red_final<1>(acc, rs, site, tot) && threadIdx.x == 0) fin_k1(ctrl, tot, it);
 }
@@ -189,6 +191,7 @@ template <typename T, bool UPDATE, bool SUBMEAN, int MODE>
 __device__ __forceinline__ void pcg_r_body(const Grid& g, const T* __restrict__ p, const T* __restrict__ dv,
                                            const T* __restrict__ dh, T* __restrict__ x, T* __restrict__ r,
                                            PcgCtrl* ctrl, double* res_norms, const RedScratch& rs, int site, int it) {
+  pdl_enter(g);
   if (ctrl->done) return;
   const long long P = g.plane, ld = g.ld;
   const T alpha = (T)ctrl->alpha, nalpha = (T)(-ctrl->alpha);
@@ -246,6 +249,7 @@ __device__ __forceinline__ void pcg_r_body(const Grid& g, const T* __restrict__ 
     acc[0] += (double)prr;  // chunk partials in T, grid sums in fp64
     acc[1] += (double)prz;
   }
+  pdl_trigger(g);
   double tot[2];
   if (red_final<2>(acc, rs, site, tot) && threadIdx.x == 0) fin_k2(g, ctrl, res_norms, tot, it, MODE);
 }
@@ -263,6 +267,7 @@ template <typename T>
 __device__ __forceinline__ void pcg_upd_sum_body(const Grid& g, const T* __restrict__ p, const T* __restrict__ dv,
                                                  const T* __restrict__ dh, T* __restrict__ x, T* __restrict__ r,
                                                  PcgCtrl* ctrl, const RedScratch& rs, int site) {
+  pdl_enter(g);
   if (ctrl->done) return;
   const long long P = g.plane, ld = g.ld;
   const T alpha = (T)ctrl->alpha, nalpha = (T)(-ctrl->alpha);
