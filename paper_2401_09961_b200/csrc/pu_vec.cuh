@@ -78,7 +78,12 @@ __device__ __forceinline__ void apply4(const Grid& g, int i, int j0, const Stenc
 // fast division in fp32 mode (K1 and K2a use the same expression, so rho and
 // p stay consistent), IEEE division in fp64 mode (parity with the reference)
 __device__ __forceinline__ float slack_div(float a, float b) { return a * rcp_approx(b); }
+#ifdef PU_F64_SLACK_RCP
+// reciprocal seed + two Newton steps (<= 1 ulp) instead of the IEEE division
+__device__ __forceinline__ double slack_div(double a, double b) { return a * rcp_nr(b); }
+#else
 __device__ __forceinline__ double slack_div(double a, double b) { return a / b; }
+#endif
 
 // scalar neighbour load that tolerates the grid edge
 template <typename T>
