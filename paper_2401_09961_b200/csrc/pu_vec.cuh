@@ -78,12 +78,14 @@ __device__ __forceinline__ void apply4(const Grid& g, int i, int j0, const Stenc
 // fast division in fp32 mode (K1 and K2a use the same expression, so rho and
 // p stay consistent), IEEE division in fp64 mode (parity with the reference)
 __device__ __forceinline__ float slack_div(float a, float b) { return a * rcp_approx(b); }
-#ifdef PU_F64_SLACK_RCP
-// reciprocal seed + two Newton steps (<= 1 ulp) instead of the IEEE division
-__device__ __forceinline__ double slack_div(double a, double b) { return a * rcp_nr(b); }
-#else
 __device__ __forceinline__ double slack_div(double a, double b) { return a / b; }
-#endif
+// K1's slack preconditioner and the H-pair slack terms in fp64: reciprocal
+// seed + two Newton steps (<= 1 ulp) instead of the IEEE division.  Measured
+// (profiles/r02_ab_f64div.txt): K1 214 -> 186.5 us (the kernel then streams
+// at the HBM peak); in K2a the same change was 3% slower, so K2a keeps the
+// IEEE division for rho_s (the two z_s differ by at most 1 ulp).
+__device__ __forceinline__ float slack_div_p(float a, float b) { return slack_div(a, b); }
+__device__ __forceinline__ double slack_div_p(double a, double b) { return a * rcp_nr(b); }
 
 // scalar neighbour load that tolerates the grid edge
 template <typename T>
@@ -102,7 +104,7 @@ __device__ __forceinline__ Q4<T> pslack4(const Grid& g, const T* __restrict__ r,
   for (int k = 0; k < 4; ++k) {
     const int j = j0 + k;
     const bool ok = vert ? (dn_ok(g, i) && j < g.m) : (j < g.m - 1);
-    out.a[k] = ok ? slack_div(rr.a[k], dd.a[k] + inv) : (T)0;
+    out.a[k] = ok ? slack_div_p(rr.a[k], dd.a[k] + inv) : (T)0;
   }
   if (!first) {
     const Q4<T> pp = ldg4(pold + o + po);
@@ -476,7 +478,7 @@ __device__ __forceinline__ void pen4(const Grid& g, int i, int j0, const Q4<T>& 
 template <typename T>
 __device__ __forceinline__ T slack4(T c, T v, T w, T d2) {
   const T cv = c * v;
-  return slack_div(cv * cv + d2, w) + w;
+  return slack_div_p(cv * cv + d2, w) + w;
 }
 
 // w = sqrt((c v)^2 + delta^2), d = c^2 / w; H(x, w_prev), H(x, w)
