@@ -87,24 +87,6 @@ __device__ __forceinline__ double slack_div(double a, double b) { return a / b; 
 __device__ __forceinline__ float slack_div_p(float a, float b) { return slack_div(a, b); }
 __device__ __forceinline__ double slack_div_p(double a, double b) { return a * rcp_nr(b); }
 
-// IRLS weight w = sqrt(x) and d = c^2 / w (objective.py:92-100, irls.py:191).
-// fp32: IEEE sqrt and division (unchanged).  fp64: one reciprocal square root
-// seed + two Newton steps gives 1/w; w = x / sqrt(x) = x * (1/w) and d =
-// c^2 * (1/w), so the fused acceptance computes no sqrt and no division
-// (each within ~1 ulp of the IEEE results).
-__device__ __forceinline__ void weight_d(float x, float c, float& w, float& d) {
-  w = sqrtf(x);
-  d = c * c / w;
-}
-__device__ __forceinline__ void weight_d(double x, double c, double& w, double& d) {
-  double r;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  r = r * fma(-0.5 * x, r * r, 1.5);
-  r = r * fma(-0.5 * x, r * r, 1.5);
-  w = x * r;
-  d = c * c * r;
-}
-
 // scalar neighbour load that tolerates the grid edge
 template <typename T>
 __device__ __forceinline__ T ldg_or0(const T* p, bool ok) { return ok ? __ldg(p) : (T)0; }
@@ -528,13 +510,11 @@ __global__ void __launch_bounds__(256, PU_MINB_OUTER(T, 3)) k_weights_hpair_v(Gr
       const int j = j0 + k;
       const bool okv = dn_ok(g, i) && j < g.m, okh = j < g.m - 1;
       const T a = c1.a[k] * vv.a[k], b = c2.a[k] * vh.a[k];
-      T wa, wb, ea, eb;
-      weight_d(a * a + d2, c1.a[k], wa, ea);
-      weight_d(b * b + d2, c2.a[k], wb, eb);
+      const T wa = sqrt(a * a + d2), wb = sqrt(b * b + d2);
       w1.a[k] = okv ? wa : (T)1;
       w2.a[k] = okh ? wb : (T)1;
-      e1.a[k] = okv ? ea : (T)0;
-      e2.a[k] = okh ? eb : (T)0;
+      e1.a[k] = okv ? c1.a[k] * c1.a[k] / wa : (T)0;
+      e2.a[k] = okh ? c2.a[k] * c2.a[k] / wb : (T)0;
       if (okv) {
         part[2] += slack4(c1.a[k], vv.a[k], wa, d2);
         if (hasprev) part[0] += slack4(c1.a[k], vv.a[k], p1.a[k], d2);
@@ -719,13 +699,11 @@ __global__ void __launch_bounds__(256, PU_MINB_OUTER(T, 2)) k_accept_weights_v(G
       u.a[k] = (j < g.m) ? u.a[k] - mean : (T)0;
       ub.a[k] = ub.a[k] - mean;
       const T a = c1.a[k] * vv.a[k], bb = c2.a[k] * vh.a[k];
-      T wa, wb, ea, eb;
-      weight_d(a * a + d2, c1.a[k], wa, ea);
-      weight_d(bb * bb + d2, c2.a[k], wb, eb);
+      const T wa = sqrt(a * a + d2), wb = sqrt(bb * bb + d2);
       w1.a[k] = okv ? wa : (T)1;
       w2.a[k] = okh ? wb : (T)1;
-      e1.a[k] = okv ? ea : (T)0;
-      e2.a[k] = okh ? eb : (T)0;
+      e1.a[k] = okv ? c1.a[k] * c1.a[k] / wa : (T)0;
+      e2.a[k] = okh ? c2.a[k] * c2.a[k] / wb : (T)0;
       if (okv) {
         part[0] += slack4(c1.a[k], vv.a[k], p1.a[k], d2);
         part[2] += slack4(c1.a[k], vv.a[k], wa, d2);
@@ -814,13 +792,11 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) k_accept_start_v(
       const int j = j0 + k;
       const bool okv = hasb && j < g.m, okh = j < g.m - 1;
       const T a = c1.a[k] * s.v.a[k], bb = c2.a[k] * s.h.a[k];
-      T wa, wb, ea, eb;
-      weight_d(a * a + d2, c1.a[k], wa, ea);
-      weight_d(bb * bb + d2, c2.a[k], wb, eb);
+      const T wa = sqrt(a * a + d2), wb = sqrt(bb * bb + d2);
       w1.a[k] = okv ? wa : (T)1;
       w2.a[k] = okh ? wb : (T)1;
-      e1.a[k] = okv ? ea : (T)0;
-      e2.a[k] = okh ? eb : (T)0;
+      e1.a[k] = okv ? c1.a[k] * c1.a[k] / wa : (T)0;
+      e2.a[k] = okh ? c2.a[k] * c2.a[k] / wb : (T)0;
       if (okv) {
         part[0] += slack4(c1.a[k], s.v.a[k], p1.a[k], d2);
         part[2] += slack4(c1.a[k], s.v.a[k], wa, d2);
