@@ -345,8 +345,11 @@ def main():
                     help="N>1: one image row-sharded over the ranks (auto for c1-c4: strong scaling), or "
                          "independent images per rank (auto for c5: weak scaling)")
     ap.add_argument("--concurrency", type=int, default=8, help="c5: images in flight per GPU")
-    ap.add_argument("--peer", action="store_true",
-                    help="--shard rows: transpose fused into the row kernels over peer memory (default: all-to-all)")
+    ap.add_argument("--peer", dest="peer", action="store_true", default=None,
+                    help="--shard rows: transpose fused into the row kernels over peer memory "
+                         "(default: on when the GPUs have peer access, band._default_peer)")
+    ap.add_argument("--no-peer", dest="peer", action="store_false",
+                    help="--shard rows: NCCL all-to-all transposes instead")
     ap.add_argument("--bands", type=int, default=None,
                     help="--shard rows without torchrun: B bands in this process (loopback collectives)")
     ap.add_argument("--warmup-ref", type=int, default=None, help="reference arm (default: --warmup)")
@@ -781,7 +784,7 @@ def main_rows(args, rank, local_rank, world, dev, lib):
                        "sharding": f"one image row-sharded over {world} rank(s): bands {lay.rows}, "
                                    f"transpose blocks of {lay.mb} columns"
                                    + (" (all bands in one process, loopback collectives)" if args.bands else "")
-                                   + (", transpose fused into the row kernels (peer stores/loads)" if args.peer
+                                   + (", transpose fused into the row kernels (peer stores/loads)" if solver.bands[0].peer
                                       else ", NCCL all-to-all transposes"),
                        "l2": "inputs larger than L2", "plan": None},
             "unwrap_s": step_ms / 1e3, "pcg_iters_per_step": n_pcg, "outer_iters_per_step": len(trace.records),

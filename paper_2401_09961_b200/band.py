@@ -185,10 +185,27 @@ class BandState:
         return self.norms
 
     def read_block(self):
-        host = self.block.cpu().numpy()
+        return self._parse(self.block.cpu().numpy())
+
+    def _parse(self, host):
         scal = host[: self.NSCAL * 8].view(np.float64).copy()
-        ctrl = host[self.NSCAL * 8:].view(self._ctrl_dtype)[0]
+        ctrl = host[self.NSCAL * 8:].view(self._ctrl_dtype)[0].copy()
         return scal, ctrl
+
+    def snapshot(self):
+        """Asynchronous copy of the scalar block (end of an outer iteration)
+        into page-locked memory, so work enqueued after it (the speculative
+        start-up of the next iteration) runs while the host reads it."""
+        torch = _torch()
+        if getattr(self, "_snap", None) is None:
+            self._snap = torch.empty(self.block.numel(), dtype=torch.uint8, pin_memory=True)
+            self._snap_ev = torch.cuda.Event()
+        self._snap.copy_(self.block, non_blocking=True)
+        self._snap_ev.record(torch.cuda.current_stream(self.device))
+
+    def read_snapshot(self):
+        self._snap_ev.synchronize()
+        return self._parse(self._snap.numpy())
 
     def pack_rows(self, arr, dst, plane, r0, nrows):
         """Host/device fp64 rows [r0, r0 + nrows) of a compact array -> band rows of dst[plane]."""
@@ -223,6 +240,8 @@ class LoopbackComm:
         self.world = world
 
     def allreduce(self, bands, lo, hi):
+        if len(bands) == 1:  # one band: its totals are the grid's
+            return
         sl = _site_slice(lo, hi)
         tot = bands[0].totals[sl].clone()
         for b in bands[1:]:
@@ -401,40 +420,71 @@ class BandUnwrap:
     # ---- one outer iteration ------------------------------------------------------
     GRAPH_CHUNK = 64  # PCG iterations per captured graph
 
-    def step(self, k, m_cg, params: IrlsParams, lip, poll=16):
-        """irls.py:191-215 for iteration k.
+    def _base(self, k, lip, tol):
+        return (k & 1, self.bands[0].cur, float(lip), float(tol), tuple(b.norms.data_ptr() for b in self.bands),
+                tuple(b.W.data_ptr() if b.use_w else 0 for b in self.bands))
 
-        With graphs (the default): the start-up, z0 and the first 64 PCG
-        iterations replay as one captured CUDA graph (kernels and collectives
-        alike), every further 64 iterations as another, and the H pair +
-        acceptance as a third; the host checks the device exit flag once per
-        64-iteration chunk and only when the budget is longer than that."""
-        if not self.graphs or not self._warm:
-            # the first outer iteration runs eagerly: NCCL creates its
-            # communicators (all-reduce, all-to-all, P2P halo) lazily on first
-            # use, which cannot happen inside a stream capture
-            self._warm = True
-            return self._step(k, m_cg, params, lip, poll)
+    def begin(self, k, lip):
+        """pcg.py:59-79 start-up of iteration k (r0 = b - A x with the
+        candidate step, objective.py:103-125) and the all-reduce of its sums.
+        It depends on neither the budget nor the tolerance, so run_loop
+        enqueues it speculatively behind the previous iteration, before the
+        host has read that iteration's scalars and applied the budget rule; it
+        leaves the state untouched, so a "stop" decision just discards it."""
+        for b in self.bands:
+            b.ensure_norms(self.GRAPH_CHUNK)
+        self._run(("begin",) + self._base(k, lip, 0.0), lambda: self._begin(k, lip))
+
+    def _begin(self, k, lip):
+        P = BandState.p
+        cur = lambda b: b.S[b.cur]  # noqa: E731
+        for b in self.bands:
+            cv, ch = self._c(b)
+            w = b.Wt[k & 1]
+            b.call("pu_pcg_begin", None, P(cur(b)), P(cur(b)), P(b.D, 0), P(b.D, 1), P(b.R), _ptr(b.ctrl),
+                   _ptr(b.norms), 0, 0.0, P(b.G, 0), P(b.G, 1), cv, ch, P(w, 0), P(w, 1), float(lip),
+                   P(b.C), b.stream())
+        self.comm.allreduce(self.bands, nat.SITE_START, nat.SITE_START)
+
+    def step(self, k, m_cg, params: IrlsParams, lip, poll=16):
+        """irls.py:191-215 for iteration k, after begin(k).
+
+        With graphs (the default): the rest of the set-up (z0 = M r0, p0) and
+        the first 64 PCG iterations replay as one captured CUDA graph (kernels
+        and collectives alike), every further 64 iterations as another, and
+        the H pair + acceptance as a third; the host checks the device exit
+        flag once per 64-iteration chunk and only when the budget is longer
+        than that.  Without graphs the host polls every `poll` iterations."""
         for b in self.bands:
             b.ensure_norms(max(m_cg, self.GRAPH_CHUNK))  # stable pointer across budgets
-        base = (k & 1, self.bands[0].cur, float(lip), float(params.cg_rel_tol),
-                tuple(b.norms.data_ptr() for b in self.bands),
-                tuple(b.W.data_ptr() if b.use_w else 0 for b in self.bands))
-        first = min(m_cg, self.GRAPH_CHUNK)
+        base = self._base(k, lip, params.cg_rel_tol)
+        replay = self.graphs and self._warm
+        chunk = self.GRAPH_CHUNK if replay else (poll or m_cg)
+        first = min(m_cg, chunk)
 
         def head():
-            self._head(k, m_cg, params, lip)
+            self._head(k, m_cg, params)
             self._iters(0, first)
 
-        self._replay(("head", m_cg, first) + base, head)
+        self._run(("head", m_cg, first) + base, head)
         it = first
         while it < m_cg:
             if self._done():
                 break
-            nxt = min(m_cg, it + self.GRAPH_CHUNK)
-            self._replay(("iters", it, nxt) + base, lambda a=it, z=nxt: self._iters(a, z))
+            nxt = min(m_cg, it + chunk)
+            self._run(("iters", it, nxt) + base, lambda a=it, z=nxt: self._iters(a, z))
             it = nxt
-        self._replay(("tail",) + base, lambda: self._tail(k), flips=True)
+        self._run(("tail",) + base, lambda: self._tail(k), flips=True)
+        # the first outer iteration runs eagerly: NCCL creates its
+        # communicators (all-reduce, all-to-all, P2P halo) lazily on first
+        # use, which cannot happen inside a stream capture
+        self._warm = True
+
+    def _run(self, key, fn, flips=False):
+        if not (self.graphs and self._warm):
+            fn()  # (eagerly, `fn` flips the states itself)
+            return
+        self._replay(key, fn, flips)
 
     def _replay(self, key, fn, flips=False):
         torch = _torch()
@@ -456,33 +506,14 @@ class BandUnwrap:
             for b in self.bands:
                 b.cur = 1 - b.cur
 
-    def _step(self, k, m_cg, params: IrlsParams, lip, poll=16):
-        """Eager launches (no graphs); the host polls the exit flag every
-        `poll` PCG iterations so a converged budget stops enqueueing."""
-        self._head(k, m_cg, params, lip)
-        it = 0
-        while it < m_cg:
-            nxt = min(m_cg, it + (poll or m_cg))
-            if it > 0 and self._done():
-                break
-            self._iters(it, nxt)
-            it = nxt
-        self._tail(k)
-
-    def _head(self, k, m_cg, params: IrlsParams, lip):
-        """pcg.py:59-79: start-up (+ the candidate step), z0 = M r0, p0 = z0."""
+    def _head(self, k, m_cg, params: IrlsParams):
+        """pcg.py:59-79 after the start-up: the exits on ||r0||, z0 = M r0, p0 = z0."""
         P = BandState.p
         tol = float(params.cg_rel_tol)
-        for b in self.bands:
-            b.ensure_norms(m_cg)
         cur = lambda b: b.S[b.cur]  # noqa: E731
         for b in self.bands:
-            cv, ch = self._c(b)
-            w = b.Wt[k & 1]
-            b.call("pu_pcg_begin", None, P(cur(b)), P(cur(b)), P(b.D, 0), P(b.D, 1), P(b.R), _ptr(b.ctrl),
-                   _ptr(b.norms), int(m_cg), tol, P(b.G, 0), P(b.G, 1), cv, ch, P(w, 0), P(w, 1), float(lip),
-                   P(b.C), b.stream())
-        self._reduce(nat.SITE_START, nat.SITE_START, _mask(nat.SITE_START), 1, -1, rel_tol=tol, max_iters=m_cg)
+            b.call("pu_finalize", _mask(nat.SITE_START), 1, -1, _ptr(b.ctrl), _ptr(b.norms), ctypes.c_void_p(0), tol,
+                   int(m_cg), b.stream())
         for b in self.bands:
             b.call("pu_pcg_residual_rows", None, P(b.D, 0), P(b.D, 1), P(cur(b)), P(b.R), _ptr(b.ctrl),
                    _ptr(b.norms), b.send(), -1, 0, b.stream())
@@ -582,7 +613,9 @@ class BandUnwrap:
 
 
 def run_loop(driver: BandUnwrap, c, model: ModelParams, params: IrlsParams):
-    """The host loop of irls.py:172-222 (same as irls._unwrap_loop) over the band driver."""
+    """The host loop of irls.py:172-222 (same as irls._unwrap_loop) over the
+    band driver: one host synchronisation per outer iteration (the scalar
+    snapshot), with the next iteration's start-up already enqueued behind it."""
     from .irls import _record
     cmax = 1.0 if c is None else c.max_weight
     lip = 12.0 / model.tau + cmax ** 2 / model.delta
@@ -590,10 +623,12 @@ def run_loop(driver: BandUnwrap, c, model: ModelParams, params: IrlsParams):
     m_history = [params.max_iter_cg_start]
     pending = None
     b0 = driver.bands[0]
+    if params.max_outer_iters > 0:
+        driver.begin(0, lip)
     for k in range(params.max_outer_iters):
         delta_rel = None
         if k >= 1:
-            scal, ctrl = b0.read_block()
+            scal, ctrl = b0.read_snapshot()
             trace.append(_record(*pending, scal, ctrl, b0))
             pending = None
             h_old, h_new = float(scal[b0.S_HACC]), float(scal[b0.S_HNEXT])
@@ -608,9 +643,12 @@ def run_loop(driver: BandUnwrap, c, model: ModelParams, params: IrlsParams):
         else:
             m_cg = m_history[0]
         driver.step(k, m_cg, params, lip)
+        b0.snapshot()
+        if k + 1 < params.max_outer_iters:
+            driver.begin(k + 1, lip)  # speculative: overlaps the host's budget decision
         pending = (k, m_cg, delta_rel)
     if pending is not None:
-        scal, ctrl = b0.read_block()
+        scal, ctrl = b0.read_snapshot()
         trace.append(_record(*pending, scal, ctrl, b0))
     return trace
 
@@ -631,6 +669,31 @@ def _validate_device(x_dev):
         raise ValueError("wrapped phase values must lie in [0, 2*pi)")
 
 
+def _default_peer(distributed, group):
+    """The fused peer transpose unless PU_BAND_P2P=0: always for bands in one
+    process (same device, no mapping), and under torch.distributed when the
+    backend is NCCL and every rank's GPU is on this node with peer access to
+    the others (NVSwitch); otherwise the all-to-all transposes."""
+    import os
+    env = os.environ.get("PU_BAND_P2P")
+    if env is not None:
+        return env == "1"
+    if not distributed:
+        return True
+    import torch.distributed as dist
+    torch = _torch()
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) != "nccl" or world > torch.cuda.device_count():
+        return False
+    if world == 1:
+        return True
+    cnt = torch.cuda.device_count()
+    ok = all(torch.cuda.can_device_access_peer(a, b) for a in range(cnt) for b in range(cnt) if a != b)
+    flag = torch.tensor([1 if ok else 0], device=torch.device("cuda", torch.cuda.current_device()))
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    return bool(flag.item())
+
+
 class RowSharded:
     """Band states, communicator and driver for one (N, M, dtype, tau, delta)
     on this process's device; reused across unwraps (see `get`)."""
@@ -643,7 +706,7 @@ class RowSharded:
         import torch.distributed as dist
         distributed = bands is None and dist.is_available() and dist.is_initialized()
         if peer is None:
-            peer = os.environ.get("PU_BAND_P2P") == "1"
+            peer = _default_peer(distributed, group)
         key = (n, m, dtype, float(model.tau), float(model.delta), str(device), bands, id(group) if distributed else None,
                distributed, bool(peer))
         obj = cls._cache.get(key)
@@ -778,9 +841,10 @@ def unwrap_rows(x, c: WeightField | None = None, model: ModelParams | None = Non
     reduction totals and the DCT transpose over `group` (default: world).
     Otherwise `bands` = B runs all B bands in this process on one device
     (loopback collectives) — the same decomposition, for testing.
-    `peer` (default: PU_BAND_P2P=1) fuses the DCT transpose into the row
-    kernels (stores into / loads from the other ranks' column blocks,
-    pu_set_band_peers) instead of two all-to-alls per PCG iteration.
+    `peer` fuses the DCT transpose into the row kernels (stores into / loads
+    from the other ranks' column blocks, pu_set_band_peers) instead of two
+    all-to-alls per PCG iteration; default `_default_peer` (on, unless
+    PU_BAND_P2P=0 or the ranks' GPUs lack peer access).
     Returns an UnwrapResult with the full grid on every rank when `gather`,
     else the rank's own band rows (u, vv, vh) and the trace.
     """

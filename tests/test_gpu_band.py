@@ -44,6 +44,23 @@ def test_bands_match_single_grid_fp64(shape, bands, peer):
     assert rel(res.vv, single.vv) <= 1e-8
 
 
+@pytest.mark.parametrize("peer", [False, True])
+def test_bands_eager_match_single_grid(monkeypatch, peer):
+    """The eager launch path (no CUDA graphs: how torch.distributed bands run
+    unless PU_BAND_GRAPHS=1), with the speculative start-up and the host's
+    exit polls every 16 PCG iterations, on loopback bands."""
+    from paper_2401_09961_b200 import band
+    monkeypatch.setenv("PU_BAND_GRAPHS", "0")
+    monkeypatch.setattr(band.RowSharded, "_cache", {})
+    x = _scene(96, 80)
+    single = pu.unwrap(x, dtype="fp64")
+    res = pu.unwrap_rows(x, dtype="fp64", bands=3, peer=peer)
+    assert [r.cg_iters for r in res.trace.records] == [r.cg_iters for r in single.trace.records]
+    assert [r.sufficient_decrease for r in res.trace.records] == [r.sufficient_decrease
+                                                                  for r in single.trace.records]
+    assert rel(res.u, single.u) <= 1e-9
+
+
 @pytest.mark.parametrize("name", ["noisy64", "noisy96x80", "weighted40x36", "lo0_noisy48"])
 def test_bands_match_reference(golden_unwrap, golden_meta, name):
     """north_star fp64 bar on the sharded path: u within 1e-8 of the reference's."""
