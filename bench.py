@@ -437,9 +437,12 @@ def measure_images(args, dtype, xs, rank, local_rank, world, dev, lib, with_cloc
     ws = Workspace.get(n, m, dtype, model.tau, model.delta, dev)
     x_devs = [torch.from_numpy(xi).to(dev) for xi in xs]
 
+    seq_pcg = [0]  # PCG iterations run by one_unwrap_sequential (all of the rank's images)
+
     def one_unwrap_sequential():
         for x_dev in x_devs:
             run, trace = unwrap_device(x_dev, None, model, params, -np.pi, dtype, ws)
+            seq_pcg[0] += sum(r.cg_iters for r in trace.records)
         return run, trace
 
     def one_unwrap():
@@ -499,6 +502,7 @@ def measure_images(args, dtype, xs, rank, local_rank, world, dev, lib, with_cloc
     ws.read_timing()  # drain
     torch.cuda.synchronize()
     ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    seq_pcg[0] = 0
     ev2.record()
     for _ in range(args.steps):
         one_unwrap_sequential()
@@ -520,7 +524,8 @@ def measure_images(args, dtype, xs, rank, local_rank, world, dev, lib, with_cloc
     n_outer = len(traces[-1].records)
     iter_kinds = ("K1_p_Ap_pAp", "K2a_update_norms", "K2b_row_dct", "K3_coldct_spectral", "K4_row_idct",
                   "reproject_update")
-    iter_ms = sum(per_kind[k]["total_ms"] for k in iter_kinds if k in per_kind) / max(1, args.steps * n_pcg)
+    pcg_per_step = seq_pcg[0] / args.steps  # all of the rank's images (n_img x n_pcg when they agree)
+    iter_ms = sum(per_kind[k]["total_ms"] for k in iter_kinds if k in per_kind) / max(1, seq_pcg[0])
     # per-iteration time implied by the clean timed step: step time minus the
     # (event-timed) once-per-outer-iteration kernels, over the PCG iterations
     outer_kinds = ("pcg_start", "weights_hpair", "candidate", "hpair_states", "accept_center")
@@ -531,7 +536,7 @@ def measure_images(args, dtype, xs, rank, local_rank, world, dev, lib, with_cloc
                                                       "K4_row_idct"):
             init_ms += t
     init_ms /= args.steps
-    pcg_ms_from_step = (step_ms - outer_ms - init_ms) / max(1, n_img * n_pcg)
+    pcg_ms_from_step = (step_ms - outer_ms - init_ms) / max(1, pcg_per_step)
     traffic = ncu_traffic(dom, dtype, n)
     roofline = {
         "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -577,7 +582,7 @@ def measure_images(args, dtype, xs, rank, local_rank, world, dev, lib, with_cloc
     d2h = n_img * (res.u.size + res.vv.size + res.vh.size) * e
     return {
         "value": value, "step_ms": step_ms, "instrumented_ms": instrumented_ms, "per_kind": per_kind,
-        "roofline": roofline, "n_pcg": n_pcg, "n_outer": n_outer, "F": f_out, "launches": int(launches),
+        "roofline": roofline, "n_pcg": n_pcg, "pcg_per_step": pcg_per_step, "n_outer": n_outer, "F": f_out, "launches": int(launches),
         "clocks": clocks.summary() if clocks else None, "ws": ws, "results": results,
         "e2e": {"value": world * n_img * n * m / (e2e_step / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step,
@@ -616,7 +621,7 @@ def main_images(args, rank, local_rank, world, dev, lib):
     if not args.no_nested and args.config != "c4":
         sub = measure_images(args, other, xs, rank, local_rank, world, dev, lib, with_clocks=False)
         nested = {"dtype": "f32" if other == "fp32" else "f64", "value": sub["value"], "unit": UNIT,
-                  "ms_per_step": sub["step_ms"], "pcg_iters_per_s": world * n_img * sub["n_pcg"] / (sub["step_ms"] / 1e3),
+                  "ms_per_step": sub["step_ms"], "pcg_iters_per_s": world * sub["pcg_per_step"] / (sub["step_ms"] / 1e3),
                   "roofline": sub["roofline"], "kernels": sub["per_kind"], "e2e": sub["e2e"],
                   "objective": {"F": sub["F"], "F_reference": REF_F.get(args.config)},
                   "parity": parity_block(args.config, xs, sub["results"], other) if rank == 0 else None,
@@ -652,7 +657,7 @@ def main_images(args, rank, local_rank, world, dev, lib):
             "kernel_timing": {"how": "CUDA events around every launch on its stream, second pass of the same "
                                      f"{args.steps} steps with graphs off", "ms_per_step": head["instrumented_ms"]},
             "pcg_iters_per_step": head["n_pcg"], "outer_iters_per_step": head["n_outer"],
-            "pcg_iters_per_s": world * n_img * head["n_pcg"] / (head["step_ms"] / 1e3),
+            "pcg_iters_per_s": world * head["pcg_per_step"] / (head["step_ms"] / 1e3),
             "roofline": head["roofline"],
             "kernels": head["per_kind"],
             "parity": parity,

@@ -498,10 +498,16 @@ struct Impl : HandleBase {
       const int npan = (gc.m + cols_per_cta - 1) / cols_per_cta;
       const int nfull = npan / slots * slots;
       const int nhalf = (gc.m - nfull * cols_per_cta + cols_per_cta / 2 - 1) / (cols_per_cta / 2);
-      if (col_is_static && col_fused_rt(pcol.dev.L, EM) && cols_per_cta >= 8 && nfull > 0 && npan % slots != 0 &&
-          nhalf <= slots && std::getenv("PU_COL_NOBALANCE") == nullptr) {
+      const bool balance = col_is_static && col_fused_rt(pcol.dev.L, EM) && cols_per_cta >= 8 &&
+                           std::getenv("PU_COL_NOBALANCE") == nullptr;
+      if (balance && nfull > 0 && npan % slots != 0 && nhalf <= slots) {
         col_nfull = nfull;
         col_nhalf = nhalf;
+      } else if (balance && 2 * npan <= sms) {
+        // small grids (fewer panels than half the SMs: 512² and 1024²): half
+        // panels throughout, twice the CTAs for the same columns
+        col_nfull = 0;
+        col_nhalf = (gc.m + cols_per_cta / 2 - 1) / (cols_per_cta / 2);
       }
     }
     // persistent pipelined row kernels: one row pair per iteration
