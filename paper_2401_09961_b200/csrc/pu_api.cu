@@ -420,7 +420,7 @@ struct Impl : HandleBase {
     if (band) {
       gc.n = n_glob; gc.m = b->cols; gc.ld = b->mb; gc.plane = (long long)n_glob * b->mb;
       gc.top = gc.bot = 0;
-      pk = Pack{b->nq, b->mb, (long long)n * b->mb, nullptr, (long long)b->row0};
+      pk = Pack{b->nq, b->mb, (long long)n * b->mb, nullptr, (long long)b->row0, FastDiv((unsigned)b->mb)};
       col0 = b->col0;
     }
     int rc;
@@ -1308,7 +1308,8 @@ int pu_set_band_peers(pu_handle* h, const uint64_t* col_blocks, const uint64_t* 
     I.pk.peers = reinterpret_cast<const unsigned long long*>(col_blocks);
     const int nq = I.pk.nq;
     I.push = Push{reinterpret_cast<const unsigned long long*>(back_buffers), I.g.n_glob / nq, I.g.n_glob % nq,
-                  I.pk.mb, I.col0 / I.pk.mb};
+                  I.pk.mb, I.col0 / I.pk.mb, FastDiv((unsigned)(I.g.n_glob / nq + 1)),
+                  FastDiv((unsigned)(I.g.n_glob / nq))};
   });
   return PU_OK;
 }

@@ -49,6 +49,29 @@ template <typename P>
 __device__ __forceinline__ P* sm_chk(P* p) { return p; }
 #endif
 
+// q = n / d for 0 <= n < 2^31 by a multiply-high and a shift (round-up
+// reciprocal, Granlund & Montgomery 1994): the band kernels divide column and
+// row indices by runtime block sizes once per element
+struct FastDiv {
+  unsigned d = 1, mul = 0, shr = 0;
+  FastDiv() = default;
+  __host__ explicit FastDiv(unsigned divisor) : d(divisor < 1 ? 1 : divisor) {
+    if (d == 1) return;
+    unsigned l = 0;
+    while ((1u << l) < d) ++l;  // ceil(log2 d)
+    const unsigned p = 31 + l;
+    mul = (unsigned)(((1ull << p) + d - 1) / d);
+    shr = p - 32;
+  }
+  __host__ __device__ __forceinline__ unsigned div(unsigned n) const {
+#ifdef __CUDA_ARCH__
+    return d == 1 ? n : __umulhi(n, mul) >> shr;
+#else
+    return d == 1 ? n : (unsigned)(((unsigned long long)n * mul) >> 32) >> shr;
+#endif
+  }
+};
+
 struct Grid {
   int n;            // rows (N)
   int m;            // cols (M)

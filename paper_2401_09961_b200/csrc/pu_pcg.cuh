@@ -89,6 +89,7 @@ struct Push {
   const unsigned long long* backs;  // device: every rank's back-buffer address
   int base, extra;                  // row bands: rows_r = base + (r < extra)
   int mb, q;                        // chunk width; this rank's chunk index
+  FastDiv bigd, based;              // i / (base + 1), i / base
 };
 
 // destination row pointer of global row i
@@ -97,9 +98,9 @@ __device__ __forceinline__ T* push_row(const Push& ps, int i) {
   const int big = ps.base + 1, cut = ps.extra * big;
   int r, ir, rows;
   if (i < cut) {
-    r = i / big; ir = i - r * big; rows = big;
+    r = (int)ps.bigd.div((unsigned)i); ir = i - r * big; rows = big;
   } else {
-    r = ps.extra + (i - cut) / ps.base; ir = i - cut - (r - ps.extra) * ps.base; rows = ps.base;
+    r = ps.extra + (int)ps.based.div((unsigned)(i - cut)); ir = i - cut - (r - ps.extra) * ps.base; rows = ps.base;
   }
   return reinterpret_cast<T*>(__ldg(ps.backs + r)) + (long long)ps.q * rows * ps.mb + (long long)ir * ps.mb;
 }

@@ -156,6 +156,7 @@ struct Pack {
   long long chunk;
   const unsigned long long* peers;  // device array of nq block addresses, or null
   long long row0;                   // this band's first global row
+  FastDiv mbd;                      // k / mb
 };
 
 // pl.stage1 (rows too long for two staged rows next to the FFT buffer, e.g.
@@ -328,7 +329,7 @@ __device__ __forceinline__ void rows_pair(const Grid& g, const FftPlan<T>& pl, c
         // packed: column k of rows ia, ia + 1 -> chunk k / mb (local buffer,
         // or the owning rank's column block)
         auto at = [&](int k) -> T* {
-          const int q = k / pk.mb;
+          const int q = (int)pk.mbd.div((unsigned)k);
           T* base = pk.peers ? reinterpret_cast<T*>(__ldg(pk.peers + q)) + (pk.row0 + ia) * pk.mb
                              : out + q * pk.chunk + (long long)ia * pk.mb;
           return base + (k - q * pk.mb);

@@ -137,7 +137,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(split_threads<LH, EM
   const bool pout = !INV && pk.nq > 0, pin = INV && pk.nq > 0;
   auto at = [&](int row, int k) -> T* {  // spectrum element (row ia + row, column k)
     if (!pout) return out + oa + (long long)row * g.ld + k;
-    const int c = k / pk.mb;
+    const int c = (int)pk.mbd.div((unsigned)k);
     T* base = pk.peers ? reinterpret_cast<T*>(__ldg(pk.peers + c)) + (pk.row0 + ia + row) * pk.mb
                        : out + c * pk.chunk + (long long)(ia + row) * pk.mb;
     return base + (k - c * pk.mb);
@@ -145,7 +145,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(split_threads<LH, EM
   auto src = [&](int row, int k) -> T {
     if (row == 1 && !hasb) return (T)0;
     if (!pin) return in[oa + (long long)row * g.ld + k];
-    const int c = k / pk.mb;
+    const int c = (int)pk.mbd.div((unsigned)k);
     return in[c * pk.chunk + (long long)(ia + row) * pk.mb + (k - c * pk.mb)];
   };
   if (pl.bluestein) {  // non-smooth n <= LH: Bluestein over the cluster, CTA 0 finishes
