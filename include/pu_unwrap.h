@@ -197,8 +197,12 @@ int pu_accept_weights(pu_handle* h, const void* xa, const void* xb, const double
  * (b = build_rhs(gv, gh)) and cand = dst - (1/L) grad H(dst, w_next) from the
  * same registers, one pass over the accepted state instead of two.  The
  * start-up sums are held in the handle; ctrl is not touched until
- * pu_irls_begin_z0 finalises them.  Whole grids only (bands: pu_pcg_begin).
- * Every value is bit-identical to pu_accept_weights + pu_irls_begin. */
+ * pu_irls_begin_z0 finalises them.  Band handles: xa and xb need their ghost
+ * rows (u both ways, v from above); the sums go to the band totals (the H
+ * pair to the S_ACC row, the start-up sums to S_START's) for the all-reduce
+ * and pu_finalize, as after pu_accept_weights and pu_pcg_begin.
+ * Every value agrees with pu_accept_weights + pu_irls_begin (fp32 bitwise,
+ * fp64 to the last bits of the FMA contraction). */
 int pu_accept_weights_start(pu_handle* h, const void* xa, const void* xb, const double* sel, void* dst,
                             const void* gv, const void* gh, const void* cv, const void* ch, const void* wkv,
                             const void* wkh, void* wnv, void* wnh, void* dv, void* dh, double* out, double lipschitz,

@@ -107,7 +107,8 @@ class BandState:
         self.ld = int(self.lib.pu_pitch(h))
         z = lambda k: torch.zeros((k, self.rows + 2, self.ld), dtype=self.tdtype, device=device)  # noqa: E731
         self.S = [z(3), z(3)]
-        self.C, self.G, self.D, self.R = z(3), z(2), z(2), z(3)
+        self.Cs = [z(3), z(3)]  # candidates of even / odd outer iterations (the fused start writes k + 1's)
+        self.G, self.D, self.R = z(2), z(2), z(3)
         self.Wt = [z(2), z(2)]
         self.P = [z(3), z(3)]
         self.W, self.use_w = None, False
@@ -366,6 +367,12 @@ class BandUnwrap:
                 graphs = os.environ.get("PU_BAND_GRAPHS") == "1" and comm.dist.get_backend(comm.group) == "nccl"
         self.graphs = bool(graphs)
         self._graphs = {}
+        # acceptance fused with the next start-up (pu_accept_weights_start), as
+        # irls._fuse_start decides for whole grids: bands of >= 2048² cells
+        from .irls import FUSED_START, FUSED_START_MIN_CELLS
+        b0 = bands[0]
+        self.fuse = FUSED_START == "1" or (FUSED_START != "0" and b0.rows * b0.m >= FUSED_START_MIN_CELLS)
+        self.prestarted = False  # the last tail ran the start-up of the next iteration
         self._warm = isinstance(comm, LoopbackComm)  # nothing to initialise lazily
         self.replayed_kernels = 0  # library kernels run by graph replays (the capture counted the first)
 
@@ -396,6 +403,7 @@ class BandUnwrap:
         """x_rows[i]: fp64 device grid rows [row0, row0 + rows (+1 if not last)) of band i."""
         P = BandState.p
         self._keep = []
+        self.prestarted = False
         for b, xr in zip(self.bands, x_rows):
             b.use_w = c is not None
             if c is not None:
@@ -431,6 +439,9 @@ class BandUnwrap:
         enqueues it speculatively behind the previous iteration, before the
         host has read that iteration's scalars and applied the budget rule; it
         leaves the state untouched, so a "stop" decision just discards it."""
+        if self.prestarted:  # the previous tail's fused acceptance did it
+            self.prestarted = False
+            return
         for b in self.bands:
             b.ensure_norms(self.GRAPH_CHUNK)
         self._run(("begin",) + self._base(k, lip, 0.0), lambda: self._begin(k, lip))
@@ -443,7 +454,7 @@ class BandUnwrap:
             w = b.Wt[k & 1]
             b.call("pu_pcg_begin", None, P(cur(b)), P(cur(b)), P(b.D, 0), P(b.D, 1), P(b.R), _ptr(b.ctrl),
                    _ptr(b.norms), 0, 0.0, P(b.G, 0), P(b.G, 1), cv, ch, P(w, 0), P(w, 1), float(lip),
-                   P(b.C), b.stream())
+                   P(b.Cs[k & 1]), b.stream())
         self.comm.allreduce(self.bands, nat.SITE_START, nat.SITE_START)
 
     def step(self, k, m_cg, params: IrlsParams, lip, poll=16):
@@ -474,7 +485,9 @@ class BandUnwrap:
             nxt = min(m_cg, it + chunk)
             self._run(("iters", it, nxt) + base, lambda a=it, z=nxt: self._iters(a, z))
             it = nxt
-        self._run(("tail",) + base, lambda: self._tail(k), flips=True)
+        fuse = self.fuse and k + 1 < params.max_outer_iters
+        self._run(("tail", fuse) + base, lambda: self._tail(k, lip if fuse else None), flips=True)
+        self.prestarted = fuse
         # the first outer iteration runs eagerly: NCCL creates its
         # communicators (all-reduce, all-to-all, P2P halo) lazily on first
         # use, which cannot happen inside a stream capture
@@ -548,25 +561,39 @@ class BandUnwrap:
                        _ptr(b.ctrl), it, b.stream())
             self._dir_halo((it + 1) & 1)
 
-    def _tail(self, k):
+    def _tail(self, k, lip=None):
         """H pair (irls.py:202-205) on the proposal (= state, solved in place)
-        and the candidate, then the acceptance and the weights of k + 1."""
+        and the candidate, then the acceptance and the weights of k + 1; with
+        `lip`, fused with the start-up of k + 1 (pu_accept_weights_start: its
+        candidate into Cs[(k + 1) & 1], r0, the start-up sums into the S_START
+        totals), so begin(k + 1) has nothing left to do."""
         P = BandState.p
         cur = lambda b: b.S[b.cur]  # noqa: E731
         nxt = lambda b: b.S[1 - b.cur]  # noqa: E731
-        self.comm.halo(self.bands, [(cur, 0, "up"), (lambda b: b.C, 0, "up")])
+        cand = lambda b: b.Cs[k & 1]  # noqa: E731
+        if lip is None:
+            self.comm.halo(self.bands, [(cur, 0, "up"), (cand, 0, "up")])
+        else:  # the fused start-up's stencil reads the accepted state's rows -1 and `rows`
+            self.comm.halo(self.bands, [(cur, 0, "both"), (cur, 1, "down"), (cand, 0, "both"), (cand, 1, "down")])
         for b in self.bands:
             cv, ch = self._c(b)
             w = b.Wt[k & 1]
-            b.call("pu_hpair_states", P(cur(b)), P(b.C), P(w, 0), P(w, 1), P(b.G, 0), P(b.G, 1), cv, ch,
+            b.call("pu_hpair_states", P(cur(b)), P(cand(b)), P(w, 0), P(w, 1), P(b.G, 0), P(b.G, 1), cv, ch,
                    b.sp(b.S_HPROP), b.stream())
         self._reduce(nat.SITE_HPAIR, nat.SITE_HPAIR, _mask(nat.SITE_HPAIR), 0, -1, out_slot=BandState.S_HPROP)
         for b in self.bands:
             cv, ch = self._c(b)
             w, wn = b.Wt[k & 1], b.Wt[(k + 1) & 1]
-            b.call("pu_accept_weights", P(cur(b)), P(b.C), b.sp(b.S_MEAN), P(nxt(b)), P(b.G, 0), P(b.G, 1), cv,
-                   ch, P(w, 0), P(w, 1), P(wn, 0), P(wn, 1), P(b.D, 0), P(b.D, 1), b.sp(b.S_HACC), b.stream())
-        self._reduce(nat.SITE_ACC, nat.SITE_ACC, _mask(nat.SITE_ACC), 0, -1, out_slot=BandState.S_HACC)
+            args = (P(cur(b)), P(cand(b)), b.sp(b.S_MEAN), P(nxt(b)), P(b.G, 0), P(b.G, 1), cv, ch, P(w, 0), P(w, 1),
+                    P(wn, 0), P(wn, 1), P(b.D, 0), P(b.D, 1), b.sp(b.S_HACC))
+            if lip is None:
+                b.call("pu_accept_weights", *args, b.stream())
+            else:
+                b.call("pu_accept_weights_start", *args, float(lip), P(b.R), P(b.Cs[(k + 1) & 1]), b.stream())
+        if lip is None:
+            self._reduce(nat.SITE_ACC, nat.SITE_ACC, _mask(nat.SITE_ACC), 0, -1, out_slot=BandState.S_HACC)
+        else:  # S_ACC..S_START: the H pair and the start-up sums (finalised by the next head)
+            self._reduce(nat.SITE_ACC, nat.SITE_START, _mask(nat.SITE_ACC), 0, -1, out_slot=BandState.S_HACC)
         for b in self.bands:
             b.cur = 1 - b.cur
         self._state_halo(lambda b: b.S[b.cur], with_dv=True)

@@ -1216,13 +1216,12 @@ int pu_accept_weights_start(pu_handle* h, const void* xa, const void* xb, const 
   if (!(lipschitz > 0)) return fail(PU_ERR_ARG, "lipschitz constant must be positive");
   if (!r || !cand || !gv || !gh) return fail(PU_ERR_ARG, "r, cand, gv and gh are required");
   PU_DISPATCH(h, {
-    if (I.band) return fail(PU_ERR_ARG, "pu_accept_weights_start runs on whole grids (bands use pu_pcg_begin)");
     cudaEvent_t te_ = I.tm.begin(ST(stream));
     k_accept_start_v<T><<<I.vec_grid(), 256, 0, ST(stream)>>>(
         I.g, CP(xa), CP(xb), sel, MP(dst), CP(gv), CP(gh), CP(cv), CP(ch), CP(wkv), CP(wkh), MP(wnv), MP(wnh),
         MP(dv), MP(dh), I.rs, S_ACC, out, MP(r), (T)(-1.0 / lipschitz), MP(cand), I.held);
     PU_LAUNCH_CHECK();
-    I.held_pending = true;
+    I.held_pending = !I.band;  // bands: the start-up sums are in the totals (finalised with pu_finalize)
     I.tm.end(ST(stream), te_, TK_ACCEPT, -1);
   });
   return PU_OK;

@@ -741,6 +741,9 @@ __global__ void __launch_bounds__(256, PU_MINB_OUTER(T, 2)) k_accept_weights_v(G
 // 0.80 for the two kernels; 1 CTA/SM, 0.70 ms, is the fp64 build.  Its FMA
 // contraction differs from the two-kernel build in the last bits, so fp64
 // results agree with the unfused path to ~1e-15, not bitwise.)
+// Row bands: the neighbour rows of xa and xb are the ghost rows (exchanged
+// before the launch); the sums go to the band totals (S_ACC and S_START rows)
+// for the cross-rank all-reduce, finalised by k_finalize.
 template <typename T>
 __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) k_accept_start_v(
     Grid g, const T* __restrict__ xa, const T* __restrict__ xb, const double* sel, T* __restrict__ dst,
@@ -866,6 +869,13 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) k_accept_start_v(
   }
   double tot[9];
   if (grid_reduce<9>(acc, rs, site, tot) && threadIdx.x == 0) {
+    if (rs.dist) {  // band mode: the H-pair sums to `site`'s row, the start-up sums to S_START's
+#pragma unroll
+      for (int q = 0; q < 6; ++q) rs.dist[site * PU_MAX_SUMS + q] = tot[q];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) rs.dist[S_START * PU_MAX_SUMS + q] = tot[6 + q];
+      return;
+    }
     fin_hpair6(g, tot, out);
     held[0] = tot[6]; held[1] = tot[7]; held[2] = tot[8];
   }

@@ -61,6 +61,35 @@ def test_bands_eager_match_single_grid(monkeypatch, peer):
     assert rel(res.u, single.u) <= 1e-9
 
 
+@pytest.mark.parametrize("graphs", ["1", "0"])
+@pytest.mark.parametrize("bands,peer", [(1, True), (3, False), (4, True)])
+def test_bands_fused_start_match_single_grid(monkeypatch, bands, peer, graphs):
+    """The acceptance fused with the next start-up on bands
+    (pu_accept_weights_start on ghost rows, sums through the band totals;
+    automatic from 2048² cells per band, forced here): same trace and result
+    as the single grid, with and without captured graphs."""
+    from paper_2401_09961_b200 import band, irls
+    monkeypatch.setattr(irls, "FUSED_START", "1")
+    monkeypatch.setenv("PU_BAND_GRAPHS", graphs)
+    monkeypatch.setattr(band.RowSharded, "_cache", {})
+    x = _scene(96, 80)
+    c = pu.WeightField(np.full((95, 80), 0.8), np.full((96, 79), 1.1))
+    single = pu.unwrap(x, c, dtype="fp64")
+    res = pu.unwrap_rows(x, c, dtype="fp64", bands=bands, peer=peer)
+    solver = band.RowSharded.get(96, 80, "fp64", pu.ModelParams(), res_device(), bands, None, peer)
+    assert solver.driver.fuse
+    assert [r.cg_iters for r in res.trace.records] == [r.cg_iters for r in single.trace.records]
+    np.testing.assert_allclose([r.h_delta for r in res.trace.records], [r.h_delta for r in single.trace.records],
+                               rtol=1e-9)
+    assert rel(res.u, single.u) <= 1e-9
+    assert rel(res.vh, single.vh) <= 1e-8
+
+
+def res_device():
+    import torch
+    return torch.device("cuda", torch.cuda.current_device())
+
+
 @pytest.mark.parametrize("name", ["noisy64", "noisy96x80", "weighted40x36", "lo0_noisy48"])
 def test_bands_match_reference(golden_unwrap, golden_meta, name):
     """north_star fp64 bar on the sharded path: u within 1e-8 of the reference's."""
