@@ -308,6 +308,10 @@ int pu_dev_free(void* dev_ptr);
  * block of the outer-iteration sites (WH, HPAIR, ACC). */
 int pu_finalize(pu_handle* h, unsigned mask, int mode, int it, void* ctrl, double* res_norms, double* out,
                 double rel_tol, int max_iters, void* stream);
+/* The budget of a PCG loop whose set-up was finalised with a placeholder
+ * max_iters (the speculative start-up of row bands): ctrl->max_iters =
+ * max_iters, enqueued on `stream`. */
+int pu_set_max_iters(pu_handle* h, void* ctrl, int max_iters, void* stream);
 /* pcg.py:59-75 (+ the candidate step objective.py:118-125 when cand != NULL,
  * as in pu_irls_step).  x may alias x0.  b may be NULL when cand != NULL
  * (b = build_rhs(gv, gh) formed in the kernel, as in pu_irls_step). */

@@ -86,6 +86,7 @@ SIGNATURES = {
     "pu_dev_alloc": (_i, [_i64, ctypes.POINTER(_vp)]),
     "pu_dev_free": (_i, [_vp]),
     "pu_finalize": (_i, [_vp, ctypes.c_uint, _i, _i, _vp, _vp, _vp, _d, _i, _vp]),
+    "pu_set_max_iters": (_i, [_vp, _vp, _i, _vp]),
     "pu_pcg_begin": (_i, [_vp] + [_vp] * 8 + [_i, _d] + [_vp] * 6 + [_d, _vp, _vp]),
     "pu_pcg_residual_rows": (_i, [_vp] + [_vp] * 8 + [_i, _i, _vp]),
     "pu_pcg_update_sum": (_i, [_vp] + [_vp] * 6 + [_i, _vp]),

@@ -432,49 +432,60 @@ class BandUnwrap:
         return (k & 1, self.bands[0].cur, float(lip), float(tol), tuple(b.norms.data_ptr() for b in self.bands),
                 tuple(b.W.data_ptr() if b.use_w else 0 for b in self.bands))
 
-    def begin(self, k, lip):
-        """pcg.py:59-79 start-up of iteration k (r0 = b - A x with the
-        candidate step, objective.py:103-125) and the all-reduce of its sums.
-        It depends on neither the budget nor the tolerance, so run_loop
-        enqueues it speculatively behind the previous iteration, before the
-        host has read that iteration's scalars and applied the budget rule; it
-        leaves the state untouched, so a "stop" decision just discards it."""
-        if self.prestarted:  # the previous tail's fused acceptance did it
-            self.prestarted = False
-            return
-        for b in self.bands:
-            b.ensure_norms(self.GRAPH_CHUNK)
-        self._run(("begin",) + self._base(k, lip, 0.0), lambda: self._begin(k, lip))
+    PLACEHOLDER_ITERS = 1 << 30  # budget of the speculative set-up until pu_set_max_iters
 
-    def _begin(self, k, lip):
+    def begin(self, k, params: IrlsParams, lip):
+        """The budget-free half of iteration k, pcg.py:59-79: the start-up
+        (r0 = b - A x with the candidate step, objective.py:103-125; unless the
+        previous tail's fused acceptance ran it), the all-reduce of its sums,
+        their finalisation with a placeholder budget, z0 = M r0 and p0 = z0.
+        run_loop enqueues it speculatively behind the previous iteration,
+        before the host has read that iteration's scalars and applied the
+        budget rule (step() then sets the budget on the device); it leaves the
+        state untouched, so a "stop" decision just discards it."""
+        pre, self.prestarted = self.prestarted, False
+        tol = float(params.cg_rel_tol)
+        self._run(("begin", pre) + self._base(k, lip, tol), lambda: self._begin(k, lip, tol, pre))
+
+    def _begin(self, k, lip, tol, pre):
         P = BandState.p
         cur = lambda b: b.S[b.cur]  # noqa: E731
+        if not pre:
+            for b in self.bands:
+                cv, ch = self._c(b)
+                w = b.Wt[k & 1]
+                b.call("pu_pcg_begin", None, P(cur(b)), P(cur(b)), P(b.D, 0), P(b.D, 1), P(b.R), _ptr(b.ctrl),
+                       _ptr(b.norms), 0, 0.0, P(b.G, 0), P(b.G, 1), cv, ch, P(w, 0), P(w, 1), float(lip),
+                       P(b.Cs[k & 1]), b.stream())
+            self.comm.allreduce(self.bands, nat.SITE_START, nat.SITE_START)
+        for b in self.bands:  # the exits on ||r0|| (the budget is set by step())
+            b.call("pu_finalize", _mask(nat.SITE_START), 1, -1, _ptr(b.ctrl), _ptr(b.norms), ctypes.c_void_p(0), tol,
+                   self.PLACEHOLDER_ITERS, b.stream())
         for b in self.bands:
-            cv, ch = self._c(b)
-            w = b.Wt[k & 1]
-            b.call("pu_pcg_begin", None, P(cur(b)), P(cur(b)), P(b.D, 0), P(b.D, 1), P(b.R), _ptr(b.ctrl),
-                   _ptr(b.norms), 0, 0.0, P(b.G, 0), P(b.G, 1), cv, ch, P(w, 0), P(w, 1), float(lip),
-                   P(b.Cs[k & 1]), b.stream())
-        self.comm.allreduce(self.bands, nat.SITE_START, nat.SITE_START)
+            b.call("pu_pcg_residual_rows", None, P(b.D, 0), P(b.D, 1), P(cur(b)), P(b.R), _ptr(b.ctrl),
+                   _ptr(b.norms), b.send(), -1, 0, b.stream())
+        self._precond_tail(-1, mode=1)
+        for b in self.bands:
+            b.call("pu_pcg_rows_inv", b.send(), P(b.P[0]), P(b.P[1]), 1, _ptr(b.ctrl), -1, b.stream())
+        self._dir_halo(0)
 
     def step(self, k, m_cg, params: IrlsParams, lip, poll=16):
         """irls.py:191-215 for iteration k, after begin(k).
 
-        With graphs (the default): the rest of the set-up (z0 = M r0, p0) and
-        the first 64 PCG iterations replay as one captured CUDA graph (kernels
-        and collectives alike), every further 64 iterations as another, and
-        the H pair + acceptance as a third; the host checks the device exit
-        flag once per 64-iteration chunk and only when the budget is longer
-        than that.  Without graphs the host polls every `poll` iterations."""
-        for b in self.bands:
-            b.ensure_norms(max(m_cg, self.GRAPH_CHUNK))  # stable pointer across budgets
+        With graphs (the default): the budget and the first 64 PCG iterations
+        replay as one captured CUDA graph (kernels and collectives alike),
+        every further 64 iterations as another, and the H pair + acceptance
+        as a third; the host checks the device exit flag once per 64-iteration
+        chunk and only when the budget is longer than that.  Without graphs
+        the host polls every `poll` iterations."""
         base = self._base(k, lip, params.cg_rel_tol)
         replay = self.graphs and self._warm
         chunk = self.GRAPH_CHUNK if replay else (poll or m_cg)
         first = min(m_cg, chunk)
 
         def head():
-            self._head(k, m_cg, params)
+            for b in self.bands:
+                b.call("pu_set_max_iters", _ptr(b.ctrl), int(m_cg), b.stream())
             self._iters(0, first)
 
         self._run(("head", m_cg, first) + base, head)
@@ -518,22 +529,6 @@ class BandUnwrap:
         if flips:
             for b in self.bands:
                 b.cur = 1 - b.cur
-
-    def _head(self, k, m_cg, params: IrlsParams):
-        """pcg.py:59-79 after the start-up: the exits on ||r0||, z0 = M r0, p0 = z0."""
-        P = BandState.p
-        tol = float(params.cg_rel_tol)
-        cur = lambda b: b.S[b.cur]  # noqa: E731
-        for b in self.bands:
-            b.call("pu_finalize", _mask(nat.SITE_START), 1, -1, _ptr(b.ctrl), _ptr(b.norms), ctypes.c_void_p(0), tol,
-                   int(m_cg), b.stream())
-        for b in self.bands:
-            b.call("pu_pcg_residual_rows", None, P(b.D, 0), P(b.D, 1), P(cur(b)), P(b.R), _ptr(b.ctrl),
-                   _ptr(b.norms), b.send(), -1, 0, b.stream())
-        self._precond_tail(-1, mode=1)
-        for b in self.bands:
-            b.call("pu_pcg_rows_inv", b.send(), P(b.P[0]), P(b.P[1]), 1, _ptr(b.ctrl), -1, b.stream())
-        self._dir_halo(0)
 
     def _iters(self, it0, it1):
         """pcg.py:81-108 for iterations [it0, it1) (kernels return at once
@@ -650,8 +645,10 @@ def run_loop(driver: BandUnwrap, c, model: ModelParams, params: IrlsParams):
     m_history = [params.max_iter_cg_start]
     pending = None
     b0 = driver.bands[0]
+    for b in driver.bands:  # one allocation: the captured graphs hold its address
+        b.ensure_norms(max(params.max_cg_iters_cap, driver.GRAPH_CHUNK))
     if params.max_outer_iters > 0:
-        driver.begin(0, lip)
+        driver.begin(0, params, lip)
     for k in range(params.max_outer_iters):
         delta_rel = None
         if k >= 1:
@@ -672,7 +669,7 @@ def run_loop(driver: BandUnwrap, c, model: ModelParams, params: IrlsParams):
         driver.step(k, m_cg, params, lip)
         b0.snapshot()
         if k + 1 < params.max_outer_iters:
-            driver.begin(k + 1, lip)  # speculative: overlaps the host's budget decision
+            driver.begin(k + 1, params, lip)  # speculative: overlaps the host's budget decision
         pending = (k, m_cg, delta_rel)
     if pending is not None:
         scal, ctrl = b0.read_snapshot()

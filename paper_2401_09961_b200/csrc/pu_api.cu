@@ -718,8 +718,10 @@ struct Impl : HandleBase {
   // K4: u block of the next direction, pnew_u = beta pold_u + DCT-III rows (first: no axpy)
   int pcg_rows_inv(const T* spec_in, T* pnew, const T* pold, int first, PcgCtrl* ctrl, int it, cudaStream_t st) {
     cudaEvent_t e = tm.begin(st);
-    Pack local = pk;  // the packed rows come from the local buffer (pushed there by K3 in peer mode)
-    local.peers = nullptr;
+    // the packed rows come from the local buffer (pushed there by K3 in peer
+    // mode), this rank's own chunk from its column block (K3 left it in place)
+    Pack local = pk;
+    if (local.peers) local.own_q = col0 / pk.mb;
     PU_DCT(rows(true, st, spec_in, pnew, ctrl, pold, first, local));
     tm.end(st, e, TK_K4, it);
     return PU_OK;
@@ -1359,6 +1361,14 @@ int pu_finalize(pu_handle* h, unsigned mask, int mode, int it, void* ctrl, doubl
     k_finalize<<<1, 32, 0, ST(stream)>>>(I.g, I.rs.dist, mask, a);
     PU_LAUNCH_CHECK();
   });
+  return PU_OK;
+}
+
+int pu_set_max_iters(pu_handle* h, void* ctrl, int max_iters, void* stream) {
+  if (!h) return fail(PU_ERR_ARG, "null handle");
+  if (!ctrl || max_iters < 0) return fail(PU_ERR_ARG, "pu_set_max_iters: ctrl required, max_iters >= 0");
+  k_set_max_iters<<<1, 32, 0, ST(stream)>>>(reinterpret_cast<PcgCtrl*>(ctrl), max_iters);
+  PU_LAUNCH_CHECK();
   return PU_OK;
 }
 

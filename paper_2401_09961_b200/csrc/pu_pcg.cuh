@@ -92,9 +92,11 @@ struct Push {
   FastDiv bigd, based;              // i / (base + 1), i / base
 };
 
-// destination row pointer of global row i
+// destination row pointer of global row i: the owner's back buffer, or in
+// place (`data`, pitch ld) for this rank's own rows, which K4 reads from its
+// column block (Pack::own_q)
 template <typename T>
-__device__ __forceinline__ T* push_row(const Push& ps, int i) {
+__device__ __forceinline__ T* push_row(const Push& ps, int i, T* data, long long ld) {
   const int big = ps.base + 1, cut = ps.extra * big;
   int r, ir, rows;
   if (i < cut) {
@@ -102,6 +104,7 @@ __device__ __forceinline__ T* push_row(const Push& ps, int i) {
   } else {
     r = ps.extra + (int)ps.based.div((unsigned)(i - cut)); ir = i - cut - (r - ps.extra) * ps.base; rows = ps.base;
   }
+  if (r == ps.q) return data + (long long)i * ld;
   return reinterpret_cast<T*>(__ldg(ps.backs + r)) + (long long)ps.q * rows * ps.mb + (long long)ir * ps.mb;
 }
 
@@ -126,7 +129,7 @@ __device__ __forceinline__ void panel_store(const Grid& g, const FftPlan<T>& pl,
         o.x = a.x; o.y = -a.y;
       }
       PU_ASSERT(i < g.n && j0 + (v + 1) * VN <= g.ld && p < pl.ldseq);
-      T* row = ps.backs ? push_row<T>(ps, i) : data + (long long)i * g.ld;
+      T* row = ps.backs ? push_row<T>(ps, i, data, g.ld) : data + (long long)i * g.ld;
       *reinterpret_cast<V*>(row + j0 + v * VN) = o;
     }
   } else {
@@ -134,7 +137,7 @@ __device__ __forceinline__ void panel_store(const Grid& g, const FftPlan<T>& pl,
       const int i = e / (2 * nseq), c = e - i * (2 * nseq);
       if (c < ncols) {
         const cplx<T> v = buf[(c >> 1) * pl.ldseq + spad(mperm(i, n))];
-        T* row = ps.backs ? push_row<T>(ps, i) : data + (long long)i * g.ld;
+        T* row = ps.backs ? push_row<T>(ps, i, data, g.ld) : data + (long long)i * g.ld;
         row[j0 + c] = (c & 1) ? -v.y : v.x;
       }
     }
@@ -222,7 +225,7 @@ __device__ __forceinline__ void col_last_stage(const Grid& g, T* data, int j0, c
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = r < R / 2 ? 2 * j + 2 * r * NS : 2 * L - 1 - 2 * j - 2 * r * NS;
-        *reinterpret_cast<cplx<T>*>(push_row<T>(ps, i) + j0 + 2 * s) = mk<T>(v[r].x, -v[r].y);
+        *reinterpret_cast<cplx<T>*>(push_row<T>(ps, i, data, g.ld) + j0 + 2 * s) = mk<T>(v[r].x, -v[r].y);
       }
     } else {
       const long long ld = g.ld, step = 2LL * NS * ld;

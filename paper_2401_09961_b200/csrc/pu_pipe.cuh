@@ -157,6 +157,7 @@ struct Pack {
   const unsigned long long* peers;  // device array of nq block addresses, or null
   long long row0;                   // this band's first global row
   FastDiv mbd;                      // k / mb
+  int own_q = -1;                   // inverse (K4) in peer mode: chunk own_q is read in place from peers[own_q]
 };
 
 // pl.stage1 (rows too long for two staged rows next to the FFT buffer, e.g.
@@ -201,8 +202,9 @@ __device__ __forceinline__ void rows_pair(const Grid& g, const FftPlan<T>& pl, c
   auto fetch = [&](T* dst, int row) {  // one thread; RB bytes
     if (pin) {
       for (int q = 0; q < pk.nq; ++q) {
-        const T* src = pk.peers ? reinterpret_cast<const T*>(pk.peers[q]) + (pk.row0 + row) * pk.mb
-                                : in + q * pk.chunk + (long long)row * pk.mb;
+        const bool direct = pk.peers && (pk.own_q < 0 || q == pk.own_q);
+        const T* src = direct ? reinterpret_cast<const T*>(pk.peers[q]) + (pk.row0 + row) * pk.mb
+                              : in + q * pk.chunk + (long long)row * pk.mb;
         bulk_g2s(dst + q * pk.mb, src, pk.mb * (unsigned)sizeof(T), mbar);
       }
     } else {

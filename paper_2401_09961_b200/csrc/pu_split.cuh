@@ -146,6 +146,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(split_threads<LH, EM
     if (row == 1 && !hasb) return (T)0;
     if (!pin) return in[oa + (long long)row * g.ld + k];
     const int c = (int)pk.mbd.div((unsigned)k);
+    if (pk.peers && c == pk.own_q)  // this rank's own rows: in place in its column block
+      return reinterpret_cast<const T*>(__ldg(pk.peers + c))[(pk.row0 + ia + row) * pk.mb + (k - c * pk.mb)];
     return in[c * pk.chunk + (long long)(ia + row) * pk.mb + (k - c * pk.mb)];
   };
   if (pl.bluestein) {  // non-smooth n <= LH: Bluestein over the cluster, CTA 0 finishes
@@ -284,7 +286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(split_threads<LH, EM
     if (q == 0) {
       for (int m = threadIdx.x; m < nn; m += blockDim.x) {
         const cplx<T> x = buf[spad(mperm(m, nn))];
-        T* row = ps.backs ? push_row<T>(ps, m) : data + (long long)m * g.ld;
+        T* row = ps.backs ? push_row<T>(ps, m, data, g.ld) : data + (long long)m * g.ld;
         if (hasb) *reinterpret_cast<cplx<T>*>(row + ja) = mk<T>(x.x, -x.y);
         else row[ja] = x.x;
       }
@@ -329,7 +331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(split_threads<LH, EM
   __syncthreads();
   fft_stages_s<T, EMAX, LH, 1, 0>(buf, 0, 1, ph.stw);
   split_dit_store<T, LH>(q, pl, buf, [&](int m, cplx<T> x) {
-    T* row = ps.backs ? push_row<T>(ps, m) : data + (long long)m * g.ld;
+    T* row = ps.backs ? push_row<T>(ps, m, data, g.ld) : data + (long long)m * g.ld;
     if (hasb) *reinterpret_cast<cplx<T>*>(row + ja) = mk<T>(x.x, -x.y);
     else row[ja] = x.x;
   });
