@@ -489,13 +489,19 @@ class BandUnwrap:
             self._iters(0, first)
 
         self._run(("head", m_cg, first) + base, head)
-        it = first
+        # lagged exit polls: before enqueuing a chunk, read the exit flag left
+        # by the chunk before the previous one, so the GPU always has a chunk
+        # queued while the host waits (at most one chunk runs past the exit,
+        # its kernels returning at once)
+        it, flags = first, [self._post_flag()] if first < m_cg else []
         while it < m_cg:
-            if self._done():
+            if len(flags) >= 2 and self._flag_done(flags.pop(0)):
                 break
             nxt = min(m_cg, it + chunk)
             self._run(("iters", it, nxt) + base, lambda a=it, z=nxt: self._iters(a, z))
             it = nxt
+            if it < m_cg:
+                flags.append(self._post_flag())
         fuse = self.fuse and k + 1 < params.max_outer_iters
         self._run(("tail", fuse) + base, lambda: self._tail(k, lip if fuse else None), flips=True)
         self.prestarted = fuse
@@ -619,8 +625,29 @@ class BandUnwrap:
     def _dir_halo(self, idx):
         self.comm.halo(self.bands, [(lambda b, i=idx: b.P[i], 0, "both"), (lambda b: b.R, 1, "down")])
 
-    def _done(self):
-        return bool(self.bands[0].read_block()[1]["done"])
+    _DONE_OFFSET = 72  # byte offset of `done` in the control block (_ctrl_dtype)
+
+    def _post_flag(self):
+        """Asynchronous copy of band 0's exit flag (ctrl->done) to page-locked
+        memory, with an event behind it."""
+        torch = _torch()
+        b = self.bands[0]
+        ring = getattr(self, "_flag_ring", None)
+        if ring is None:
+            ring = self._flag_ring = [(torch.zeros(4, dtype=torch.uint8, pin_memory=True), torch.cuda.Event())
+                                      for _ in range(4)]
+            self._flag_next = 0
+        host, ev = ring[self._flag_next]
+        self._flag_next = (self._flag_next + 1) % len(ring)
+        host.copy_(b.ctrl[self._DONE_OFFSET:self._DONE_OFFSET + 4], non_blocking=True)
+        ev.record(torch.cuda.current_stream(b.device))
+        return host, ev
+
+    @staticmethod
+    def _flag_done(flag):
+        host, ev = flag
+        ev.synchronize()
+        return bool(host.numpy().view(np.int32)[0])
 
     # ---- results ---------------------------------------------------------------
     def band_arrays(self, b):

@@ -61,6 +61,24 @@ def test_bands_eager_match_single_grid(monkeypatch, peer):
     assert rel(res.u, single.u) <= 1e-9
 
 
+@pytest.mark.parametrize("graphs", ["0", "1"])
+def test_bands_long_budget_exits(monkeypatch, graphs):
+    """Budgets longer than a poll chunk (16 eager / 64 captured PCG
+    iterations) that converge before they end: the lagged exit polls stop
+    enqueueing after the device-side exit, with the single grid's trace."""
+    from paper_2401_09961_b200 import band
+    monkeypatch.setenv("PU_BAND_GRAPHS", graphs)
+    monkeypatch.setattr(band.RowSharded, "_cache", {})
+    x = _scene(96, 80)
+    prm = pu.IrlsParams(max_iter_cg_start=150, max_cg_iters_cap=300)
+    single = pu.unwrap(x, params=prm, dtype="fp64")
+    res = pu.unwrap_rows(x, params=prm, dtype="fp64", bands=2, peer=True)
+    iters = [r.cg_iters for r in res.trace.records]
+    assert iters == [r.cg_iters for r in single.trace.records]
+    assert any(16 < i < r.m_cg for i, r in zip(iters, res.trace.records))  # an exit inside a later chunk
+    assert rel(res.u, single.u) <= 1e-9
+
+
 @pytest.mark.parametrize("graphs", ["1", "0"])
 @pytest.mark.parametrize("bands,peer", [(1, True), (3, False), (4, True)])
 def test_bands_fused_start_match_single_grid(monkeypatch, bands, peer, graphs):
