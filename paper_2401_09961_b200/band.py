@@ -356,15 +356,21 @@ class BandUnwrap:
     def __init__(self, bands, comm, graphs=None):
         import os
         self.bands, self.comm = bands, comm
-        # captured CUDA graphs replay the outer iteration (kernels and loopback
-        # copies).  NCCL collectives only on request (PU_BAND_GRAPHS=1): with
-        # them captured, the world-1 torchrun test hung on the B200 (round 2,
-        # tests/test_gpu_dist1.py), so torch.distributed bands launch eagerly
+        # captured CUDA graphs replay the outer iteration (kernels, loopback
+        # copies, NCCL all-reduces and halo sends/receives).  Under
+        # torch.distributed only with the fused peer transpose: capturing the
+        # NCCL all-to-all of the other mode hung the world-1 torchrun test on
+        # the B200 (tests/test_gpu_dist1.py, peer 0), so that mode launches
+        # eagerly.  PU_BAND_GRAPHS=0 / 1 forces either.
         if graphs is None:
-            if isinstance(comm, LoopbackComm):
-                graphs = os.environ.get("PU_BAND_GRAPHS", "1") != "0"
+            env = os.environ.get("PU_BAND_GRAPHS")
+            if env is not None:
+                graphs = env != "0" and (isinstance(comm, LoopbackComm)
+                                         or comm.dist.get_backend(comm.group) == "nccl")
+            elif isinstance(comm, LoopbackComm):
+                graphs = True
             else:
-                graphs = os.environ.get("PU_BAND_GRAPHS") == "1" and comm.dist.get_backend(comm.group) == "nccl"
+                graphs = comm.dist.get_backend(comm.group) == "nccl" and all(b.peer for b in bands)
         self.graphs = bool(graphs)
         self._graphs = {}
         # acceptance fused with the next start-up (pu_accept_weights_start), as

@@ -20,7 +20,10 @@ spec = pu.SceneSpec("gaussian-bumps", 96, 80, 10.0, 6.0, 5)
 x = pu.add_phase_noise(pu.wrap_scene(pu.generate_scene(spec)), 0.7, 105)
 single = pu.unwrap(x, dtype="fp64")
 res = pu.unwrap_rows(x, dtype="fp64", peer=peer)
+from paper_2401_09961_b200 import band  # noqa: E402
+solver = band.RowSharded.get(96, 80, "fp64", pu.ModelParams(), torch.device("cuda", local), None, None, peer)
 report = {
+    "graphs": bool(solver.driver.graphs), "replayed": int(solver.driver.replayed_kernels),
     "world": dist.get_world_size(),
     "same_counts": [r.cg_iters for r in res.trace.records] == [r.cg_iters for r in single.trace.records],
     "u_rel": float(np.linalg.norm(res.u - single.u) / np.linalg.norm(single.u)),

@@ -47,8 +47,8 @@ def test_bands_match_single_grid_fp64(shape, bands, peer):
 @pytest.mark.parametrize("peer", [False, True])
 def test_bands_eager_match_single_grid(monkeypatch, peer):
     """The eager launch path (no CUDA graphs: how torch.distributed bands run
-    unless PU_BAND_GRAPHS=1), with the speculative start-up and the host's
-    exit polls every 16 PCG iterations, on loopback bands."""
+    with the all-to-all transposes), with the speculative start-up and the
+    host's exit polls every 16 PCG iterations, on loopback bands."""
     from paper_2401_09961_b200 import band
     monkeypatch.setenv("PU_BAND_GRAPHS", "0")
     monkeypatch.setattr(band.RowSharded, "_cache", {})

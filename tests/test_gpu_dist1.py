@@ -31,7 +31,8 @@ def _port():
 @pytest.mark.parametrize("peer", ["0", "1"])
 def test_nccl_rows(tmp_path, peer, world):
     """world 1 always; world 2/4/8 run when that many GPUs are visible (one
-    rank per GPU, NCCL collectives captured in the per-budget CUDA graphs)."""
+    rank per GPU; with the peer transpose the NCCL collectives are captured in
+    the per-budget CUDA graphs)."""
     import torch
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
@@ -43,3 +44,7 @@ def test_nccl_rows(tmp_path, peer, world):
     rep = json.loads(out.read_text())
     assert rep["world"] == world and rep["same_counts"] and rep["shapes_ok"]
     assert rep["u_rel"] <= (1e-12 if world == 1 else 1e-9)
+    # the fused peer transpose replays captured graphs (NCCL all-reduces and
+    # halos inside); the all-to-all mode launches eagerly
+    assert rep["graphs"] == (peer == "1")
+    assert (rep["replayed"] > 0) == (peer == "1")
