@@ -17,7 +17,9 @@
 namespace pu {
 
 #define PU_FFT_MAX_STAGES 20
+#ifndef PU_PANEL_COLS
 #define PU_PANEL_COLS 4  // columns per CTA of the column-transform kernel (2 packed sequences)
+#endif
 
 // Complex values per thread of one FFT stage (the largest radix): 16 in fp32;
 // in fp64 PU_F64_EMAX (8: radix-8 stages at <= 64 registers; 16: radix-16
