@@ -222,8 +222,8 @@ __device__ __forceinline__ void pcg_r_body(const Grid& g, const T* __restrict__ 
       s.ur = ldg_or0(p + o + 4, j0 + 4 < g.m);
       Q4<T> au, av, ah;
       apply4<T>(g, i, j0, s, d1, d2, au, av, ah);
-      Q4<T> xu = ld4(x + o), xv = ld4(x + o + P), xh = ld4(x + o + 2 * P);
-      ru = ld4(r + o); rv = ld4(r + o + P); rh = ld4(r + o + 2 * P);
+      Q4<T> xu = ldx4(x + o), xv = ldx4(x + o + P), xh = ldx4(x + o + 2 * P);
+      ru = ldx4(r + o); rv = ldx4(r + o + P); rh = ldx4(r + o + 2 * P);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {  // pcg.py:90-91
         xu.a[k] = add_rn(xu.a[k], mul_rn(alpha, s.u.a[k]));
@@ -237,7 +237,7 @@ __device__ __forceinline__ void pcg_r_body(const Grid& g, const T* __restrict__ 
       st4(r + o + P, rv); st4(r + o + 2 * P, rh);
       if (!SUBMEAN) st4(r + o, ru);
     } else {
-      ru = ld4(r + o); rv = ld4(r + o + P); rh = ld4(r + o + 2 * P);
+      ru = ldx4(r + o); rv = ldx4(r + o + P); rh = ldx4(r + o + 2 * P);
     }
     if (SUBMEAN) {  // pcg.py:92-93
 #pragma unroll
@@ -294,8 +294,8 @@ __device__ __forceinline__ void pcg_upd_sum_body(const Grid& g, const T* __restr
     s.ur = ldg_or0(p + o + 4, j0 + 4 < g.m);
     Q4<T> au, av, ah;
     apply4<T>(g, i, j0, s, d1, d2, au, av, ah);
-    Q4<T> xu = ld4(x + o), xv = ld4(x + o + P), xh = ld4(x + o + 2 * P);
-    Q4<T> ru = ld4(r + o), rv = ld4(r + o + P), rh = ld4(r + o + 2 * P);
+    Q4<T> xu = ldx4(x + o), xv = ldx4(x + o + P), xh = ldx4(x + o + 2 * P);
+    Q4<T> ru = ldx4(r + o), rv = ldx4(r + o + P), rh = ldx4(r + o + 2 * P);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       xu.a[k] = add_rn(xu.a[k], mul_rn(alpha, s.u.a[k]));
