@@ -12,5 +12,6 @@ timeout 1500 python bench.py --config c4 --steps 3 --warmup 3 --no-cpu-baseline 
 timeout 1500 python bench.py --config c4 --dtype fp32 --steps 3 --warmup 3 --no-cpu-baseline --no-nested > gpurun_out/fin_c4_fp32.json 2> gpurun_out/fin_c4_fp32.err
 timeout 900 python bench.py --bands 1 --steps 5 --warmup 3 > gpurun_out/fin_rows1.json 2> gpurun_out/fin_rows1.err
 timeout 900 python bench.py --bands 1 --dtype fp32 --steps 5 --warmup 3 > gpurun_out/fin_rows1_fp32.json 2> gpurun_out/fin_rows1_fp32.err
+timeout 900 python bench.py --bands 2 --steps 5 --warmup 3 > gpurun_out/fin_rows2.json 2> gpurun_out/fin_rows2.err
 timeout 1700 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/fin_reference.json 2> gpurun_out/fin_reference.err
 ls -la gpurun_out/fin_*
