@@ -198,15 +198,31 @@ class Workspace:
             self._bufs[key] = t
         return t
 
+    UPLOAD_CHUNKS = 8
+
     def upload_grid(self, x):
-        """Host (numpy / CPU tensor) fp64 grid -> device, through pinned staging."""
+        """Host (numpy / CPU tensor) fp64 grid -> device, through pinned
+        staging in row chunks: the host copy of chunk i + 1 overlaps the
+        H2D copy of chunk i."""
         torch = _torch()
         src = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)) if isinstance(x, np.ndarray) else x
-        if not src.is_pinned():
-            stage = self.pinned("x_in", tuple(src.shape), torch.float64)
-            stage.copy_(src)  # multi-threaded host copy
-            src = stage
-        return src.to(self.device, non_blocking=True)
+        if src.is_pinned() or src.dim() != 2:
+            return src.to(self.device, non_blocking=True)
+        src = src.to(torch.float64).contiguous()
+        stage = self.pinned("x_in", tuple(src.shape), torch.float64)
+        ev = self._bufs.get(("ev", "x_in"))
+        if ev is not None:
+            ev.synchronize()  # the previous upload's copies out of the staging buffer are done
+        dst = torch.empty(tuple(src.shape), dtype=torch.float64, device=self.device)
+        rows = int(src.shape[0])
+        step = max(1, -(-rows // self.UPLOAD_CHUNKS))
+        for a in range(0, rows, step):
+            b = min(rows, a + step)
+            stage[a:b].copy_(src[a:b])  # multi-threaded host copy
+            dst[a:b].copy_(stage[a:b], non_blocking=True)
+        ev = self._bufs[("ev", "x_in")] = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        return dst
 
     def download_system(self, x, out=None):
         """Device system vector -> fresh host fp64 numpy (u, vv, vh).
