@@ -227,26 +227,12 @@ class Workspace:
     def download_system(self, x, out=None):
         """Device system vector -> fresh host fp64 numpy (u, vv, vh).
 
-        Default: the compact blocks are widened to fp64 on the device
-        (pu_unpack) and copied straight into fresh page-locked arrays (torch's
-        caching host allocator reuses the blocks of results the caller has
-        dropped), so the link's DMA writes the result and no host copy
-        follows; the arrays are ordinary numpy arrays whose memory happens to
-        be pinned.  With `out` (preallocated fp64 arrays): the blocks move in
-        the handle's dtype through persistent pinned buffers, then one
-        multi-threaded host copy widens them into `out`."""
+        The compact blocks move in the handle's dtype through persistent
+        pinned buffers (full link bandwidth; half the bytes in fp32 mode),
+        then one multi-threaded host copy widens them into new fp64 arrays."""
         torch = _torch()
         n, m = self.n, self.m
         shapes = ((n, m), (n - 1, m), (n, m - 1))
-        if out is None:
-            pins = []
-            for idx, (r, c) in enumerate(shapes):
-                pin = torch.empty((max(r, 0), max(c, 0)), dtype=torch.float64, pin_memory=True)
-                if r > 0 and c > 0:
-                    pin.copy_(self.unpack(x[idx], r, c), non_blocking=True)
-                pins.append(pin)
-            torch.cuda.current_stream(self.device).synchronize()
-            return tuple(p.numpy() for p in pins)
         outs, events = [], []
         stream = torch.cuda.current_stream(self.device)
         for idx, (r, c) in enumerate(shapes):

@@ -439,6 +439,22 @@ def unwrap(x, c: WeightField | None = None, model: ModelParams | None = None, pa
     model = model or ModelParams()
     params = params or IrlsParams()
     _check_call(c, n, m, gradient_lo)
+    # the host is idle while the device loop runs: allocate and page in the
+    # result arrays meanwhile, so the final widening copy touches no new pages
+    import threading
+    outs = {}
+
+    def _prefault():
+        shapes = ((n, m), (n - 1, m), (n, m - 1))
+        arrs = [np.empty((max(r, 0), max(q, 0)), dtype=np.float64) for r, q in shapes]
+        for a in arrs:
+            if a.size:
+                torch.from_numpy(a).zero_()
+        outs["arrays"] = arrs
+
+    th = threading.Thread(target=_prefault, daemon=True)
+    th.start()
     run, trace = unwrap_device(x_dev, c, model, params, gradient_lo, dtype)
-    u, vv, vh = run.ws.download_system(run.state)  # fp64 straight into fresh pinned arrays
+    th.join()
+    u, vv, vh = run.ws.download_system(run.state, out=outs.get("arrays"))
     return UnwrapResult(u=u, vv=vv, vh=vh, trace=trace)
