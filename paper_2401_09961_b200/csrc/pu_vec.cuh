@@ -480,6 +480,13 @@ __device__ __forceinline__ T slack4(T c, T v, T w, T d2) {
   const T cv = c * v;
   return slack_div_p(cv * cv + d2, w) + w;
 }
+// slack4 with 1/w given (fp64: slack_div_p is a * rcp_nr(w), so this is the
+// same arithmetic; fp32 divides as slack4)
+__device__ __forceinline__ float slack4r(float c, float v, float w, float, float d2) { return slack4(c, v, w, d2); }
+__device__ __forceinline__ double slack4r(double c, double v, double w, double rw, double d2) {
+  const double cv = c * v;
+  return (cv * cv + d2) * rw + w;
+}
 
 // w = sqrt((c v)^2 + delta^2), d = c^2 / w; H(x, w_prev), H(x, w)
 template <typename T>
@@ -549,6 +556,11 @@ __global__ void __launch_bounds__(256, PU_MINB_OUTER(T, 2)) k_hpair_states_v(Gri
     Q4<T> c1 = ones4<T>(), c2 = ones4<T>();
     if (cv) { c1 = ldg4(cv + o); c2 = ldg4(ch + o); }
     const Q4<T> w1 = ldg4(wv + o), w2 = ldg4(wh + o);
+    Q4<T> r1 = w1, r2 = w2;  // 1/w, shared by both states (fp64)
+    if constexpr (sizeof(T) == 8) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) { r1.a[k] = rcp_nr(w1.a[k]); r2.a[k] = rcp_nr(w2.a[k]); }
+    }
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const T* x = s ? xb : xa;
@@ -559,8 +571,8 @@ __global__ void __launch_bounds__(256, PU_MINB_OUTER(T, 2)) k_hpair_states_v(Gri
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int j = j0 + k;
-        if (dn_ok(g, i) && j < g.m) pv += slack4(c1.a[k], vv.a[k], w1.a[k], d2);
-        if (j < g.m - 1) ph += slack4(c2.a[k], vh.a[k], w2.a[k], d2);
+        if (dn_ok(g, i) && j < g.m) pv += slack4r(c1.a[k], vv.a[k], w1.a[k], r1.a[k], d2);
+        if (j < g.m - 1) ph += slack4r(c2.a[k], vh.a[k], w2.a[k], r2.a[k], d2);
         if (j < g.m) pu += u.a[k];
       }
       acc[5 * s + 0] += (double)pv;
