@@ -870,9 +870,19 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) k_accept_start_v(
       if (hash) rhh = ((right - uo) - g2.a[k]) - s.h.a[k];
       if (j > 0) rhm = ((uo - left) - gleft) - hleft;
       const T gu = inv * ((rvm - rvv) + (rhm - rhh));
-      const T cv2 = cv ? c1.a[k] * c1.a[k] : (T)1, ch2 = cv ? c2.a[k] * c2.a[k] : (T)1;
-      const T gvv = slack_div(cv2, w1.a[k]) * s.v.a[k] - inv * rvv;
-      const T gvh = slack_div(ch2, w2.a[k]) * s.h.a[k] - inv * rhh;
+      // c^2 / w_next: in fp64 exactly the diagonal d just formed (e1, e2: the
+      // same IEEE division) wherever ov / oh use it; fp32 divides as k_pcg_start_v
+      T qv, qh;
+      if constexpr (sizeof(T) == 8) {
+        qv = e1.a[k];
+        qh = e2.a[k];
+      } else {
+        const T cv2 = cv ? c1.a[k] * c1.a[k] : (T)1, ch2 = cv ? c2.a[k] * c2.a[k] : (T)1;
+        qv = slack_div(cv2, w1.a[k]);
+        qh = slack_div(ch2, w2.a[k]);
+      }
+      const T gvv = qv * s.v.a[k] - inv * rvv;
+      const T gvh = qh * s.h.a[k] - inv * rhh;
       ou.a[k] = ok ? add_rn(uo, mul_rn(neg_inv_lip, gu)) : (T)0;
       ov.a[k] = (ok && hasb) ? add_rn(s.v.a[k], mul_rn(neg_inv_lip, gvv)) : (T)0;
       oh.a[k] = hash ? add_rn(s.h.a[k], mul_rn(neg_inv_lip, gvh)) : (T)0;
