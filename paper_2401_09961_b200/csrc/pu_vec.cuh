@@ -846,8 +846,8 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) k_accept_start_v(
       rh.a[k] = add_rn(bh, -ah.a[k]);
       pb += bu * bu + bv * bv + bh * bh;
       pr += ru.a[k] * ru.a[k] + rv.a[k] * rv.a[k] + rh.a[k] * rh.a[k];
-      const T zv = (hasb && j < g.m) ? slack_div(rv.a[k], e1.a[k] + inv) : (T)0;
-      const T zh = (j < g.m - 1) ? slack_div(rh.a[k], e2.a[k] + inv) : (T)0;
+      const T zv = (hasb && j < g.m) ? slack_div_p(rv.a[k], e1.a[k] + inv) : (T)0;
+      const T zh = (j < g.m - 1) ? slack_div_p(rh.a[k], e2.a[k] + inv) : (T)0;
       prz += rv.a[k] * zv + rh.a[k] * zh;
     }
     acc[6] += (double)pb;
