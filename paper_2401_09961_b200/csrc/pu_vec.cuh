@@ -810,15 +810,25 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) k_accept_start_v(
       const T wa = sqrt(a * a + d2), wb = sqrt(bb * bb + d2);
       w1.a[k] = okv ? wa : (T)1;
       w2.a[k] = okh ? wb : (T)1;
-      e1.a[k] = okv ? c1.a[k] * c1.a[k] / wa : (T)0;
-      e2.a[k] = okh ? c2.a[k] * c2.a[k] / wb : (T)0;
+      // fp64: one reciprocal of each new weight serves d = c^2 / w and the
+      // H(dst, w_next) slack term (reciprocal + Newton, as K1)
+      T ra = wa, rb = wb;
+      if constexpr (sizeof(T) == 8) {
+        ra = rcp_nr(wa);
+        rb = rcp_nr(wb);
+        e1.a[k] = okv ? c1.a[k] * c1.a[k] * ra : (T)0;
+        e2.a[k] = okh ? c2.a[k] * c2.a[k] * rb : (T)0;
+      } else {
+        e1.a[k] = okv ? c1.a[k] * c1.a[k] / wa : (T)0;
+        e2.a[k] = okh ? c2.a[k] * c2.a[k] / wb : (T)0;
+      }
       if (okv) {
         part[0] += slack4(c1.a[k], s.v.a[k], p1.a[k], d2);
-        part[2] += slack4(c1.a[k], s.v.a[k], wa, d2);
+        part[2] += slack4r(c1.a[k], s.v.a[k], wa, ra, d2);
       }
       if (okh) {
         part[1] += slack4(c2.a[k], s.h.a[k], p2.a[k], d2);
-        part[3] += slack4(c2.a[k], s.h.a[k], wb, d2);
+        part[3] += slack4r(c2.a[k], s.h.a[k], wb, rb, d2);
       }
     }
 #pragma unroll
