@@ -365,8 +365,10 @@ __global__ void __launch_bounds__(256, PU_MINB_OUTER(T, 2)) k_pcg_start_v(Grid g
       g1 = ldg4(ca.gv + o); g2 = ldg4(ca.gh + o);
       ga = up_ok(g, i) ? ldg4(ca.gv + o - ld) : zero4<T>();
       gl = ldg_or0(ca.gh + o - 1, j0 > 0);
-      w1 = ldg4(ca.wv + o); w2 = ldg4(ca.wh + o);
-      if (ca.cv) { c1 = ldg4(ca.cv + o); c2 = ldg4(ca.ch + o); }
+      if constexpr (sizeof(T) == 4) {  // fp64 uses the diagonal d instead
+        w1 = ldg4(ca.wv + o); w2 = ldg4(ca.wh + o);
+        if (ca.cv) { c1 = ldg4(ca.cv + o); c2 = ldg4(ca.ch + o); }
+      }
     };
     constexpr bool EARLY = sizeof(T) == 4 || RHSG;
     if constexpr (CAND && EARLY) load_cand();
@@ -424,9 +426,19 @@ __global__ void __launch_bounds__(256, PU_MINB_OUTER(T, 2)) k_pcg_start_v(Grid g
         if (hash) rhh = ((right - uo) - g2.a[k]) - s.h.a[k];
         if (j > 0) rhm = ((uo - left) - gleft) - hleft;
         const T gu = inv * ((rvm - rvv) + (rhm - rhh));
-        const T cv2 = ca.cv ? c1.a[k] * c1.a[k] : (T)1, ch2 = ca.cv ? c2.a[k] * c2.a[k] : (T)1;
-        const T gvv = slack_div(cv2, w1.a[k]) * s.v.a[k] - inv * rvv;
-        const T gvh = slack_div(ch2, w2.a[k]) * s.h.a[k] - inv * rhh;
+        // c^2 / w: in fp64 the diagonal d itself (diag_w formed it from the
+        // same weights), so the candidate needs no c or w loads
+        T qv, qh;
+        if constexpr (sizeof(T) == 8) {
+          qv = d1.a[k];
+          qh = d2.a[k];
+        } else {
+          const T cv2 = ca.cv ? c1.a[k] * c1.a[k] : (T)1, ch2 = ca.cv ? c2.a[k] * c2.a[k] : (T)1;
+          qv = slack_div(cv2, w1.a[k]);
+          qh = slack_div(ch2, w2.a[k]);
+        }
+        const T gvv = qv * s.v.a[k] - inv * rvv;
+        const T gvh = qh * s.h.a[k] - inv * rhh;
         ou.a[k] = ok ? add_rn(uo, mul_rn(ca.neg_inv_lip, gu)) : (T)0;
         ov.a[k] = (ok && hasb) ? add_rn(s.v.a[k], mul_rn(ca.neg_inv_lip, gvv)) : (T)0;
         oh.a[k] = hash ? add_rn(s.h.a[k], mul_rn(ca.neg_inv_lip, gvh)) : (T)0;
@@ -487,6 +499,10 @@ __device__ __forceinline__ double slack4r(double c, double v, double w, double r
   const double cv = c * v;
   return (cv * cv + d2) * rw + w;
 }
+// d = c^2 / w of a new weight, and 1/w for slack4r: fp64 one reciprocal +
+// Newton (rcp_nr) for both; fp32 the IEEE quotient (rw unused)
+__device__ __forceinline__ float diag_w(float c, float w, float& rw) { rw = w; return c * c / w; }
+__device__ __forceinline__ double diag_w(double c, double w, double& rw) { rw = rcp_nr(w); return c * c * rw; }
 
 // w = sqrt((c v)^2 + delta^2), d = c^2 / w; H(x, w_prev), H(x, w)
 template <typename T>
@@ -520,14 +536,16 @@ __global__ void __launch_bounds__(256, PU_MINB_OUTER(T, 3)) k_weights_hpair_v(Gr
       const T wa = sqrt(a * a + d2), wb = sqrt(b * b + d2);
       w1.a[k] = okv ? wa : (T)1;
       w2.a[k] = okh ? wb : (T)1;
-      e1.a[k] = okv ? c1.a[k] * c1.a[k] / wa : (T)0;
-      e2.a[k] = okh ? c2.a[k] * c2.a[k] / wb : (T)0;
+      T ra, rb;
+      const T da = diag_w(c1.a[k], wa, ra), db = diag_w(c2.a[k], wb, rb);
+      e1.a[k] = okv ? da : (T)0;
+      e2.a[k] = okh ? db : (T)0;
       if (okv) {
-        part[2] += slack4(c1.a[k], vv.a[k], wa, d2);
+        part[2] += slack4r(c1.a[k], vv.a[k], wa, ra, d2);
         if (hasprev) part[0] += slack4(c1.a[k], vv.a[k], p1.a[k], d2);
       }
       if (okh) {
-        part[3] += slack4(c2.a[k], vh.a[k], wb, d2);
+        part[3] += slack4r(c2.a[k], vh.a[k], wb, rb, d2);
         if (hasprev) part[1] += slack4(c2.a[k], vh.a[k], p2.a[k], d2);
       }
     }
@@ -714,15 +732,17 @@ __global__ void __launch_bounds__(256, PU_MINB_OUTER(T, 2)) k_accept_weights_v(G
       const T wa = sqrt(a * a + d2), wb = sqrt(bb * bb + d2);
       w1.a[k] = okv ? wa : (T)1;
       w2.a[k] = okh ? wb : (T)1;
-      e1.a[k] = okv ? c1.a[k] * c1.a[k] / wa : (T)0;
-      e2.a[k] = okh ? c2.a[k] * c2.a[k] / wb : (T)0;
+      T ra, rb;
+      const T da = diag_w(c1.a[k], wa, ra), db = diag_w(c2.a[k], wb, rb);
+      e1.a[k] = okv ? da : (T)0;
+      e2.a[k] = okh ? db : (T)0;
       if (okv) {
         part[0] += slack4(c1.a[k], vv.a[k], p1.a[k], d2);
-        part[2] += slack4(c1.a[k], vv.a[k], wa, d2);
+        part[2] += slack4r(c1.a[k], vv.a[k], wa, ra, d2);
       }
       if (okh) {
         part[1] += slack4(c2.a[k], vh.a[k], p2.a[k], d2);
-        part[3] += slack4(c2.a[k], vh.a[k], wb, d2);
+        part[3] += slack4r(c2.a[k], vh.a[k], wb, rb, d2);
       }
     }
 #pragma unroll
@@ -811,17 +831,11 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) k_accept_start_v(
       w1.a[k] = okv ? wa : (T)1;
       w2.a[k] = okh ? wb : (T)1;
       // fp64: one reciprocal of each new weight serves d = c^2 / w and the
-      // H(dst, w_next) slack term (reciprocal + Newton, as K1)
-      T ra = wa, rb = wb;
-      if constexpr (sizeof(T) == 8) {
-        ra = rcp_nr(wa);
-        rb = rcp_nr(wb);
-        e1.a[k] = okv ? c1.a[k] * c1.a[k] * ra : (T)0;
-        e2.a[k] = okh ? c2.a[k] * c2.a[k] * rb : (T)0;
-      } else {
-        e1.a[k] = okv ? c1.a[k] * c1.a[k] / wa : (T)0;
-        e2.a[k] = okh ? c2.a[k] * c2.a[k] / wb : (T)0;
-      }
+      // H(dst, w_next) slack term (reciprocal + Newton, as K1; diag_w)
+      T ra, rb;
+      const T da = diag_w(c1.a[k], wa, ra), db = diag_w(c2.a[k], wb, rb);
+      e1.a[k] = okv ? da : (T)0;
+      e2.a[k] = okh ? db : (T)0;
       if (okv) {
         part[0] += slack4(c1.a[k], s.v.a[k], p1.a[k], d2);
         part[2] += slack4r(c1.a[k], s.v.a[k], wa, ra, d2);
