@@ -29,6 +29,9 @@
 #define PU_OUTER64_MINB 2
 #endif
 #define PU_MINB_OUTER(T, N) (sizeof(T) == 4 ? (N) : PU_OUTER64_MINB)
+#ifndef PU_F64_RSQRT_W
+#define PU_F64_RSQRT_W 1
+#endif
 
 namespace pu {
 
@@ -827,13 +830,29 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) k_accept_start_v(
       const int j = j0 + k;
       const bool okv = hasb && j < g.m, okh = j < g.m - 1;
       const T a = c1.a[k] * s.v.a[k], bb = c2.a[k] * s.h.a[k];
+#if PU_F64_RSQRT_W
+      // fp64: w = x rsqrt(x) and 1/w = rsqrt(x) from one reciprocal square
+      // root (profiles/r02_ab_rsqrt.txt: 504 -> 490 us; PU_F64_RSQRT_W=0 for
+      // the sqrt + reciprocal form)
+      T wa, wb, ra, rb, da, db;
+      if constexpr (sizeof(T) == 8) {
+        const T xa = a * a + d2, xb = bb * bb + d2;
+        ra = rsqrt(xa); rb = rsqrt(xb);
+        wa = xa * ra; wb = xb * rb;
+        da = c1.a[k] * c1.a[k] * ra; db = c2.a[k] * c2.a[k] * rb;
+      } else {
+        wa = sqrt(a * a + d2); wb = sqrt(bb * bb + d2);
+        da = diag_w(c1.a[k], wa, ra); db = diag_w(c2.a[k], wb, rb);
+      }
+#else
       const T wa = sqrt(a * a + d2), wb = sqrt(bb * bb + d2);
-      w1.a[k] = okv ? wa : (T)1;
-      w2.a[k] = okh ? wb : (T)1;
       // fp64: one reciprocal of each new weight serves d = c^2 / w and the
       // H(dst, w_next) slack term (reciprocal + Newton, as K1; diag_w)
       T ra, rb;
       const T da = diag_w(c1.a[k], wa, ra), db = diag_w(c2.a[k], wb, rb);
+#endif
+      w1.a[k] = okv ? wa : (T)1;
+      w2.a[k] = okh ? wb : (T)1;
       e1.a[k] = okv ? da : (T)0;
       e2.a[k] = okh ? db : (T)0;
       if (okv) {
